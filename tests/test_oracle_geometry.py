@@ -1,0 +1,222 @@
+"""Pins of the oracle's level sets, sides, crossings and normals,
+and of the manufactured data families (P:40-41 jump problem, configs 1-4)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from paper_2210_14907_b200 import inputs
+
+SPEC = json.load(open(os.path.join(GOLDEN, "spec_vectors.json")))
+
+
+def _sphere_cfg(beta=(1.0, 10.0)):
+    cfg = inputs.config("c2")
+    cfg["beta"] = beta
+    return cfg
+
+
+def test_spec_sphere_vectors(orc):
+    pb, _ = orc.from_config(_sphere_cfg())
+    g = SPEC["geometry"]
+    for v in g["phi"]:
+        assert orc.phi(pb, v["x"]) == v["phi"]
+    for v in g["side"]:
+        assert orc.side(pb, v["x"]) == v["side"]
+    for v in g["normal"]:
+        assert np.allclose(orc.normal(pb, v["x"]), v["n"], atol=v["tol"])
+    for v in g["crossing"]:
+        c = orc.crossing(pb, v["a"], v["b"])
+        if v["theta"] is None:
+            assert c is None
+        else:
+            th, xg, n = c
+            assert abs(th - v["theta"]) < 1e-12
+            assert np.allclose(xg, v["location"], atol=1e-12)
+            assert np.allclose(n, v["normal"], atol=1e-12)
+
+
+def test_spec_plane_crossing_exact(orc):
+    v = SPEC["geometry"]["plane_crossing"]
+    cfg = inputs.config("c1")
+    cfg.update(ls_kind=inputs.LS_PLANE, plane=(v["plane_n"], v["plane_c"]))
+    pb, _ = orc.from_config(cfg)
+    th, xg, n = orc.crossing(pb, v["a"], v["b"])
+    assert th == float(np.float32(v["theta"]))
+    assert np.array_equal(n, [1.0, 0.0, 0.0])
+
+
+def test_constant_level_set_is_degenerate(orc):
+    cfg = inputs.config("c1")
+    cfg.update(ls_kind=inputs.LS_PLANE, plane=((0.0, 0.0, 0.0), 0.3))   # phi == -0.3
+    pb, _ = orc.from_config(cfg)
+    with pytest.raises(RuntimeError):
+        orc.normal(pb, [0.1, 0.2, 0.3])
+
+
+def _geoms():
+    c4 = inputs.config("c4")
+    c3 = inputs.config("c3")
+    # two heavily overlapping spheres: exercises the union rule of G8
+    ov = inputs.config("c2")
+    ov.update(centers=np.array([[0.0, 0, 0], [0.3, 0.05, 0]], np.float32),
+              radii=np.array([0.4, 0.35], np.float32))
+    return {"sphere": _sphere_cfg(), "union32": c4, "star": c3, "overlap": ov}
+
+
+@pytest.mark.parametrize("name", ["sphere", "union32", "star", "overlap"])
+def test_crossing_symmetry_and_bisection(orc, name):
+    """theta(a->b) + theta(b->a) = 1; closed form agrees with an
+    independent bisection of the side function (G8)."""
+    cfg = _geoms()[name]
+    pb, _ = orc.from_config(cfg)
+    rng = np.random.default_rng(11)
+    found = 0
+    tries = 0
+    while found < 60 and tries < 200000:
+        tries += 1
+        a = rng.uniform(-0.9, 0.9, 3)
+        b = a.copy()
+        b[rng.integers(3)] += rng.choice([-1, 1]) * 0.05
+        c1 = orc.crossing(pb, a, b)
+        if c1 is None:
+            continue
+        found += 1
+        c2 = orc.crossing(pb, b, a)
+        assert abs(c1[0] + c2[0] - 1.0) < 1e-10
+        tb = orc.crossing_bisect(pb, a, b)
+        assert abs(c1[0] - tb) < 1e-10
+        assert abs(np.linalg.norm(c1[2]) - 1.0) < 1e-12
+        # the normal points from Omega- to Omega+ 
+        x = c1[1]
+        assert orc.side(pb, x + 1e-7 * c1[2]) == 1 and orc.side(pb, x - 1e-7 * c1[2]) == 0
+    assert found == 60
+
+
+def test_sphere_crossing_location_on_sphere(orc):
+    pb, _ = orc.from_config(_sphere_cfg())
+    rng = np.random.default_rng(3)
+    n = 0
+    while n < 100:
+        a = rng.uniform(-0.7, 0.7, 3)
+        b = a.copy()
+        b[rng.integers(3)] += 0.1
+        c = orc.crossing(pb, a, b)
+        if c:
+            n += 1
+            assert abs(np.linalg.norm(c[1]) - 0.5) < 1e-12
+
+
+def test_star_polynomial_matches_trigonometric_form(orc):
+    """G13: the recurrence form equals r - r0 - amp sin(5 t) cos(3 p)."""
+    cfg = inputs.config("c3")
+    pb, _ = orc.from_config(cfg)
+    r0, amp, m, n = [float(np.float32(v)) for v in cfg["star"]]
+    rng = np.random.default_rng(0)
+    for x in rng.uniform(-1, 1, size=(1000, 3)):
+        r = np.linalg.norm(x)
+        th = np.arccos(x[2] / r)
+        ph = np.arctan2(x[1], x[0])
+        want = r - r0 - amp * np.sin(m * th) * np.cos(n * ph)
+        assert abs(orc.phi(pb, x) - want) < 1e-13
+    assert orc.phi(pb, [0, 0, 0]) == -r0
+    assert abs(orc.phi(pb, [0, 0, 0.7]) - (0.7 - r0)) < 1e-15
+
+
+def test_union_is_min_of_sphere_distances(orc):
+    cfg = inputs.config("c4")
+    pb, _ = orc.from_config(cfg)
+    c = cfg["centers"].astype(np.float64)
+    r = cfg["radii"].astype(np.float64)
+    rng = np.random.default_rng(1)
+    for x in rng.uniform(-1, 1, size=(500, 3)):
+        want = np.min(np.linalg.norm(x - c, axis=1) - r)
+        assert abs(orc.phi(pb, x) - want) < 1e-15
+
+
+# ---------------- manufactured data ----------------
+
+def _fd_laplacian(fn, x, e=1e-3):
+    x = np.asarray(x, float)
+    lap = 0.0
+    for d in range(3):
+        v = []
+        for k in (-2, -1, 0, 1, 2):
+            y = x.copy()
+            y[d] += k * e
+            v.append(fn(y))
+        lap += (-v[0] + 16 * v[1] - 30 * v[2] + 16 * v[3] - v[4]) / (12 * e * e)
+    return lap
+
+
+def _fd_grad(fn, x, e=1e-5):
+    x = np.asarray(x, float)
+    g = np.zeros(3)
+    for d in range(3):
+        yp, ym = x.copy(), x.copy()
+        yp[d] += e
+        ym[d] -= e
+        g[d] = (fn(yp) - fn(ym)) / (2 * e)
+    return g
+
+
+@pytest.mark.parametrize("name,k", [("c1", 0.0), ("c2", 0.0), ("c2", 2.5), ("c1", 1.5)])
+def test_source_is_k_u_minus_div_beta_grad_u(orc, name, k):
+    """f_s = k_s u_s - beta_s Lap u_s, checked by 4th-order finite differences
+    of the exact solution; the exact gradient is checked by central differences."""
+    cfg = inputs.config(name)
+    cfg["k"] = (k, 2 * k)
+    pb, _ = orc.from_config(cfg)
+    rng = np.random.default_rng(2)
+    for x in rng.uniform(-0.9, 0.9, size=(40, 3)):
+        for s in (0, 1):
+            u = lambda y: orc.exact(pb, s, y)[0]
+            lap = _fd_laplacian(u, x)
+            kk = float(np.float32(cfg["k"][s]))
+            bb = float(np.float32(cfg["beta"][s]))
+            want = kk * u(x) - bb * lap
+            assert abs(orc.f(pb, s, x) - want) < 1e-6 * max(1.0, abs(want))
+            assert np.allclose(orc.exact(pb, s, x)[1], _fd_grad(u, x), atol=1e-8)
+
+
+def test_jump_data_of_config2_pair(orc):
+    """alpha = [u] = u+ - u-, sigma = beta+ d_n u+ - beta- d_n u- on the sphere (G12)."""
+    pb, _ = orc.from_config(_sphere_cfg())
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        v = rng.normal(size=3)
+        x = 0.5 * v / np.linalg.norm(v)
+        n = orc.normal(pb, x)
+        up = np.sin(x.sum())
+        um = np.exp(x[0]) * np.cos(x[1]) * x[2]
+        assert abs(orc.alpha(pb, x) - (up - um)) < 1e-14
+        dn_p = _fd_grad(lambda y: orc.exact(pb, 1, y)[0], x) @ n
+        dn_m = _fd_grad(lambda y: orc.exact(pb, 0, y)[0], x) @ n
+        assert abs(orc.sigma(pb, x, n) - (10.0 * dn_p - 1.0 * dn_m)) < 1e-8
+
+
+def test_gaussian_charge_is_normalised(orc):
+    """G13: the smoothed charge integrates to q (midpoint rule, spectrally accurate)."""
+    cfg = inputs.config("c3")
+    cfg.update(charges_q=np.array([1.0], np.float32), charges_c=np.zeros((1, 3), np.float32))
+    pb, _ = orc.from_config(cfg)
+    s = float(np.float32(0.02))
+    hq = 0.25 * s
+    ax = np.arange(-28, 29) * hq
+    tot = 0.0
+    for x in ax:
+        for y in ax:
+            for z in ax:
+                tot += orc.f(pb, 0, [x, y, z])
+    assert abs(tot * hq**3 - 1.0) < 1e-6
+
+
+def test_boundary_data_is_side_exact_solution(orc):
+    pb, _ = orc.from_config(_sphere_cfg())
+    x = [1.0, 0.2, -0.3]
+    assert orc.g(pb, x) == pytest.approx(np.sin(0.9), abs=1e-15)
+    cfg3 = inputs.config("c3")
+    pb3, _ = orc.from_config(cfg3)
+    assert orc.g(pb3, x) == 0.0                                           # G13: u = 0 on faces
