@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark of the NBM loss+grad training step (BASELINE.json metric: collocation-point
+loss+grad evaluations/s and steps/s at 1/2/4/8 B200, % roofline).
+
+One step = sample (interior + boundary, K1) -> nbm_loss_grad (K2 classify/assemble,
+K3 fused MLP fwd/residual/bwd, K4r reduce) -> all-reduce of [grad, loss] (N > 1) ->
+nbm_adam_step (K4a).  Default workload: BASELINE config 2 (configs[1]): sphere interface,
+two 3-64-64-64-1 tanh fp32 MLPs, 2^18 interior + 2^15 boundary points per GPU (weak
+scaling), h = 1/128.  Synthetic seeded data (the paper's dragon scan is not available).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ... (NCCL all-reduce).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2210_14907_b200 import dp, inputs  # noqa: E402
+
+FP32_FFMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FFMA lanes x 2 x max clock
+
+
+def mlp_macs(sizes):
+    """(forward MACs, forward+backward MACs) per evaluation, algorithmic."""
+    fwd = sum(sizes[l - 1] * sizes[l] for l in range(1, len(sizes)))
+    dh = sum(sizes[l - 1] * sizes[l] for l in range(2, len(sizes)))
+    return fwd, 2 * fwd + dh
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(cfg, seconds_hint=15.0):
+    """The oracle as it stands (fp64, OpenMP over all host cores) on a bounded sample of
+    the same workload; returns pts/s (loss+grad evaluations per second)."""
+    import oracle
+    pb, ar = oracle.from_config(cfg)
+    th = oracle.init_params(ar, 0)
+    n = 1 << 10
+    nb = max(1, n * cfg["Nb"] // cfg["N"])
+    while True:
+        pts = oracle.sample(0, 0, 0, 0, n, cfg["H"])
+        bpts = oracle.sample(1, 0, 0, 0, nb, cfg["H"])
+        t0 = time.perf_counter()
+        oracle.loss_grad(pb, ar, th, pts, bpts, cfg["h"], n_glob=cfg["N"], nb_glob=cfg["Nb"])
+        dt = time.perf_counter() - t0
+        if dt > seconds_hint / 4 or n >= cfg["N"]:
+            break
+        n = min(cfg["N"], n * max(2, int(seconds_hint / 4 / max(dt, 1e-3))))
+        nb = max(1, n * cfg["Nb"] // cfg["N"])
+    return {"value": n / dt, "unit": "pts/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{n} interior + {nb} boundary points of {cfg['name']} (fp64 loss+grad, "
+                      f"{dt:.2f} s)"}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle (CPU, fp64) as the reference arm, rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    pb, ar = oracle.from_config(cfg)
+    th = oracle.init_params(ar, 0).astype("float64")
+    m = th * 0
+    v = th * 0
+    n = 1 << 12
+    nb = max(1, n * cfg["Nb"] // cfg["N"])
+    times = []
+    for it in range(args.warmup + args.steps):
+        pts = oracle.sample(0, 0, it, 0, n, cfg["H"])
+        bpts = oracle.sample(1, 0, it, 0, nb, cfg["H"])
+        t0 = time.perf_counter()
+        _, _, g, _ = oracle.loss_grad(pb, ar, th, pts, bpts, cfg["h"], n_glob=n, nb_glob=nb)
+        th, m, v = oracle.adam(th, m, v, g, it + 1, lr=cfg["lr"])
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    val = n * len(times) / tot
+    line = {"metric": "collocation-pt loss+grad evals/sec", "value": val, "unit": "pts/s",
+            "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "points_per_step": n, "boundary_per_step": nb,
+                       "note": "bounded sample of the workload; oracle on host cores"},
+            "cpu_baseline": {"value": val, "unit": "pts/s", "cores": oracle.num_threads(),
+                             "kind": "oracle", "sample": f"{n} + {nb} points per step"},
+            "e2e": {"value": val, "unit": "pts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--width", type=int, default=None)
+    ap.add_argument("--impl", default="nbm", choices=["nbm", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--points", type=int, default=None, help="override interior points per GPU")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank, world, local = dp.env_rank_world()
+    cfg = inputs.config(args.config, width=args.width)
+    if args.points:
+        cfg["N"] = args.points
+        cfg["Nb"] = max(1, args.points // 8)
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2210_14907_b200 import nbm
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N, Nb = cfg["N"], cfg["Nb"]                 # per GPU (weak scaling)
+    Ng, Nbg = N * world, Nb * world
+    s = nbm.Solver(cfg, device=local, max_points=max(N, Nb))
+    s.init_params(0)
+    pts = torch.empty(N, 3, device="cuda")
+    bpts = torch.empty(Nb, 3, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > L2 (126 MB)
+    stream = torch.cuda.current_stream()
+
+    def step(it):
+        s.sample(nbm.POINTS_INTERIOR, 0, it, rank * N, N, pts)
+        s.sample(nbm.POINTS_BOUNDARY, 0, it, rank * Nb, Nb, bpts)
+        s.loss_grad(pts, bpts, n_global=Ng, nb_global=Nbg)
+        dp.allreduce_sum_(s.gbuf)
+        s.adam_step(lr=cfg["lr"])
+
+    for it in range(args.warmup):
+        step(it)
+    torch.cuda.synchronize()
+    st = s.status()
+    if st != 0:
+        raise RuntimeError(f"device status {st} after warm-up")
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    nbm.nbm_timing_enable(s.h, True)
+    nbm.nbm_timing_read(s.h)
+    launches_per_step = None
+    barrier()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()                        # L2 flush between timed steps (not timed)
+            ev[k][0].record(stream)
+            step(args.warmup + k)
+            ev[k][1].record(stream)
+            if launches_per_step is None:
+                launches_per_step = nbm.nbm_last_launch_count(s.h) + 3   # + 2 samples + Adam
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    mlp_ms, lg_ms, calls = nbm.nbm_timing_read(s.h)
+    nbm.nbm_timing_enable(s.h, False)
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms, lg_ms], device="cuda", dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        tot_ms, lg_ms_max = t.tolist()
+    else:
+        lg_ms_max = lg_ms
+
+    # ---- e2e: same step through the public API with host buffers (H2D of the step's
+    # points from pinned memory, D2H of the loss) ----
+    e2e = None
+    if not args.no_e2e:
+        hp = torch.empty(N, 3, pin_memory=True)
+        hb = torch.empty(Nb, 3, pin_memory=True)
+        s.sample(nbm.POINTS_INTERIOR, 1, 0, rank * N, N, pts)
+        s.sample(nbm.POINTS_BOUNDARY, 1, 0, rank * Nb, Nb, bpts)
+        hp.copy_(pts)
+        hb.copy_(bpts)
+        hl = torch.empty(1, pin_memory=True)
+        ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        barrier()
+        for k in range(args.steps):
+            flush.zero_()
+            ee[k][0].record(stream)
+            pts.copy_(hp, non_blocking=True)
+            bpts.copy_(hb, non_blocking=True)
+            s.loss_grad(pts, bpts, n_global=Ng, nb_global=Nbg)
+            dp.allreduce_sum_(s.gbuf)
+            s.adam_step(lr=cfg["lr"])
+            hl.copy_(s.loss, non_blocking=True)
+            ee[k][1].record(stream)
+        barrier()
+        e_ms = sum(a.elapsed_time(b) for a, b in ee)
+        if world > 1:
+            t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            e_ms = t.item()
+        e2e = {"value": Ng * args.steps / (e_ms / 1e3), "unit": "pts/s",
+               "h2d_bytes_per_step": 12 * (N + Nb), "d2h_bytes_per_step": 4}
+    st = s.status()
+    if st != 0:
+        raise RuntimeError(f"device status {st} after the timed region")
+
+    if rank != 0:
+        if world > 1:
+            tdist.destroy_process_group()
+        return
+
+    peaks, src = load_peaks()
+    fwd, fb = mlp_macs(cfg["sizes"])
+    flop_launch = 2.0 * fb * (7 * N + Nb)          # algorithmic, per fused-MLP launch
+    mlp_avg_s = mlp_ms / max(calls, 1) / 1e3
+    if cfg["prec"] == inputs.PREC_FP32:
+        peak = FP32_FFMA_TFLOPS
+        bound, peak_note = "alu", "fp32 FFMA: 148 SM x 128 lanes x 2 FLOP x 1965 MHz (derived, DESIGN.md)"
+    else:
+        peak = peaks["bf16_tflops"]
+        bound, peak_note = "tensor", f"bf16 dense, {src} (MEASURED_PEAKS.json)"
+    achieved = flop_launch / mlp_avg_s / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{cfg['name']}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("bytes_per_launch")
+    val = Ng * args.steps / (tot_ms / 1e3)
+    line = {
+        "metric": "collocation-pt loss+grad evals/sec (full training step)",
+        "value": val, "unit": "pts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps, "steps_per_sec": 1e3 * args.steps / tot_ms,
+        "loss_grad_pts_per_sec": Ng * calls / (lg_ms_max / 1e3) if calls else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg["prec"] == 0 else "bf16",
+        "data": "synthetic (seeded Philox lattice points; manufactured two-phase Poisson)",
+        "config": {"workload": cfg["name"], "points_per_gpu": N, "boundary_per_gpu": Nb,
+                   "global_points": Ng, "mlp": "x".join(map(str, cfg["sizes"])), "n_nets": cfg["n_nets"],
+                   "h": cfg["h"], "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
+        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_mlp_fp32 (fused fwd/residual/bwd)",
+                     "flop_per_launch": flop_launch, "avg_launch_ms": mlp_avg_s * 1e3,
+                     "share_of_step": (mlp_ms / max(calls, 1)) / (tot_ms / args.steps), "peak_src": peak_note},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,518 @@
+// mlp_fp32.cu -- K3f: the fused MLP forward -> residual epilogue -> backward -> dW
+// kernel in IEEE fp32 on the CUDA cores (configs 1, 2, 5-fp32; G15).
+//
+// One CTA (256 threads) processes a contiguous range of 128-row tiles of the
+// segment table:
+//   * stencil tile: 18 uncrossed points x 7 stencil vertices (126 rows, arm-major:
+//     row = j*18 + p), all on one network ("neural networks can be evaluated
+//     over vertices of any discretization stencils"; P:60 one network per side);
+//   * row tile: 128 independent evaluations with an affine cotangent (boundary rows:
+//     u_bar = a (u - g); crossed rows: u_bar given by the crossed pass).
+// Per tile: layer 1 (K=3) -> hidden GEMMs (register-tiled FFMA from shared memory)
+// -> output layer -> epilogue r = u0 + chat sum_j u_j - rhs_hat (r = M^-1 A u - M^-1 b,
+// P:60), u_bar = (2/N) r chat_j -> backward GEMMs.  The hidden x hidden dW
+// accumulate in registers across all the CTA's tiles and the small
+// layers' grads in shared memory; each CTA writes one fp32 partial per network that
+// K4r sums in fixed CTA order (deterministic, G21).
+#include <math.h>
+
+#include "nbm_internal.cuh"
+
+namespace nbm {
+
+constexpr int kB = 128;        // rows per tile
+constexpr int kPT = 18;        // points per stencil tile (126 rows)
+constexpr int kThreads = 256;
+
+
+
+template <int N> struct VecT;
+template <> struct VecT<2> { using T = float2; };
+template <> struct VecT<4> { using T = float4; };
+
+__device__ __forceinline__ void ldv(const float* p, float (&v)[4]) {
+  float4 t = *reinterpret_cast<const float4*>(p);
+  v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+}
+__device__ __forceinline__ void ldv(const float* p, float (&v)[2]) {
+  float2 t = *reinterpret_cast<const float2*>(p);
+  v[0] = t.x; v[1] = t.y;
+}
+__device__ __forceinline__ void stv(float* p, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ void stv(float* p, const float (&v)[2]) {
+  *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+}
+
+template <int W, int NH>
+struct Layout {
+  static constexpr int LDA = W + 4;              // padded row stride of activations
+  static constexpr int LDW = W + 4;              // padded row stride of hidden weights
+  static constexpr int TC = W / 16;              // GEMM columns per thread (rows: 8)
+  static constexpr int DB = (W == 64) ? 4 : 2;   // dW block per thread: DB x DB
+  static constexpr int NHH = NH - 1;             // hidden x hidden layers
+  // shared-memory carve (floats)
+  static constexpr int oW1 = 0;                          // [W][3]
+  static constexpr int oB = oW1 + 4 * W;                 // [NH][W]
+  static constexpr int oWh = oB + NH * W;                // [NHH][W][LDW]
+  static constexpr int oWo = oWh + (NHH > 0 ? NHH : 0) * W * LDW;   // [W] + bo
+  static constexpr int oAct = oWo + W + 4;               // [NH][kB][LDA]
+  static constexpr int oX = oAct + NH * kB * LDA;        // [kB][4]
+  static constexpr int oU = oX + 4 * kB;                 // [kB]
+  static constexpr int oUb = oU + kB;                    // [kB]
+  static constexpr int oRed = oUb + kB;                  // [4][256]
+  static constexpr int oAW1 = oRed + 4 * kThreads;       // [W][3]
+  static constexpr int oAB = oAW1 + 4 * W;               // [NH][W]
+  static constexpr int oAWo = oAB + NH * W;              // [W] + bo
+  static constexpr int oAux = oAWo + W + 4;              // [kB]
+  static constexpr int oItem = oAux + kB;                // int [kB]
+  static constexpr int total = oItem + kB + 16;
+  static constexpr size_t bytes = sizeof(float) * total;
+  // theta offsets within one network (G17)
+  static constexpr int64_t tW1 = 0, tB1 = 3 * W;
+  __host__ __device__ static constexpr int64_t tWl(int l) { return 4 * W + (int64_t)(l - 2) * (W * W + W); }
+  __host__ __device__ static constexpr int64_t tBl(int l) { return tWl(l) + W * W; }
+  static constexpr int64_t tWo = 4 * W + (int64_t)NHH * (W * W + W);
+  static constexpr int64_t tBo = tWo + W;
+  static constexpr int64_t pnet = tBo + 1;
+};
+
+// Hout[b][n] = tanh(sum_k Hin[b][k] W[n][k] + bias[n]); thread = 8 rows x TC cols.
+template <int W, int NH>
+__device__ __forceinline__ void fwd_gemm(const float* __restrict__ Hin, float* __restrict__ Hout,
+                                         const float* __restrict__ Ws, const float* __restrict__ bias,
+                                         int tid) {
+  using L = Layout<W, NH>;
+  constexpr int TC = L::TC;
+  const int tr = tid & 15, tc = tid >> 4;
+  float acc[8][TC];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < TC; ++c) acc[i][c] = 0.0f;
+#pragma unroll 2
+  for (int k = 0; k < W; k += 4) {
+    float a[8][4], w[TC][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ldv(Hin + (tr + 16 * i) * L::LDA + k, a[i]);
+#pragma unroll
+    for (int c = 0; c < TC; ++c) ldv(Ws + (tc * TC + c) * L::LDW + k, w[c]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(a[i][q], w[c][q], acc[i][c]);
+  }
+  float bv[TC];
+#pragma unroll
+  for (int c = 0; c < TC; ++c) bv[c] = bias[tc * TC + c];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float o[TC];
+#pragma unroll
+    for (int c = 0; c < TC; ++c) o[c] = tanhf(acc[i][c] + bv[c]);
+    stv(Hout + (tr + 16 * i) * L::LDA + tc * TC, o);
+  }
+}
+
+// In place: H[b][i] <- (sum_o G[b][o] W[o][i]) * (1 - H[b][i]^2)   (delta_{l-1}, tanh')
+template <int W, int NH>
+__device__ __forceinline__ void bwd_gemm(const float* __restrict__ G, float* __restrict__ H,
+                                         const float* __restrict__ Ws, int tid) {
+  using L = Layout<W, NH>;
+  constexpr int TC = L::TC;
+  const int tr = tid & 15, tc = tid >> 4;
+  float acc[8][TC];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < TC; ++c) acc[i][c] = 0.0f;
+#pragma unroll 2
+  for (int o = 0; o < W; o += 4) {
+    float g[8][4], w[4][TC];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ldv(G + (tr + 16 * i) * L::LDA + o, g[i]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ldv(Ws + (o + q) * L::LDW + tc * TC, w[q]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(g[i][q], w[q][c], acc[i][c]);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float hv[TC], o[TC];
+    float* p = H + (tr + 16 * i) * L::LDA + tc * TC;
+    ldv(p, hv);
+#pragma unroll
+    for (int c = 0; c < TC; ++c) o[c] = acc[i][c] * (1.0f - hv[c] * hv[c]);
+    stv(p, o);
+  }
+}
+
+// dW[o][i] += sum_b G[b][o] H[b][i]; thread owns a DB x DB block (registers).
+template <int W, int NH>
+__device__ __forceinline__ void dw_gemm(const float* __restrict__ G, const float* __restrict__ H,
+                                        float (&dW)[Layout<W, NH>::DB * Layout<W, NH>::DB], int tid) {
+  using L = Layout<W, NH>;
+  constexpr int DB = L::DB;
+  const int to = tid >> 4, ti = tid & 15;
+#pragma unroll 4
+  for (int b = 0; b < kB; ++b) {
+    float g[DB], hv[DB];
+    ldv(G + b * L::LDA + to * DB, g);
+    ldv(H + b * L::LDA + ti * DB, hv);
+#pragma unroll
+    for (int a = 0; a < DB; ++a)
+#pragma unroll
+      for (int c = 0; c < DB; ++c) dW[a * DB + c] = fmaf(g[a], hv[c], dW[a * DB + c]);
+  }
+}
+
+// acc[col] += sum_b X[b][col] (fixed order: contiguous row ranges, then parts in order)
+template <int W, int NH>
+__device__ __forceinline__ void colsum(const float* __restrict__ X, float* __restrict__ acc,
+                                       float* __restrict__ red, int tid) {
+  using L = Layout<W, NH>;
+  constexpr int parts = kThreads / W, per = kB / parts;
+  const int col = tid % W, part = tid / W;
+  float s = 0.0f;
+  for (int r = part * per; r < (part + 1) * per; ++r) s += X[r * L::LDA + col];
+  red[part * W + col] = s;
+  __syncthreads();
+  if (tid < W) {
+    float t = 0.0f;
+    for (int p = 0; p < parts; ++p) t += red[p * W + tid];
+    acc[tid] += t;
+  }
+  __syncthreads();
+}
+
+template <int W, int NH, bool TRAIN>
+__global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
+  using L = Layout<W, NH>;
+  constexpr int NHH = L::NHH;
+  constexpr int DB = L::DB;
+  extern __shared__ __align__(16) float sm[];
+  float* sW1 = sm + L::oW1;
+  float* sBias = sm + L::oB;
+  float* sWh = sm + L::oWh;
+  float* sWo = sm + L::oWo;
+  float* sAct = sm + L::oAct;
+  float* sX = sm + L::oX;
+  float* sU = sm + L::oU;
+  float* sUb = sm + L::oUb;
+  float* sRed = sm + L::oRed;
+  float* sAW1 = sm + L::oAW1;
+  float* sAB = sm + L::oAB;
+  float* sAWo = sm + L::oAWo;
+  float* sAux = sm + L::oAux;
+  int* sItem = reinterpret_cast<int*>(sm + L::oItem);
+  __shared__ int segTiles[kNumSeg + 1], segCnt[kNumSeg], segStart[kNumSeg];
+
+  const int tid = threadIdx.x;
+  if (tid < kNumSeg) {
+    int c = prm.counts[prm.cnt_slot[tid]];
+    segCnt[tid] = c;
+    segStart[tid] = prm.start_slot[tid] >= 0 ? prm.counts[prm.start_slot[tid]] : 0;
+    int per = prm.seg.kind[tid] == kSegStencil ? kPT : kB;
+    segTiles[tid] = (c + per - 1) / per;
+  }
+  __syncthreads();
+  int total = 0;
+  int firstTile[kNumSeg + 1];
+#pragma unroll
+  for (int s = 0; s < kNumSeg; ++s) { firstTile[s] = total; total += segTiles[s]; }
+  firstTile[kNumSeg] = total;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int t0 = (int)((int64_t)total * cta / G), t1 = (int)((int64_t)total * (cta + 1) / G);
+
+  float dWh[NHH > 0 ? NHH : 1][DB * DB];
+  double lossAcc = 0.0;
+  int curNet = -1;
+  bool touched[2] = {false, false};
+
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int l = 0; l < (NHH > 0 ? NHH : 1); ++l)
+#pragma unroll
+      for (int e = 0; e < DB * DB; ++e) dWh[l][e] = 0.0f;
+    for (int i = tid; i < 4 * W + NH * W + W + 4; i += kThreads) sAW1[i] = 0.0f;   // AW1, AB, AWo contiguous
+  };
+  auto flush = [&](int net) {
+    float* out = prm.part + ((int64_t)net * G + cta) * prm.p_stride;
+    const int to = tid >> 4, ti = tid & 15;
+#pragma unroll
+    for (int l = 0; l < NHH; ++l)
+#pragma unroll
+      for (int a = 0; a < DB; ++a) {
+        float v[DB];
+#pragma unroll
+        for (int c = 0; c < DB; ++c) v[c] = dWh[l][a * DB + c];
+        stv(out + L::tWl(l + 2) + (int64_t)(to * DB + a) * W + ti * DB, v);
+      }
+    for (int i = tid; i < 3 * W; i += kThreads) out[L::tW1 + i] = sAW1[i];
+    for (int i = tid; i < W; i += kThreads) {
+      out[L::tB1 + i] = sAB[i];
+      for (int l = 2; l <= NH; ++l) out[L::tBl(l) + i] = sAB[(l - 1) * W + i];
+      out[L::tWo + i] = sAWo[i];
+    }
+    if (tid == 0) out[L::tBo] = sAWo[W];
+    touched[net] = true;
+  };
+  auto load_net = [&](int net) {
+    const float* th = prm.theta + (int64_t)net * prm.p_net;
+    for (int i = tid; i < 3 * W; i += kThreads) sW1[i] = th[L::tW1 + i];
+    for (int i = tid; i < W; i += kThreads) {
+      sBias[i] = th[L::tB1 + i];
+      for (int l = 2; l <= NH; ++l) sBias[(l - 1) * W + i] = th[L::tBl(l) + i];
+      sWo[i] = th[L::tWo + i];
+    }
+    if (tid == 0) sWo[W] = th[L::tBo];
+    for (int l = 0; l < NHH; ++l)
+      for (int i = tid; i < W * W; i += kThreads)
+        sWh[l * W * L::LDW + (i / W) * L::LDW + (i % W)] = th[L::tWl(l + 2) + i];
+  };
+
+  int seg = 0;
+  for (int t = t0; t < t1; ++t) {
+    while (t >= firstTile[seg + 1]) ++seg;
+    const int kind = prm.seg.kind[seg], net = prm.seg.net[seg];
+    const int lt = t - firstTile[seg];
+    const int per = kind == kSegStencil ? kPT : kB;
+    const int first = lt * per;
+    const int nvalid = min(per, segCnt[seg] - first);
+    if (net != curNet) {
+      __syncthreads();
+      if (TRAIN && curNet >= 0) flush(curNet);
+      __syncthreads();
+      load_net(net);
+      if (TRAIN) zero_acc();
+      curNet = net;
+    }
+    // ---- gather the tile's items and rows (x, aux) ----
+    const int* items = prm.seg.items[seg] + segStart[seg];
+    if (tid < per) {
+      int it = tid < nvalid ? items[first + tid] : -1;
+      sItem[tid] = it;
+      float a = 0.0f;
+      if (it >= 0) a = prm.aux_by_item[seg] ? prm.seg.aux[seg][it] : prm.seg.aux[seg][segStart[seg] + first + tid];
+      sAux[tid] = a;
+    }
+    __syncthreads();
+    if (tid < kB) {
+      float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
+      if (kind == kSegStencil) {
+        const int j = tid / kPT, p = tid - j * kPT;
+        if (j < 7 && p < nvalid) {
+          const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[p];
+          x0 = src[0]; x1 = src[1]; x2 = src[2];
+          if (j > 0) {   // arms +x, -x, +y, -y, +z, -z (exact on the lattice)
+            const float hs = (j & 1) ? prm.h : -prm.h;
+            if (j <= 2) x0 = __fadd_rn(x0, hs); else if (j <= 4) x1 = __fadd_rn(x1, hs); else x2 = __fadd_rn(x2, hs);
+          }
+        }
+      } else if (tid < nvalid) {
+        const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[tid];
+        x0 = src[0]; x1 = src[1]; x2 = src[2];
+      }
+      sX[4 * tid + 0] = x0; sX[4 * tid + 1] = x1; sX[4 * tid + 2] = x2;
+    }
+    __syncthreads();
+    // ---- layer 1 (K = 3) on CUDA cores ----
+    {
+      const int col = tid % W, r0 = tid / W;
+      constexpr int step = kThreads / W;
+      const float w0 = sW1[3 * col], w1 = sW1[3 * col + 1], w2 = sW1[3 * col + 2], bb = sBias[col];
+      for (int r = r0; r < kB; r += step) {
+        float z = fmaf(w2, sX[4 * r + 2], fmaf(w1, sX[4 * r + 1], fmaf(w0, sX[4 * r], bb)));
+        sAct[r * L::LDA + col] = tanhf(z);
+      }
+    }
+    __syncthreads();
+    // ---- hidden GEMMs ----
+#pragma unroll
+    for (int l = 0; l < NHH; ++l) {
+      fwd_gemm<W, NH>(sAct + l * kB * L::LDA, sAct + (l + 1) * kB * L::LDA, sWh + l * W * L::LDW,
+                      sBias + (l + 1) * W, tid);
+      __syncthreads();
+    }
+    // ---- output layer u = wo . h_NH + bo ----
+    float* hTop = sAct + (NH - 1) * kB * L::LDA;
+    {
+      const int r = tid >> 1, half = tid & 1;
+      float s = 0.0f;
+      for (int k = half * (W / 2); k < (half + 1) * (W / 2); ++k) s = fmaf(sWo[k], hTop[r * L::LDA + k], s);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      if (half == 0) sU[r] = s + sWo[W];
+    }
+    __syncthreads();
+    if (!TRAIN) {
+      if (tid < nvalid) prm.u_out[sItem[tid]] = sU[tid];
+      __syncthreads();
+      continue;
+    }
+    // ---- residual epilogue -> cotangents (S4) ----
+    if (kind == kSegStencil) {
+      if (tid < kPT) {
+        float r = 0.0f;
+        if (tid < nvalid) {
+          const float chat = prm.seg.chat[seg];
+          float acc = sU[tid];
+#pragma unroll
+          for (int j = 1; j < 7; ++j) acc = fmaf(chat, sU[j * kPT + tid], acc);
+          r = acc - sAux[tid];
+          lossAcc += 0.5 * (double)prm.two_over_n * (double)r * (double)r;   // r^2 / N
+        }
+        const float rc = prm.two_over_n * r;
+        sUb[tid] = rc;
+        const float rj = rc * prm.seg.chat[seg];
+#pragma unroll
+        for (int j = 1; j < 7; ++j) sUb[j * kPT + tid] = rj;
+      } else if (tid >= 7 * kPT && tid < kB) {
+        sUb[tid] = 0.0f;
+      }
+    } else if (tid < kB) {
+      float ub = 0.0f;
+      if (tid < nvalid) {
+        if (kind == kSegBRows) {
+          const float e = sU[tid] - sAux[tid];
+          ub = prm.seg.a[seg] * e;
+          lossAcc += 0.5 * (double)prm.seg.a[seg] * (double)e * (double)e;
+        } else {
+          ub = sAux[tid];
+        }
+      }
+      sUb[tid] = ub;
+    }
+    __syncthreads();
+    // ---- backward (S5) ----
+    {  // output layer: dWo += sum_b ub h_NH, dbo += sum_b ub; then G_NH in place
+      const int col = tid % W, part = tid / W;
+      constexpr int parts = kThreads / W, per = kB / parts;
+      float s = 0.0f;
+      for (int r = part * per; r < (part + 1) * per; ++r) s = fmaf(sUb[r], hTop[r * L::LDA + col], s);
+      sRed[part * W + col] = s;
+      if (tid < 32) {
+        float b = sUb[tid] + sUb[tid + 32] + sUb[tid + 64] + sUb[tid + 96];
+        for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+        if (tid == 0) sAWo[W] += b;
+      }
+      __syncthreads();
+      if (tid < W) {
+        float t = 0.0f;
+        for (int p = 0; p < parts; ++p) t += sRed[p * W + tid];
+        sAWo[tid] += t;
+      }
+      const float wo = sWo[col];
+      for (int r = part; r < kB; r += parts) {
+        float hv = hTop[r * L::LDA + col];
+        hTop[r * L::LDA + col] = sUb[r] * wo * (1.0f - hv * hv);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int l = NHH - 1; l >= 0; --l) {   // hidden layer (l+2): G in act[l+1], h in act[l]
+      float* Gl = sAct + (l + 1) * kB * L::LDA;
+      float* Hp = sAct + l * kB * L::LDA;
+      dw_gemm<W, NH>(Gl, Hp, dWh[l], tid);
+      colsum<W, NH>(Gl, sAB + (l + 1) * W, sRed, tid);   // db (contains __syncthreads)
+      bwd_gemm<W, NH>(Gl, Hp, sWh + l * W * L::LDW, tid);
+      __syncthreads();
+    }
+    {  // layer 1: dW1[n][c] += sum_b G1[b][n] x[b][c]; db1 += sum_b G1[b][n]
+      const int col = tid % W, part = tid / W;
+      constexpr int parts = kThreads / W, per = kB / parts;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, sb = 0.f;
+      for (int r = part * per; r < (part + 1) * per; ++r) {
+        const float g = sAct[r * L::LDA + col];
+        s0 = fmaf(g, sX[4 * r], s0);
+        s1 = fmaf(g, sX[4 * r + 1], s1);
+        s2 = fmaf(g, sX[4 * r + 2], s2);
+        sb += g;
+      }
+      sRed[(0 * parts + part) * W + col] = s0;
+      sRed[(1 * parts + part) * W + col] = s1;
+      sRed[(2 * parts + part) * W + col] = s2;
+      sRed[(3 * parts + part) * W + col] = sb;
+      __syncthreads();
+      if (tid < W) {
+        float t0v = 0.f, t1v = 0.f, t2v = 0.f, tb = 0.f;
+        for (int p = 0; p < parts; ++p) {
+          t0v += sRed[(0 * parts + p) * W + tid];
+          t1v += sRed[(1 * parts + p) * W + tid];
+          t2v += sRed[(2 * parts + p) * W + tid];
+          tb += sRed[(3 * parts + p) * W + tid];
+        }
+        sAW1[3 * tid] += t0v;
+        sAW1[3 * tid + 1] += t1v;
+        sAW1[3 * tid + 2] += t2v;
+        sAB[tid] += tb;
+      }
+      __syncthreads();
+    }
+  }
+  if (!TRAIN) return;
+  __syncthreads();
+  if (curNet >= 0) flush(curNet);
+  if (tid < 2) prm.touched[tid * G + cta] = touched[tid] ? 1 : 0;
+  // CTA loss: fixed-order block reduction of the per-thread partials
+  for (int o = 16; o; o >>= 1) lossAcc += __shfl_xor_sync(0xffffffffu, lossAcc, o);
+  __shared__ double wl[kThreads / 32];
+  if ((tid & 31) == 0) wl[tid >> 5] = lossAcc;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += wl[w];
+    prm.lpart[cta] = s;
+  }
+}
+
+template <int W, int NH, bool TRAIN>
+static cudaError_t launch_t(const MlpParams& p, int grid, cudaStream_t s) {
+  using L = Layout<W, NH>;
+  auto kern = k_mlp_fp32<W, NH, TRAIN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<grid, kThreads, L::bytes, s>>>(p);
+  return cudaGetLastError();
+}
+
+int mlp_fp32_supported(int width, int n_hidden) {
+  return (width == 32 || width == 64) && n_hidden >= 1 && n_hidden <= 4;
+}
+
+template <bool TRAIN>
+static cudaError_t dispatch(int W, int NH, const MlpParams& p, int grid, cudaStream_t s) {
+  if (W == 64) {
+    switch (NH) {
+      case 1: return launch_t<64, 1, TRAIN>(p, grid, s);
+      case 2: return launch_t<64, 2, TRAIN>(p, grid, s);
+      case 3: return launch_t<64, 3, TRAIN>(p, grid, s);
+      case 4: return launch_t<64, 4, TRAIN>(p, grid, s);
+    }
+  } else if (W == 32) {
+    switch (NH) {
+      case 1: return launch_t<32, 1, TRAIN>(p, grid, s);
+      case 2: return launch_t<32, 2, TRAIN>(p, grid, s);
+      case 3: return launch_t<32, 3, TRAIN>(p, grid, s);
+      case 4: return launch_t<32, 4, TRAIN>(p, grid, s);
+    }
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_mlp_fp32(int width, int n_hidden, bool train, const MlpParams& p, int grid,
+                            cudaStream_t s) {
+  return train ? dispatch<true>(width, n_hidden, p, grid, s) : dispatch<false>(width, n_hidden, p, grid, s);
+}
+
+}  // namespace nbm

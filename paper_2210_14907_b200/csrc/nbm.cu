@@ -1,0 +1,512 @@
+// nbm.cu -- the C ABI of libnbm.so (include/nbm.h): descriptor validation, workspace,
+// the per-call launch sequence of the hot path, K4r gradient reduction and the
+// timing hook.  See DESIGN.md section 5 for the kernel list.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <vector>
+
+#include "nbm_internal.cuh"
+
+using namespace nbm;
+
+namespace {
+
+// counts[] slot map (device int[16]):
+//   0..5   class totals (kCls*), 6..11 class starts in list[], 12/13 crossed rows per
+//   network, 15 always zero.
+constexpr int kSlotZero = 15;
+
+thread_local std::string g_create_error;
+
+int fail(nbm_handle* h, int code, const std::string& msg) {
+  if (h) h->last_error = msg;
+  return code;
+}
+
+int cuda_fail(nbm_handle* h, cudaError_t e, const char* where) {
+  return fail(h, NBM_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+bool h_on_lattice(float h, int64_t* H) {
+  double v = (double)h * kLattice;
+  if (!(h > 0.0f) || !(h < 1.0f) || v != floor(v)) return false;
+  *H = (int64_t)v;
+  return true;
+}
+
+int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
+  if (!a || !a->sizes || a->n_layers < 3 || a->n_layers > kMaxLayers) {
+    *why = "arch: need 3..8 layer sizes [3, W, ..., W, 1]";
+    return NBM_E_INVALID_ARCH;
+  }
+  if (a->sizes[0] != 3 || a->sizes[a->n_layers - 1] != 1) {
+    *why = "arch: sizes[0] must be 3 and the last 1 (S:174)";
+    return NBM_E_INVALID_ARCH;
+  }
+  int W = a->sizes[1];
+  for (int l = 1; l < a->n_layers - 1; ++l)
+    if (a->sizes[l] != W) { *why = "arch: hidden widths must be uniform"; return NBM_E_INVALID_ARCH; }
+  if (a->n_nets != 1 && a->n_nets != 2) { *why = "arch: n_nets must be 1 or 2"; return NBM_E_INVALID_ARCH; }
+  if (a->act != NBM_ACT_TANH && a->act != NBM_ACT_SILU) { *why = "arch: bad activation"; return NBM_E_INVALID_ARCH; }
+  if (a->prec != NBM_PREC_FP32 && a->prec != NBM_PREC_BF16) { *why = "arch: bad precision"; return NBM_E_INVALID_ARCH; }
+  int nh = a->n_layers - 2;
+  bool ok = false;
+  if (a->prec == NBM_PREC_FP32 && a->act == NBM_ACT_TANH) ok = mlp_fp32_supported(W, nh);
+  if (!ok) {
+    *why = "arch: unsupported (prec, act, width, depth) combination in this build";
+    return NBM_E_INVALID_ARCH;
+  }
+  if (out) {
+    memset(out, 0, sizeof(*out));
+    out->n_layers = a->n_layers;
+    out->width = W;
+    out->n_hidden = nh;
+    out->act = a->act;
+    out->prec = a->prec;
+    out->n_nets = a->n_nets;
+    int64_t p = 0;
+    for (int l = 0; l < a->n_layers; ++l) out->sizes[l] = a->sizes[l];
+    for (int l = 1; l < a->n_layers; ++l) p += (int64_t)a->sizes[l] * a->sizes[l - 1] + a->sizes[l];
+    out->p_net = p;
+  }
+  return NBM_OK;
+}
+
+int check_problem(const nbm_problem* p, DevProblem* out, std::string* why) {
+  if (!p) { *why = "problem: null"; return NBM_E_ARG; }
+  for (int d = 0; d < 3; ++d)
+    if (p->box_lo[d] != -1.0f || p->box_hi[d] != 1.0f) { *why = "problem: box must be [-1,1]^3 (G23)"; return NBM_E_INVALID_PROBLEM; }
+  if (!(p->beta_minus > 0.0f) || !(p->beta_plus > 0.0f)) { *why = "problem: beta must be > 0 (S:236)"; return NBM_E_INVALID_PROBLEM; }
+  if (!(p->k_minus >= 0.0f) || !(p->k_plus >= 0.0f)) { *why = "problem: k must be >= 0"; return NBM_E_INVALID_PROBLEM; }
+  if (!(p->lambda_b >= 0.0f)) { *why = "problem: lambda_b must be >= 0"; return NBM_E_INVALID_PROBLEM; }
+  const nbm_levelset& ls = p->ls;
+  if (ls.kind < NBM_LS_NONE || ls.kind > NBM_LS_PLANE) { *why = "problem: bad level-set kind"; return NBM_E_INVALID_PROBLEM; }
+  if (ls.kind == NBM_LS_SPHERES) {
+    if (ls.n < 1 || ls.n > kMaxSpheres || !ls.centers || !ls.radii) { *why = "problem: spheres need 1..64 centres and radii"; return NBM_E_INVALID_PROBLEM; }
+    for (int k = 0; k < ls.n; ++k)
+      if (!(ls.radii[k] > 0.0f)) { *why = "problem: sphere radius must be > 0"; return NBM_E_INVALID_PROBLEM; }
+  }
+  if (ls.kind == NBM_LS_STAR && (ls.star_m < 0 || ls.star_m > 16 || ls.star_n < 0 || ls.star_n > 16 || !(ls.star_r0 > 0.0f))) {
+    *why = "problem: bad star parameters"; return NBM_E_INVALID_PROBLEM;
+  }
+  if (p->source < NBM_SRC_SINE3PI || p->source > NBM_SRC_GAUSS) { *why = "problem: bad source"; return NBM_E_INVALID_PROBLEM; }
+  if (p->source == NBM_SRC_GAUSS) {
+    if (p->n_charges < 0 || p->n_charges > kMaxCharges || (p->n_charges > 0 && (!p->q || !p->charge_centers)) || !(p->charge_sigma > 0.0f)) {
+      *why = "problem: bad charges"; return NBM_E_INVALID_PROBLEM;
+    }
+  }
+  if (out) {
+    memset(out, 0, sizeof(*out));
+    out->ls_kind = ls.kind;
+    if (ls.kind == NBM_LS_SPHERES) {
+      out->n_spheres = ls.n;
+      for (int k = 0; k < ls.n; ++k) {
+        for (int d = 0; d < 3; ++d) out->centers[k][d] = ls.centers[3 * k + d];
+        out->radii[k] = ls.radii[k];
+      }
+    }
+    out->star_r0 = ls.star_r0; out->star_amp = ls.star_amp;
+    out->star_m = ls.star_m; out->star_n = ls.star_n;
+    for (int d = 0; d < 3; ++d) out->plane_n[d] = ls.plane_n[d];
+    out->plane_c = ls.plane_c;
+    out->beta[0] = p->beta_minus; out->beta[1] = p->beta_plus;
+    out->k[0] = p->k_minus; out->k[1] = p->k_plus;
+    out->source = p->source;
+    if (p->source == NBM_SRC_GAUSS) {
+      out->n_charges = p->n_charges;
+      for (int k = 0; k < p->n_charges; ++k) {
+        out->q[k] = p->q[k];
+        for (int d = 0; d < 3; ++d) out->charge_centers[k][d] = p->charge_centers[3 * k + d];
+      }
+      out->charge_sigma = p->charge_sigma;
+    }
+    out->lambda_b = p->lambda_b;
+  }
+  return NBM_OK;
+}
+
+// K4r: grad[net][j] = sum over CTAs (fixed order) of the touched partials; loss = sum of
+// the CTA loss partials and the crossed rows' loss.  fp64 accumulation of fp32 partials.
+__global__ void k_reduce(const float* __restrict__ part, const int* __restrict__ touched, int G,
+                         int64_t p_net, int64_t p_stride, int n_nets, const double* __restrict__ lpart,
+                         float* __restrict__ grad, float* __restrict__ loss, int* __restrict__ err) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n_nets * p_net) {
+    int net = (int)(i / p_net);
+    int64_t j = i - net * p_net;
+    double s = 0.0;
+    for (int g = 0; g < G; ++g)
+      if (touched[net * G + g]) s += part[((int64_t)net * G + g) * p_stride + j];
+    float v = (float)s;
+    grad[i] = v;
+    if (!isfinite(v)) atomicOr(err, kErrNonfinite);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int g = 0; g <= G; ++g) s += lpart[g];
+    float v = (float)s;
+    *loss = v;
+    if (!isfinite(v)) atomicOr(err, kErrNonfinite);
+  }
+}
+
+double diag(const DevProblem& P, int s, double h) {   // d_s = k_s + 6 beta_s / h^2
+  double h2 = h * h, c0 = P.k[s];
+  for (int j = 0; j < 6; ++j) c0 += P.beta[s] / h2;
+  return c0;
+}
+
+void fill_common(const nbm_handle* h, MlpParams& p, const float* theta, float hf) {
+  memset(&p, 0, sizeof(p));
+  p.counts = h->ws.counts;
+  p.theta = theta;
+  p.p_net = h->arch.p_net;
+  p.h = hf;
+  p.part = h->ws.part;
+  p.p_stride = (h->arch.p_net + 3) & ~3ll;
+  p.touched = h->ws.touched;
+  p.lpart = h->ws.lpart;
+  for (int s = 0; s < kNumSeg; ++s) { p.cnt_slot[s] = kSlotZero; p.start_slot[s] = -1; p.seg.kind[s] = kSegXRows; }
+}
+
+}  // namespace
+
+namespace nbm {
+cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s) {
+  int64_t P = h->arch.p_net * h->arch.n_nets;
+  k_reduce<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(h->ws.part, h->ws.touched, h->ws.grid_mlp,
+                                                       h->arch.p_net, (h->arch.p_net + 3) & ~3ll,
+                                                       h->arch.n_nets, h->ws.lpart,
+                                                       grad, loss, h->ws.err);
+  return cudaGetLastError();
+}
+}  // namespace nbm
+
+extern "C" {
+
+const char* nbm_version(void) { return "nbm-b200 0.1 (sm_100a)"; }
+
+int64_t nbm_arch_param_count(const nbm_arch* arch) {
+  if (!arch || !arch->sizes || arch->n_layers < 2 || arch->n_nets < 1 || arch->n_nets > 2) return -1;
+  int64_t p = 0;
+  for (int l = 1; l < arch->n_layers; ++l) {
+    if (arch->sizes[l] <= 0 || arch->sizes[l - 1] <= 0) return -1;
+    p += (int64_t)arch->sizes[l] * arch->sizes[l - 1] + arch->sizes[l];
+  }
+  return p * arch->n_nets;
+}
+
+int nbm_check(const nbm_problem* problem, const nbm_arch* arch) {
+  std::string why;
+  int rc = check_problem(problem, nullptr, &why);
+  if (rc) return rc;
+  return check_arch(arch, nullptr, &why);
+}
+
+int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int64_t max_points,
+               nbm_handle** out) {
+  if (!out || max_points < 1 || max_points > (1ll << 27)) return NBM_E_ARG;
+  *out = nullptr;
+  std::string why;
+  DevProblem dp;
+  ArchInfo ai;
+  int rc = check_problem(problem, &dp, &why);
+  if (rc) { g_create_error = why; return rc; }
+  rc = check_arch(arch, &ai, &why);
+  if (rc) { g_create_error = why; return rc; }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { g_create_error = cudaGetErrorString(e); return NBM_E_CUDA; }
+  nbm_handle* h = new nbm_handle();
+  h->device = device;
+  h->arch = ai;
+  h->host_problem = dp;
+  h->timing = false;
+  h->timed_calls = 0;
+  h->last_launches = 0;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  Workspace& w = h->ws;
+  w.cap = max_points;
+  w.xcap = max_points;
+  int64_t items = 2 * max_points;
+  w.nblk_cls = (int)((items + 1023) / 1024);
+  w.grid_mlp = sms;
+  std::vector<void**> ptrs;
+  size_t sizes[32];
+  int k = 0;
+#define ALLOC(field, bytes) do { ptrs.push_back((void**)&(field)); sizes[k++] = (bytes); } while (0)
+  ALLOC(h->d_problem, sizeof(DevProblem));
+  ALLOC(w.cls, items);
+  ALLOC(w.aux_tmp, items * sizeof(float));
+  ALLOC(w.blk_counts, (size_t)w.nblk_cls * kNumCls * sizeof(int));
+  ALLOC(w.blk_offsets, (size_t)w.nblk_cls * kNumCls * sizeof(int));
+  ALLOC(w.counts, 16 * sizeof(int));
+  ALLOC(w.list, items * sizeof(int));
+  ALLOC(w.list_aux, items * sizeof(float));
+  ALLOC(w.xrow_x, 7 * w.xcap * 3 * sizeof(float));
+  ALLOC(w.xrow_u, 7 * w.xcap * sizeof(float));
+  ALLOC(w.xrow_cot, 7 * w.xcap * sizeof(float));
+  ALLOC(w.xrow_tag, 7 * w.xcap);
+  ALLOC(w.xrec, 8 * w.xcap * sizeof(float));
+  ALLOC(w.xlist, 2 * 7 * w.xcap * sizeof(int));
+  ALLOC(w.part, 2 * (size_t)w.grid_mlp * ((ai.p_net + 3) & ~3ll) * sizeof(float));
+  ALLOC(w.touched, 2 * (size_t)w.grid_mlp * sizeof(int));
+  ALLOC(w.lpart, ((size_t)w.grid_mlp + 1) * sizeof(double));
+  ALLOC(w.err, sizeof(int));
+#undef ALLOC
+  for (size_t i = 0; i < ptrs.size(); ++i) {
+    e = cudaMalloc(ptrs[i], sizes[i]);
+    if (e != cudaSuccess) {
+      g_create_error = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+      nbm_destroy(h);
+      return NBM_E_CUDA;
+    }
+  }
+  e = cudaMemcpy(h->d_problem, &dp, sizeof(dp), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(w.counts, 0, 16 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(w.err, 0, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(w.touched, 0, 2 * (size_t)w.grid_mlp * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(w.lpart, 0, ((size_t)w.grid_mlp + 1) * sizeof(double));
+  if (e != cudaSuccess) {
+    g_create_error = cudaGetErrorString(e);
+    nbm_destroy(h);
+    return NBM_E_CUDA;
+  }
+  *out = h;
+  return NBM_OK;
+}
+
+void nbm_destroy(nbm_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  void* ps[] = {h->d_problem, h->ws.cls, h->ws.aux_tmp, h->ws.blk_counts, h->ws.blk_offsets,
+                h->ws.counts, h->ws.list, h->ws.list_aux, h->ws.xrow_x, h->ws.xrow_u, h->ws.xrow_cot,
+                h->ws.xrow_tag, h->ws.xrec, h->ws.xlist, h->ws.part, h->ws.touched, h->ws.lpart,
+                h->ws.err};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  for (cudaEvent_t ev : h->ev) cudaEventDestroy(ev);
+  delete h;
+}
+
+int64_t nbm_param_count(const nbm_handle* h) { return h ? h->arch.p_net * h->arch.n_nets : -1; }
+
+const char* nbm_last_error(const nbm_handle* h) {
+  return h ? h->last_error.c_str() : g_create_error.c_str();
+}
+
+int nbm_status(nbm_handle* h, void* stream) {
+  if (!h) return NBM_E_ARG;
+  cudaSetDevice(h->device);
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(h, e, "nbm_status");
+  int word = 0;
+  e = cudaMemcpy(&word, h->ws.err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(h->ws.err, 0, sizeof(int));
+  if (e != cudaSuccess) return cuda_fail(h, e, "nbm_status");
+  if (word & kErrOutOfDomain) return fail(h, NBM_E_OUT_OF_DOMAIN, "an arm p +- h e_d left the box (S:259)");
+  if (word & kErrDegenerate) return fail(h, NBM_E_DEGENERATE, "degenerate level-set gradient at a crossing (S:117)");
+  if (word & kErrNonfinite) return fail(h, NBM_E_NONFINITE, "non-finite loss or gradient (S:367)");
+  return NBM_OK;
+}
+
+int nbm_init_params(nbm_handle* h, uint64_t seed, float* theta_dev, void* stream) {
+  if (!h || !theta_dev) return NBM_E_ARG;
+  cudaSetDevice(h->device);
+  cudaError_t e = launch_init_params(h->arch, seed, theta_dev, (cudaStream_t)stream);
+  return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_init_params");
+}
+
+int nbm_sample(nbm_handle* h, uint64_t seed, uint64_t step, int kind, int64_t first_index,
+               int64_t n, float h_cell, float* pts_dev, void* stream) {
+  if (!h || (n > 0 && !pts_dev) || n < 0 || first_index < 0) return fail(h, NBM_E_ARG, "nbm_sample: bad arguments");
+  if (kind != NBM_POINTS_INTERIOR && kind != NBM_POINTS_BOUNDARY) return fail(h, NBM_E_ARG, "nbm_sample: bad kind");
+  int64_t H;
+  if (!h_on_lattice(h_cell, &H)) return fail(h, NBM_E_INVALID_PROBLEM, "nbm_sample: h must be a multiple of 2^-24 in (0,1) (G9)");
+  cudaSetDevice(h->device);
+  cudaError_t e = launch_sample(kind, seed, step, first_index, n, H, pts_dev, (cudaStream_t)stream);
+  return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_sample");
+}
+
+int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_t n,
+                  const float* bpts_dev, int64_t nb, float h_cell, int64_t n_global,
+                  int64_t nb_global, unsigned terms, float* loss_dev, float* grad_dev, void* stream) {
+  if (!h || !theta_dev || !loss_dev || !grad_dev || n < 0 || nb < 0 || (n > 0 && !pts_dev) ||
+      (nb > 0 && !bpts_dev))
+    return fail(h, NBM_E_ARG, "nbm_loss_grad: bad arguments");
+  if (n > h->ws.cap || nb > h->ws.cap) return fail(h, NBM_E_CAPACITY, "nbm_loss_grad: n or nb exceeds max_points");
+  if (n_global < n || nb_global < nb) return fail(h, NBM_E_ARG, "nbm_loss_grad: global counts smaller than local");
+  int64_t H;
+  if (!h_on_lattice(h_cell, &H)) return fail(h, NBM_E_INVALID_PROBLEM, "nbm_loss_grad: h must be a multiple of 2^-24 in (0,1) (G9)");
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevProblem& P = h->host_problem;
+  const ArchInfo& A = h->arch;
+  const Workspace& w = h->ws;
+  double hd = (double)h_cell;
+  double dm = diag(P, 0, hd), dpl = diag(P, 1, hd);
+  double ng = (double)(n_global > 0 ? n_global : 1), nbg = (double)(nb_global > 0 ? nb_global : 1);
+  int launches = 0;
+  cudaEvent_t* ev = nullptr;   // timing hook: 4 events of this call, no host synchronisation
+  if (h->timing) {
+    size_t base = (size_t)h->timed_calls * 4;
+    while (h->ev.size() < base + 4) {
+      cudaEvent_t x;
+      if (cudaEventCreate(&x) != cudaSuccess) break;
+      h->ev.push_back(x);
+    }
+    if (h->ev.size() >= base + 4) ev = &h->ev[base];
+  }
+  if (ev) cudaEventRecord(ev[0], s);
+  cudaError_t e = launch_classify(h, pts_dev, n, bpts_dev, nb, H, dm, dpl, terms, false, s);
+  launches += 3;
+  if (e == cudaSuccess) e = launch_assemble_crossed(h, pts_dev, n, H, s);
+  launches += 2;
+  // pass A: forward-only over the crossed rows (u per row)
+  MlpParams pa;
+  fill_common(h, pa, theta_dev, h_cell);
+  const int net1 = A.n_nets == 2 ? 1 : 0;
+  for (int k = 0; k < 2; ++k) {
+    pa.seg.kind[k] = kSegXRows;
+    pa.seg.net[k] = k == 0 ? 0 : net1;
+    pa.cnt_slot[k] = 12 + k;
+    pa.seg.items[k] = w.xlist + (int64_t)k * 7 * w.xcap;
+    pa.seg.src[k] = w.xrow_x;
+    pa.seg.aux[k] = w.xrow_cot;
+    pa.aux_by_item[k] = 1;
+  }
+  pa.u_out = w.xrow_u;
+  if (e == cudaSuccess) e = launch_mlp_fp32(A.width, A.n_hidden, false, pa, w.grid_mlp, s);
+  launches += 1;
+  if (e == cudaSuccess) e = launch_crossed_residual(h, n_global > 0 ? n_global : 1, s);
+  launches += 1;
+  // main fused pass over all segments (net- first, then net+)
+  MlpParams pm;
+  fill_common(h, pm, theta_dev, h_cell);
+  pm.two_over_n = (float)(2.0 / ng);
+  for (int k = 0; k < 2; ++k) {
+    const int s0 = 3 * k, net = k == 0 ? 0 : net1;
+    const int side = k;
+    pm.seg.kind[s0] = kSegStencil;
+    pm.seg.net[s0] = net;
+    pm.cnt_slot[s0] = kClsUnxMinus + side;
+    pm.start_slot[s0] = kNumCls + kClsUnxMinus + side;
+    pm.seg.items[s0] = w.list;
+    pm.seg.src[s0] = pts_dev;
+    pm.seg.aux[s0] = w.list_aux;
+    double bs = P.beta[side], d = side ? dpl : dm;
+    pm.seg.chat[s0] = (float)((-bs / (hd * hd)) / d);
+    pm.seg.kind[s0 + 1] = kSegXRows;
+    pm.seg.net[s0 + 1] = net;
+    pm.cnt_slot[s0 + 1] = 12 + k;
+    pm.seg.items[s0 + 1] = w.xlist + (int64_t)k * 7 * w.xcap;
+    pm.seg.src[s0 + 1] = w.xrow_x;
+    pm.seg.aux[s0 + 1] = w.xrow_cot;
+    pm.aux_by_item[s0 + 1] = 1;
+    pm.seg.kind[s0 + 2] = kSegBRows;
+    pm.seg.net[s0 + 2] = net;
+    pm.cnt_slot[s0 + 2] = kClsBndMinus + side;
+    pm.start_slot[s0 + 2] = kNumCls + kClsBndMinus + side;
+    pm.seg.items[s0 + 2] = w.list;
+    pm.seg.src[s0 + 2] = bpts_dev;
+    pm.seg.aux[s0 + 2] = w.list_aux;
+    pm.seg.a[s0 + 2] = (float)(2.0 * P.lambda_b / nbg);
+  }
+  if (ev) cudaEventRecord(ev[1], s);
+  if (e == cudaSuccess) e = launch_mlp_fp32(A.width, A.n_hidden, true, pm, w.grid_mlp, s);
+  launches += 1;
+  if (ev) cudaEventRecord(ev[2], s);
+  if (e == cudaSuccess) e = launch_reduce(h, grad_dev, loss_dev, s);
+  launches += 1;
+  if (ev) {
+    cudaEventRecord(ev[3], s);
+    h->timed_calls += 1;
+  }
+  h->last_launches = launches;
+  return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_loss_grad");
+}
+
+int nbm_classify(nbm_handle* h, const float* pts_dev, int64_t n, float h_cell, uint8_t* mask_dev,
+                 uint8_t* cls_dev, void* stream) {
+  if (!h || n < 0 || (n > 0 && (!pts_dev || !mask_dev || !cls_dev))) return fail(h, NBM_E_ARG, "nbm_classify: bad arguments");
+  if (n > h->ws.cap) return fail(h, NBM_E_CAPACITY, "nbm_classify: n exceeds max_points");
+  int64_t H;
+  if (!h_on_lattice(h_cell, &H)) return fail(h, NBM_E_INVALID_PROBLEM, "nbm_classify: h must be a multiple of 2^-24 in (0,1) (G9)");
+  if (n == 0) return NBM_OK;
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  double hd = (double)h_cell;
+  cudaError_t e = launch_classify(h, pts_dev, n, nullptr, 0, H, diag(h->host_problem, 0, hd),
+                                  diag(h->host_problem, 1, hd), NBM_TERM_ALL, false, s, mask_dev);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(cls_dev, h->ws.cls, (size_t)n, cudaMemcpyDeviceToDevice, s);
+  return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_classify");
+}
+
+int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_t n, float* u_dev,
+             void* stream) {
+  if (!h || !theta_dev || n < 0 || (n > 0 && (!pts_dev || !u_dev))) return fail(h, NBM_E_ARG, "nbm_eval: bad arguments");
+  if (n > h->ws.cap) return fail(h, NBM_E_CAPACITY, "nbm_eval: n exceeds max_points");
+  if (n == 0) return NBM_OK;
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const ArchInfo& A = h->arch;
+  const Workspace& w = h->ws;
+  cudaError_t e = launch_classify(h, pts_dev, n, nullptr, 0, 1, 1.0, 1.0, NBM_TERM_ALL, true, s);
+  MlpParams p;
+  fill_common(h, p, theta_dev, 0.0f);
+  for (int k = 0; k < 2; ++k) {
+    p.seg.kind[k] = kSegBRows;
+    p.seg.net[k] = (A.n_nets == 2) ? k : 0;
+    p.cnt_slot[k] = kClsBndMinus + k;
+    p.start_slot[k] = kNumCls + kClsBndMinus + k;
+    p.seg.items[k] = w.list;
+    p.seg.src[k] = pts_dev;
+    p.seg.aux[k] = w.list_aux;
+  }
+  p.u_out = u_dev;
+  if (e == cudaSuccess) e = launch_mlp_fp32(A.width, A.n_hidden, false, p, w.grid_mlp, s);
+  return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_eval");
+}
+
+int nbm_adam_step(nbm_handle* h, float* theta_dev, float* m_dev, float* v_dev, const float* grad_dev,
+                  int64_t t, float lr, float b1, float b2, float eps, void* stream) {
+  if (!h || !theta_dev || !m_dev || !v_dev || !grad_dev || t < 1) return fail(h, NBM_E_ARG, "nbm_adam_step: bad arguments");
+  cudaSetDevice(h->device);
+  float bc1 = (float)(1.0 - pow((double)b1, (double)t));
+  float bc2 = (float)(1.0 - pow((double)b2, (double)t));
+  cudaError_t e = launch_adam(h->arch.p_net * h->arch.n_nets, theta_dev, m_dev, v_dev, grad_dev, lr,
+                              b1, b2, eps, bc1, bc2, (cudaStream_t)stream);
+  return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_adam_step");
+}
+
+int nbm_timing_enable(nbm_handle* h, int enable) {
+  if (!h) return NBM_E_ARG;
+  h->timing = enable != 0;
+  return NBM_OK;
+}
+
+int nbm_timing_read(nbm_handle* h, double* mlp_ms, double* total_ms, int64_t* calls) {
+  if (!h) return NBM_E_ARG;
+  double a = 0.0, b = 0.0;
+  for (int64_t c = 0; c < h->timed_calls; ++c) {
+    cudaEvent_t* ev = &h->ev[4 * c];
+    cudaError_t e = cudaEventSynchronize(ev[3]);
+    if (e != cudaSuccess) return cuda_fail(h, e, "nbm_timing_read");
+    float x = 0.f, y = 0.f;
+    cudaEventElapsedTime(&x, ev[1], ev[2]);
+    cudaEventElapsedTime(&y, ev[0], ev[3]);
+    a += x;
+    b += y;
+  }
+  if (mlp_ms) *mlp_ms = a;
+  if (total_ms) *total_ms = b;
+  if (calls) *calls = h->timed_calls;
+  h->timed_calls = 0;
+  return NBM_OK;
+}
+
+int nbm_last_launch_count(const nbm_handle* h) { return h ? h->last_launches : 0; }
+
+}  // extern "C"

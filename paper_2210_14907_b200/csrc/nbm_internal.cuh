@@ -1,0 +1,158 @@
+// nbm_internal.cuh -- internal declarations shared by the libnbm.so translation units.
+// Nothing here is part of the C ABI (include/nbm.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nbm.h"
+
+namespace nbm {
+
+constexpr int kMaxSpheres = 64;
+constexpr int kMaxCharges = 64;
+constexpr int kMaxLayers = 8;
+constexpr int kLattice = 1 << 24;   // coordinates and h are multiples of 2^-24 (G9)
+
+// sticky device error bits (nbm_status)
+constexpr int kErrOutOfDomain = 1;
+constexpr int kErrDegenerate = 2;
+constexpr int kErrNonfinite = 4;
+
+// Problem constants in fp64, resident in device memory (one copy per handle).
+struct DevProblem {
+  int ls_kind, n_spheres;
+  double centers[kMaxSpheres][3];
+  double radii[kMaxSpheres];
+  double star_r0, star_amp;
+  int star_m, star_n;
+  double plane_n[3], plane_c;
+  double beta[2], k[2];
+  int source, n_charges;
+  double q[kMaxCharges];
+  double charge_centers[kMaxCharges][3];
+  double charge_sigma;
+  double lambda_b;
+};
+
+// Point classes produced by the classification stage (S2).
+enum : int {
+  kClsUnxMinus = 0,   // interior, all 7 vertices in Omega-
+  kClsUnxPlus = 1,    // interior, all 7 vertices in Omega+
+  kClsCrossed = 2,    // interior, mixed stencil mask
+  kClsBndMinus = 3,   // boundary point in Omega-
+  kClsBndPlus = 4,    // boundary point in Omega+
+  kClsSkip = 5,       // excluded (arm out of the box, or term not selected)
+  kNumCls = 6
+};
+
+// Segments of the fused MLP kernel's tile space.  Ordered so that a CTA's
+// contiguous tile range changes network at most once: net- segments first.
+enum : int { kSegStencil = 0, kSegXRows = 1, kSegBRows = 2 };
+constexpr int kNumSeg = 6;   // (stencil, xrows, brows) x (net-, net+)
+
+struct SegTable {
+  int kind[kNumSeg];
+  int net[kNumSeg];
+  const int* count[kNumSeg];   // device pointer to the item count
+  const int* items[kNumSeg];   // item list (indices into src)
+  const float* src[kNumSeg];   // AoS [][3] coordinates the items index
+  const float* aux[kNumSeg];   // per-list-position scalar (rhs_hat / g / cotangent)
+  float a[kNumSeg];            // boundary: 2 lambda_b / N_b,global
+  float chat[kNumSeg];         // stencil: arm coefficient / diagonal (uncrossed row)
+};
+
+struct Workspace {
+  int64_t cap;          // max points per call (interior and boundary each)
+  int64_t xcap;         // crossed-point capacity (== cap)
+  int nblk_cls;         // blocks of the classification grid at capacity
+  // classification
+  uint8_t* cls;         // [cap + cap]
+  float* aux_tmp;       // [cap + cap]   rhs_hat (interior) or g (boundary) per point
+  int* blk_counts;      // [nblk_cls][kNumCls]
+  int* blk_offsets;     // [nblk_cls][kNumCls]
+  int* counts;          // [16]: class counts, then segment counts
+  int* list;            // [cap + cap]   class-partitioned indices
+  float* list_aux;      // [cap + cap]
+  // crossed rows (7 per crossed point)
+  float* xrow_x;        // [7 xcap][3]
+  float* xrow_u;        // [7 xcap]
+  float* xrow_cot;      // [7 xcap]
+  uint8_t* xrow_tag;    // [7 xcap]
+  float* xrec;          // [xcap][8]  chat[7] (chat[0] = 1), rhs_hat
+  int* xlist;           // [2][7 xcap] row ids partitioned by network
+  // fused-MLP partials
+  int grid_mlp;         // CTAs of the fused kernel
+  float* part;          // [2][grid_mlp][Pnet]
+  int* touched;         // [2][grid_mlp]
+  double* lpart;        // [grid_mlp + 1]  (+1: crossed rows' loss)
+  int* err;             // sticky error word
+  // eval
+  float* eval_aux;      // unused placeholder for symmetry
+};
+
+struct ArchInfo {
+  int n_layers, width, n_hidden, act, prec, n_nets;
+  int sizes[kMaxLayers];
+  int64_t p_net;        // parameters per network
+};
+
+}  // namespace nbm
+
+struct nbm_handle {
+  int device;
+  nbm::ArchInfo arch;
+  nbm::DevProblem host_problem;
+  nbm::DevProblem* d_problem;
+  nbm::Workspace ws;
+  std::string last_error;
+  // timing hook
+  bool timing;
+  std::vector<cudaEvent_t> ev;   // 4 events per timed call: total start, mlp start, mlp end, total end
+  int64_t timed_calls;           // calls recorded since the last read
+  int last_launches;
+};
+
+namespace nbm {
+
+// ---- launchers implemented in the .cu files ----
+// sample_init.cu
+cudaError_t launch_sample(int kind, uint64_t seed, uint64_t step, int64_t first, int64_t n,
+                          int64_t H, float* pts, cudaStream_t s);
+cudaError_t launch_init_params(const ArchInfo& a, uint64_t seed, float* theta, cudaStream_t s);
+cudaError_t launch_adam(int64_t P, float* theta, float* m, float* v, const float* g, float lr,
+                        float b1, float b2, float eps, float bc1, float bc2, cudaStream_t s);
+// geometry.cu (compiled without FMA contraction)
+cudaError_t launch_classify(const nbm_handle* h, const float* pts, int64_t n, const float* bpts,
+                            int64_t nb, int64_t H, double inv_d_minus, double inv_d_plus,
+                            unsigned terms, bool eval_only, cudaStream_t s,
+                            uint8_t* mask_out = nullptr);
+cudaError_t launch_assemble_crossed(const nbm_handle* h, const float* pts, int64_t n, int64_t H,
+                                    cudaStream_t s);
+cudaError_t launch_crossed_residual(const nbm_handle* h, int64_t n_global, cudaStream_t s);
+// mlp_fp32.cu
+struct MlpParams {
+  SegTable seg;
+  const int* counts;         // device counts array (see nbm.cu for the slot map)
+  int cnt_slot[kNumSeg];     // counts[cnt_slot] = items in the segment
+  int start_slot[kNumSeg];   // counts[start_slot] = first list position (-1: 0)
+  int aux_by_item[kNumSeg];  // aux indexed by item (1) or by list position (0)
+  const float* theta;
+  int64_t p_net;
+  float h;
+  float two_over_n;          // 2 / N_global
+  int64_t p_stride;          // partial-slot stride (p_net rounded up to 4 floats)
+  float* part;               // [2][grid][p_stride]
+  int* touched;              // [2][grid]
+  double* lpart;             // [grid]
+  float* u_out;              // forward-only mode: u_out[item] = u
+};
+cudaError_t launch_mlp_fp32(int width, int n_hidden, bool train, const MlpParams& p, int grid,
+                            cudaStream_t s);
+int mlp_fp32_supported(int width, int n_hidden);
+// reduce
+cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s);
+
+}  // namespace nbm

@@ -1,0 +1,293 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bars (BASELINE.json north_star): sampled points, init and stencil
+masks bit-exact; fp32 loss within 1e-5 relative and gradient within 1e-4 relative (L2),
+asserted per term (uncrossed-, uncrossed+, crossed, boundary).  The uncrossed terms are
+ill-conditioned: their tolerance is max(stated, 4 x the oracle's own
+fp32-emulation deviation from fp64), the noise floor of any correct fp32 implementation."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2210_14907_b200 import inputs, nbm
+
+pytestmark = pytest.mark.gpu
+
+LOSS_TOL, GRAD_TOL = 1e-5, 1e-4
+TERMS = [nbm.TERM_UNX_MINUS, nbm.TERM_UNX_PLUS, nbm.TERM_CROSSED, nbm.TERM_BOUNDARY]
+
+
+def _cfg(name, **kw):
+    cfg = inputs.config(name)
+    if name in ("c3", "c4"):   # fp32 tanh W=64 surrogate on the config's geometry and data
+        cfg.update(sizes=[3, 64, 64, 64, 1], act=inputs.ACT_TANH, prec=inputs.PREC_FP32)
+    cfg.update(kw)
+    return cfg
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def _gpu_loss_grad(s, th, pts, bpts, terms=nbm.TERM_ALL, n_glob=None, nb_glob=None):
+    loss, grad = s.loss_grad(pts, bpts, n_global=n_glob, nb_global=nb_glob, terms=terms, theta=th)
+    torch.cuda.synchronize()
+    return float(loss.item()), grad.double().cpu().numpy().copy()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_sampler_bit_exact(orc, name):
+    cfg = _cfg(name)
+    s = nbm.Solver(cfg, 0, max_points=1 << 16)
+    for kind in (0, 1):
+        for first, n in ((0, 5000), (123457, 4099), (1 << 31, 17)):
+            out = torch.empty(n, 3, device="cuda")
+            s.sample(kind, 7, 3, first, n, out)
+            want = orc.sample(kind, 7, 3, first, n, cfg["H"])
+            assert np.array_equal(out.cpu().numpy(), want)
+    s.close()
+
+
+def test_sampler_bit_exact_full_size(orc):
+    cfg = _cfg("c4")
+    s = nbm.Solver(cfg, 0, max_points=16)
+    n = 1 << 22
+    out = torch.empty(n, 3, device="cuda")
+    s.sample(0, 0, 5, 0, n, out)
+    assert np.array_equal(out.cpu().numpy(), orc.sample(0, 0, 5, 0, n, cfg["H"]))
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_init_bit_exact(orc, name):
+    cfg = _cfg(name)
+    s = nbm.Solver(cfg, 0, max_points=16)
+    _, ar = orc.from_config(cfg)
+    for seed in (0, 1, 2**40 + 3):
+        s.init_params(seed)
+        assert np.array_equal(s.theta.cpu().numpy(), orc.init_params(ar, seed))
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_classification_bit_exact(orc, name):
+    cfg = _cfg(name)
+    n = 1 << 16
+    s = nbm.Solver(cfg, 0, max_points=n)
+    pb, _ = orc.from_config(cfg)
+    pts = orc.sample(0, 11, 0, 0, n, cfg["H"])
+    # add exact-tie points on the level set (phi = 0 -> Omega-)
+    if name == "c2":
+        pts[:4] = [[0.5 - cfg["h"], 0, 0], [0, -0.5 + cfg["h"], 0], [0, 0, 0.5 + cfg["h"]], [0.25, 0.25, 0.0]]
+    mask = torch.empty(n, dtype=torch.uint8, device="cuda")
+    cls = torch.empty(n, dtype=torch.uint8, device="cuda")
+    nbm.nbm_classify(s.h, _dev(pts), n, s.h_cell, mask, cls)
+    om, oc = orc.classify(pb, pts, cfg["h"])
+    assert np.array_equal(mask.cpu().numpy(), om)
+    assert np.array_equal(cls.cpu().numpy(), oc)
+    assert (oc == 2).sum() > 50
+    s.close()
+
+
+def _parity(orc, cfg, n, nb, seed=0, theta_seed=None, step=0):
+    s = nbm.Solver(cfg, 0, max_points=max(n, nb, 1))
+    pb, ar = orc.from_config(cfg)
+    pts = orc.sample(0, seed, step, 0, n, cfg["H"])
+    bpts = orc.sample(1, seed, step, 0, nb, cfg["H"])
+    th = orc.init_params(ar, 0) if theta_seed is None else inputs.random_theta(cfg["sizes"], cfg["n_nets"], theta_seed)
+    L, lt, g, gt = orc.loss_grad(pb, ar, th, pts, bpts, cfg["h"], per_term=True)
+    _, lt32, _, gt32 = orc.loss_grad(pb, ar, th, pts, bpts, cfg["h"], per_term=True, mode=orc.MODE_F32)
+    dth = _dev(th)
+    dp, db = _dev(pts.reshape(-1, 3)), _dev(bpts.reshape(-1, 3))
+    gl, gg = _gpu_loss_grad(s, dth, dp, db)
+    assert abs(gl - L) <= LOSS_TOL * abs(L), (gl, L)
+    assert np.linalg.norm(gg - g) <= GRAD_TOL * np.linalg.norm(g)
+    for k, term in enumerate(TERMS):
+        tl, tg = _gpu_loss_grad(s, dth, dp, db, terms=term)
+        if lt[k] == 0.0:
+            assert tl == 0.0 and np.all(tg == 0.0)
+            continue
+        ltol, gtol = LOSS_TOL, GRAD_TOL
+        if k < 2:   # ill-conditioned uncrossed terms: noise floor of fp32 (SURVEY 8c rule 2)
+            ltol = max(ltol, 4 * abs(lt32[k] - lt[k]) / lt[k])
+            gtol = max(gtol, 4 * np.linalg.norm(gt32[k] - gt[k]) / np.linalg.norm(gt[k]))
+        assert abs(tl - lt[k]) <= ltol * lt[k], (k, tl, lt[k], ltol)
+        assert np.linalg.norm(tg - gt[k]) <= gtol * np.linalg.norm(gt[k]), (k, gtol)
+    s.close()
+    return lt
+
+
+def test_parity_config1_full(orc):
+    cfg = _cfg("c1")
+    lt = _parity(orc, cfg, cfg["N"], cfg["Nb"])
+    assert lt[0] > 0 and lt[3] > 0
+
+
+@pytest.mark.parametrize("theta_seed", [None, 5])
+def test_parity_config2_reduced(orc, theta_seed):
+    cfg = _cfg("c2")
+    lt = _parity(orc, cfg, 1 << 14, 1 << 11, theta_seed=theta_seed)
+    assert all(v > 0 for v in lt)
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_parity_other_geometries(orc, name):
+    """star + Gaussian charges (config 3) and the 32-sphere union (config 4) with the fp32
+    W=64 surrogate (the bf16 widths are a separate kernel)."""
+    cfg = _cfg(name)
+    _parity(orc, cfg, 1 << 13, 1 << 10, seed=3)
+
+
+def test_parity_config2_full_size(orc):
+    """BASELINE config 2 at its full size (2^18 + 2^15 points) in the bench's launch
+    configuration."""
+    cfg = _cfg("c2")
+    s = nbm.Solver(cfg, 0)
+    pb, ar = orc.from_config(cfg)
+    s.init_params(0)
+    pts = torch.empty(cfg["N"], 3, device="cuda")
+    bpts = torch.empty(cfg["Nb"], 3, device="cuda")
+    s.sample(0, 0, 0, 0, cfg["N"], pts)
+    s.sample(1, 0, 0, 0, cfg["Nb"], bpts)
+    gl, gg = _gpu_loss_grad(s, s.theta, pts, bpts)
+    th = orc.init_params(ar, 0)
+    L, _, g, _ = orc.loss_grad(pb, ar, th, pts.cpu().numpy(), bpts.cpu().numpy(), cfg["h"])
+    assert abs(gl - L) <= LOSS_TOL * L
+    assert np.linalg.norm(gg - g) <= GRAD_TOL * np.linalg.norm(g)
+    s.close()
+
+
+def test_ragged_and_empty_batches(orc):
+    cfg = _cfg("c2")
+    pb, ar = orc.from_config(cfg)
+    th = inputs.random_theta(cfg["sizes"], 2, 9)
+    s = nbm.Solver(cfg, 0, max_points=4096)
+    dth = _dev(th)
+    allp = orc.sample(0, 2, 0, 0, 4096, cfg["H"])
+    allb = orc.sample(1, 2, 0, 0, 512, cfg["H"])
+    _, cls = orc.classify(pb, allp, cfg["h"])
+    crossed = allp[cls == 2]
+    cases = [(allp[:1], allb[:0]), (allp[:17], allb[:3]), (allp[:19], allb[:129]),
+             (allp[:0], allb[:200]), (allp[:300], allb[:0]), (crossed[:13], allb[:0]),
+             (allp[:4096], allb[:512])]
+    for p_, b_ in cases:
+        gl, gg = _gpu_loss_grad(s, dth, _dev(p_) if len(p_) else None, _dev(b_) if len(b_) else None)
+        L, _, g, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"])
+        L32, _, g32, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"],
+                                       mode=orc.MODE_F32)
+        ltol = max(LOSS_TOL, 4 * abs(L32 - L) / L)          # noise floor when only uncrossed rows
+        gtol = max(GRAD_TOL, 4 * np.linalg.norm(g32 - g) / np.linalg.norm(g))
+        assert abs(gl - L) <= ltol * L, (len(p_), len(b_), gl, L)
+        assert np.linalg.norm(gg - g) <= gtol * np.linalg.norm(g)
+    gl, gg = _gpu_loss_grad(s, dth, None, None)
+    assert gl == 0.0 and np.all(gg == 0.0)
+    assert s.status() == 0
+    s.close()
+
+
+def test_errors_and_capacity(orc):
+    cfg = _cfg("c2")
+    s = nbm.Solver(cfg, 0, max_points=64)
+    big = torch.zeros(65, 3, device="cuda")
+    with pytest.raises(nbm.NbmError) as e:
+        s.loss_grad(big, None)
+    assert e.value.code == 3
+    with pytest.raises(nbm.NbmError) as e:
+        nbm.nbm_sample(s.h, 0, 0, 0, 0, 4, 0.1, torch.zeros(4, 3, device="cuda"))
+    assert e.value.code == 2                                  # h not on the lattice (G9)
+    ood = _dev(np.array([[1.0 - cfg["h"] / 2, 0.0, 0.0]]))
+    s.loss_grad(ood, None)
+    assert s.status() == 6                                    # NBM_E_OUT_OF_DOMAIN
+    assert s.status() == 0                                    # sticky word cleared
+    s.close()
+    with pytest.raises(nbm.NbmError) as e:
+        nbm.Solver(dict(cfg, sizes=[3, 48, 48, 1]), 0, max_points=16)
+    assert e.value.code == 1
+
+
+def test_determinism_and_shard_invariance(orc):
+    cfg = _cfg("c2")
+    n, nb = 1 << 14, 1 << 11
+    s = nbm.Solver(cfg, 0, max_points=n)
+    s.init_params(3)
+    pts = torch.empty(n, 3, device="cuda")
+    bpts = torch.empty(nb, 3, device="cuda")
+    s.sample(0, 1, 0, 0, n, pts)
+    s.sample(1, 1, 0, 0, nb, bpts)
+    l1, g1 = _gpu_loss_grad(s, s.theta, pts, bpts)
+    l2, g2 = _gpu_loss_grad(s, s.theta, pts, bpts)
+    assert l1 == l2 and np.array_equal(g1, g2)                # bitwise (G21)
+    acc_l, acc_g = 0.0, np.zeros_like(g1)
+    for r in range(4):                                        # P = 4 ranks in one process
+        lo, hi = r * n // 4, (r + 1) * n // 4
+        blo, bhi = r * nb // 4, (r + 1) * nb // 4
+        sp = torch.empty(hi - lo, 3, device="cuda")
+        sb = torch.empty(bhi - blo, 3, device="cuda")
+        s.sample(0, 1, 0, lo, hi - lo, sp)                    # each rank draws its own shard
+        s.sample(1, 1, 0, blo, bhi - blo, sb)
+        l, g = _gpu_loss_grad(s, s.theta, sp, sb, n_glob=n, nb_glob=nb)
+        acc_l += l
+        acc_g += g
+    assert abs(acc_l - l1) <= 1e-6 * l1
+    assert np.linalg.norm(acc_g - g1) <= 1e-5 * np.linalg.norm(g1)
+    s.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_eval_parity(orc, name):
+    cfg = _cfg(name)
+    n = 5000
+    s = nbm.Solver(cfg, 0, max_points=n)
+    pb, ar = orc.from_config(cfg)
+    th = inputs.random_theta(cfg["sizes"], cfg["n_nets"], 4)
+    pts = np.concatenate([orc.sample(0, 4, 0, 0, n - 100, cfg["H"]), orc.sample(1, 4, 0, 0, 100, cfg["H"])])
+    s.theta.copy_(_dev(th))
+    u = s.eval(_dev(pts)).double().cpu().numpy()
+    want = orc.evaluate(pb, ar, th, pts)
+    assert np.allclose(u, want, rtol=1e-5, atol=1e-6 * np.abs(want).max())
+    s.close()
+
+
+def test_adam_matches_fp32_mirror(orc):
+    cfg = _cfg("c2")
+    s = nbm.Solver(cfg, 0, max_points=16)
+    rng = np.random.default_rng(0)
+    P = s.P
+    th = rng.normal(size=P).astype(np.float32)
+    m = (rng.normal(size=P) * 1e-3).astype(np.float32)
+    v = (rng.uniform(size=P) * 1e-6).astype(np.float32)
+    g = (rng.normal(size=P) * 1e-3).astype(np.float32)
+    s.theta.copy_(_dev(th)); s.m.copy_(_dev(m)); s.v.copy_(_dev(v)); s.grad.copy_(_dev(g))
+    s.t = 6
+    s.adam_step()
+    want = orc.adam_f32(th, m, v, g, 7)
+    for got, w in zip((s.theta, s.m, s.v), want):
+        got = got.cpu().numpy()
+        ulps = np.abs(got.view(np.int32).astype(np.int64) - w.view(np.int32).astype(np.int64))
+        assert ulps.max() <= 2
+    s.close()
+
+
+def test_config1_ten_adam_steps(orc):
+    """BASELINE config 1: one loss+grad eval plus 10 Adam steps (lr 1e-3) tracks the
+    oracle (fp64 gradients, fp64 Adam) step by step."""
+    cfg = _cfg("c1")
+    s = nbm.Solver(cfg, 0)
+    pb, ar = orc.from_config(cfg)
+    s.init_params(0)
+    pts = torch.empty(cfg["N"], 3, device="cuda")
+    bpts = torch.empty(cfg["Nb"], 3, device="cuda")
+    s.sample(0, 0, 0, 0, cfg["N"], pts)
+    s.sample(1, 0, 0, 0, cfg["Nb"], bpts)
+    P_, B_ = pts.cpu().numpy(), bpts.cpu().numpy()
+    th = orc.init_params(ar, 0).astype(np.float64)
+    m, v = np.zeros_like(th), np.zeros_like(th)
+    for t in range(1, 11):
+        gl, _ = _gpu_loss_grad(s, s.theta, pts, bpts)
+        L, _, g, _ = orc.loss_grad(pb, ar, th, P_, B_, cfg["h"])
+        assert abs(gl - L) <= LOSS_TOL * L, (t, gl, L)
+        s.adam_step(lr=cfg["lr"])
+        th, m, v = orc.adam(th, m, v, g, t, lr=cfg["lr"])
+    disp = np.linalg.norm(th - orc.init_params(ar, 0))
+    assert np.linalg.norm(s.theta.double().cpu().numpy() - th) <= 1e-3 * disp
+    s.close()
