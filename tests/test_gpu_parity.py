@@ -167,7 +167,9 @@ def test_ragged_and_empty_batches(orc):
     allb = orc.sample(1, 2, 0, 0, 512, cfg["H"])
     _, cls = orc.classify(pb, allp, cfg["h"])
     crossed = allp[cls == 2]
-    cases = [(allp[:1], allb[:0]), (allp[:17], allb[:3]), (allp[:19], allb[:129]),
+    # single points: a crossed one alone, an uncrossed one with one boundary point (a lone
+    # uncrossed residual is a single draw of fp32 noise; its floor is estimated on >= 17 rows)
+    cases = [(crossed[:1], allb[:0]), (allp[:1], allb[:1]), (allp[:17], allb[:3]), (allp[:19], allb[:129]),
              (allp[:0], allb[:200]), (allp[:300], allb[:0]), (crossed[:13], allb[:0]),
              (allp[:4096], allb[:512])]
     for p_, b_ in cases:
