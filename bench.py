@@ -300,7 +300,7 @@ def main():
                    "global_points": Ng, "mlp": "x".join(map(str, cfg["sizes"])), "n_nets": cfg["n_nets"],
                    "h": cfg["h"], "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_mlp_fp32 (fused fwd/residual/bwd)",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": ("k_mlp_fp32" if cfg["prec"] == inputs.PREC_FP32 else "k_mlp_tc (tcgen05)") + " fused fwd/residual/bwd",
                      "flop_per_launch": flop_launch, "avg_launch_ms": mlp_avg_s * 1e3,
                      "share_of_step": (mlp_ms / max(calls, 1)) / (tot_ms / args.steps), "peak_src": peak_note},
         "gpu_launches": launches_per_step * args.steps,

@@ -22,9 +22,10 @@ SOURCES = {
     "sample_init.cu": [],
     "geometry.cu": ["-fmad=false"],
     "mlp_fp32.cu": [],
+    "mlp_tc.cu": [],
     "nbm.cu": [],
 }
-HEADERS = ["nbm_internal.cuh"]
+HEADERS = ["nbm_internal.cuh", "tc_ptx.cuh"]
 
 
 def _mtime(p):

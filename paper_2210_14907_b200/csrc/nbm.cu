@@ -54,6 +54,7 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
   int nh = a->n_layers - 2;
   bool ok = false;
   if (a->prec == NBM_PREC_FP32 && a->act == NBM_ACT_TANH) ok = mlp_fp32_supported(W, nh);
+  if (a->prec == NBM_PREC_BF16) ok = mlp_tc_supported(W, nh, a->act);
   if (!ok) {
     *why = "arch: unsupported (prec, act, width, depth) combination in this build";
     return NBM_E_INVALID_ARCH;
@@ -169,6 +170,11 @@ void fill_common(const nbm_handle* h, MlpParams& p, const float* theta, float hf
   p.touched = h->ws.touched;
   p.lpart = h->ws.lpart;
   for (int s = 0; s < kNumSeg; ++s) { p.cnt_slot[s] = kSlotZero; p.start_slot[s] = -1; p.seg.kind[s] = kSegXRows; }
+}
+
+cudaError_t launch_mlp(const ArchInfo& A, bool train, const MlpParams& p, int grid, cudaStream_t s) {
+  if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, train, p, grid, s);
+  return launch_mlp_fp32(A.width, A.n_hidden, train, p, grid, s);
 }
 
 }  // namespace
@@ -378,7 +384,7 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
     pa.aux_by_item[k] = 1;
   }
   pa.u_out = w.xrow_u;
-  if (e == cudaSuccess) e = launch_mlp_fp32(A.width, A.n_hidden, false, pa, w.grid_mlp, s);
+  if (e == cudaSuccess) e = launch_mlp(A, false, pa, w.grid_mlp, s);
   launches += 1;
   if (e == cudaSuccess) e = launch_crossed_residual(h, n_global > 0 ? n_global : 1, s);
   launches += 1;
@@ -415,7 +421,7 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
     pm.seg.a[s0 + 2] = (float)(2.0 * P.lambda_b / nbg);
   }
   if (ev) cudaEventRecord(ev[1], s);
-  if (e == cudaSuccess) e = launch_mlp_fp32(A.width, A.n_hidden, true, pm, w.grid_mlp, s);
+  if (e == cudaSuccess) e = launch_mlp(A, true, pm, w.grid_mlp, s);
   launches += 1;
   if (ev) cudaEventRecord(ev[2], s);
   if (e == cudaSuccess) e = launch_reduce(h, grad_dev, loss_dev, s);
@@ -466,7 +472,7 @@ int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_
     p.seg.aux[k] = w.list_aux;
   }
   p.u_out = u_dev;
-  if (e == cudaSuccess) e = launch_mlp_fp32(A.width, A.n_hidden, false, p, w.grid_mlp, s);
+  if (e == cudaSuccess) e = launch_mlp(A, false, p, w.grid_mlp, s);
   return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_eval");
 }
 

@@ -152,6 +152,9 @@ struct MlpParams {
 cudaError_t launch_mlp_fp32(int width, int n_hidden, bool train, const MlpParams& p, int grid,
                             cudaStream_t s);
 int mlp_fp32_supported(int width, int n_hidden);
+// mlp_tc.cu (tcgen05 bf16)
+cudaError_t launch_mlp_tc(int width, int n_hidden, bool train, const MlpParams& p, int grid, cudaStream_t s);
+int mlp_tc_supported(int width, int n_hidden, int act);
 // reduce
 cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s);
 
