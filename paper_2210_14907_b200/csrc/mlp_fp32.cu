@@ -22,7 +22,8 @@ namespace nbm {
 
 constexpr int kB = 128;        // rows per tile
 constexpr int kPT = 18;        // points per stencil tile (126 rows)
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;   // 16 warps: 4 per scheduler hide the LDS latency
+constexpr int kRT = kB / 32;     // GEMM rows per thread
 
 
 
@@ -49,7 +50,7 @@ template <int W, int NH>
 struct Layout {
   static constexpr int LDA = W + 4;              // padded row stride of activations
   static constexpr int LDW = W + 4;              // padded row stride of hidden weights
-  static constexpr int TC = W / 16;              // GEMM columns per thread (rows: 8)
+  static constexpr int TC = W / 16;              // GEMM columns per thread (rows: kRT)
   static constexpr int DB = (W == 64) ? 4 : 2;   // dW block per thread: DB x DB
   static constexpr int NHH = NH - 1;             // hidden x hidden layers
   // shared-memory carve (floats)
@@ -85,23 +86,23 @@ __device__ __forceinline__ void fwd_gemm(const float* __restrict__ Hin, float* _
                                          int tid) {
   using L = Layout<W, NH>;
   constexpr int TC = L::TC;
-  const int tr = tid & 15, tc = tid >> 4;
-  float acc[8][TC];
+  const int tr = tid & 31, tc = tid >> 5;
+  float acc[kRT][TC];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < kRT; ++i)
 #pragma unroll
     for (int c = 0; c < TC; ++c) acc[i][c] = 0.0f;
-#pragma unroll 2
+#pragma unroll 4
   for (int k = 0; k < W; k += 4) {
-    float a[8][4], w[TC][4];
+    float a[kRT][4], w[TC][4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ldv(Hin + (tr + 16 * i) * L::LDA + k, a[i]);
+    for (int i = 0; i < kRT; ++i) ldv(Hin + (tr + 32 * i) * L::LDA + k, a[i]);
 #pragma unroll
     for (int c = 0; c < TC; ++c) ldv(Ws + (tc * TC + c) * L::LDW + k, w[c]);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < kRT; ++i)
 #pragma unroll
         for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(a[i][q], w[c][q], acc[i][c]);
   }
@@ -109,11 +110,11 @@ __device__ __forceinline__ void fwd_gemm(const float* __restrict__ Hin, float* _
 #pragma unroll
   for (int c = 0; c < TC; ++c) bv[c] = bias[tc * TC + c];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < kRT; ++i) {
     float o[TC];
 #pragma unroll
     for (int c = 0; c < TC; ++c) o[c] = tanhf(acc[i][c] + bv[c]);
-    stv(Hout + (tr + 16 * i) * L::LDA + tc * TC, o);
+    stv(Hout + (tr + 32 * i) * L::LDA + tc * TC, o);
   }
 }
 
@@ -123,30 +124,30 @@ __device__ __forceinline__ void bwd_gemm(const float* __restrict__ G, float* __r
                                          const float* __restrict__ Ws, int tid) {
   using L = Layout<W, NH>;
   constexpr int TC = L::TC;
-  const int tr = tid & 15, tc = tid >> 4;
-  float acc[8][TC];
+  const int tr = tid & 31, tc = tid >> 5;
+  float acc[kRT][TC];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < kRT; ++i)
 #pragma unroll
     for (int c = 0; c < TC; ++c) acc[i][c] = 0.0f;
-#pragma unroll 2
+#pragma unroll 4
   for (int o = 0; o < W; o += 4) {
-    float g[8][4], w[4][TC];
+    float g[kRT][4], w[4][TC];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ldv(G + (tr + 16 * i) * L::LDA + o, g[i]);
+    for (int i = 0; i < kRT; ++i) ldv(G + (tr + 32 * i) * L::LDA + o, g[i]);
 #pragma unroll
     for (int q = 0; q < 4; ++q) ldv(Ws + (o + q) * L::LDW + tc * TC, w[q]);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < kRT; ++i)
 #pragma unroll
         for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(g[i][q], w[q][c], acc[i][c]);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < kRT; ++i) {
     float hv[TC], o[TC];
-    float* p = H + (tr + 16 * i) * L::LDA + tc * TC;
+    float* p = H + (tr + 32 * i) * L::LDA + tc * TC;
     ldv(p, hv);
 #pragma unroll
     for (int c = 0; c < TC; ++c) o[c] = acc[i][c] * (1.0f - hv[c] * hv[c]);
@@ -154,15 +155,17 @@ __device__ __forceinline__ void bwd_gemm(const float* __restrict__ G, float* __r
   }
 }
 
-// dW[o][i] += sum_b G[b][o] H[b][i]; thread owns a DB x DB block (registers).
+// dW[o][i] += sum_b G[b][o] H[b][i] over this thread's half of the rows; thread owns a
+// DB x DB block (registers); the two halves are summed at the flush.
 template <int W, int NH>
 __device__ __forceinline__ void dw_gemm(const float* __restrict__ G, const float* __restrict__ H,
                                         float (&dW)[Layout<W, NH>::DB * Layout<W, NH>::DB], int tid) {
   using L = Layout<W, NH>;
   constexpr int DB = L::DB;
-  const int to = tid >> 4, ti = tid & 15;
+  const int t = tid & 255, half = tid >> 8;
+  const int to = t >> 4, ti = t & 15;
 #pragma unroll 4
-  for (int b = 0; b < kB; ++b) {
+  for (int b = half * (kB / 2); b < (half + 1) * (kB / 2); ++b) {
     float g[DB], hv[DB];
     ldv(G + b * L::LDA + to * DB, g);
     ldv(H + b * L::LDA + ti * DB, hv);
@@ -194,6 +197,7 @@ __device__ __forceinline__ void colsum(const float* __restrict__ X, float* __res
 
 template <int W, int NH, bool TRAIN>
 __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
+  static_assert(kB % 32 == 0, "tile rows");
   using L = Layout<W, NH>;
   constexpr int NHH = L::NHH;
   constexpr int DB = L::DB;
@@ -245,16 +249,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
   };
   auto flush = [&](int net) {
     float* out = prm.part + ((int64_t)net * G + cta) * prm.p_stride;
-    const int to = tid >> 4, ti = tid & 15;
+    const int t = tid & 255, half = tid >> 8;
+    const int to = t >> 4, ti = t & 15;
+    float* scr = sAct;   // free between tiles: [256][NHH][DB*DB] partials of the second row-half
+    if (half == 1) {
 #pragma unroll
-    for (int l = 0; l < NHH; ++l)
+      for (int l = 0; l < NHH; ++l)
 #pragma unroll
-      for (int a = 0; a < DB; ++a) {
-        float v[DB];
+        for (int e = 0; e < DB * DB; ++e) scr[(t * (NHH > 0 ? NHH : 1) + l) * DB * DB + e] = dWh[l][e];
+    }
+    __syncthreads();
+    if (half == 0) {
 #pragma unroll
-        for (int c = 0; c < DB; ++c) v[c] = dWh[l][a * DB + c];
-        stv(out + L::tWl(l + 2) + (int64_t)(to * DB + a) * W + ti * DB, v);
-      }
+      for (int l = 0; l < NHH; ++l)
+#pragma unroll
+        for (int a = 0; a < DB; ++a) {
+          float v[DB];
+#pragma unroll
+          for (int c = 0; c < DB; ++c) v[c] = dWh[l][a * DB + c] + scr[(t * (NHH > 0 ? NHH : 1) + l) * DB * DB + a * DB + c];
+          stv(out + L::tWl(l + 2) + (int64_t)(to * DB + a) * W + ti * DB, v);
+        }
+    }
     for (int i = tid; i < 3 * W; i += kThreads) out[L::tW1 + i] = sAW1[i];
     for (int i = tid; i < W; i += kThreads) {
       out[L::tB1 + i] = sAB[i];
@@ -344,11 +359,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
     // ---- output layer u = wo . h_NH + bo ----
     float* hTop = sAct + (NH - 1) * kB * L::LDA;
     {
-      const int r = tid >> 1, half = tid & 1;
+      const int r = tid >> 2, qq = tid & 3;
       float s = 0.0f;
-      for (int k = half * (W / 2); k < (half + 1) * (W / 2); ++k) s = fmaf(sWo[k], hTop[r * L::LDA + k], s);
+      for (int k = qq * (W / 4); k < (qq + 1) * (W / 4); ++k) s = fmaf(sWo[k], hTop[r * L::LDA + k], s);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
-      if (half == 0) sU[r] = s + sWo[W];
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (qq == 0) sU[r] = s + sWo[W];
     }
     __syncthreads();
     if (!TRAIN) {
