@@ -541,9 +541,9 @@ static void bwd_tape(const orc_arch* a, const double* theta, int net, double cot
         if (gemm) { w = rbf16(w); dv = rbf16(dv); }
         acc = rnd(mode, acc + rnd(mode, w * dv));
       }
-      /* bf16 path (G16): tanh' of hidden layers 2..NH-1 is taken from the bf16 operand copy */
+      /* bf16 path (G16): tanh' of hidden layers 1..NH-1 is taken from the bf16 operand copy */
       double hv = T->h[l - 1][i];
-      if (mode == ORC_MODE_BF16 && l - 1 >= 2 && l - 1 <= L - 3) hv = rbf16(hv);
+      if (mode == ORC_MODE_BF16 && l - 1 <= L - 3) hv = rbf16(hv);
       dn[i] = rnd(mode, acc * rnd(mode, act_d(a->act, T->z[l - 1][i], hv)));
     }
     memcpy(dl, dn, sizeof(double) * fi);

@@ -2,25 +2,27 @@
 // with the hidden x hidden GEMMs on the 5th-generation tensor cores (tcgen05, bf16 in,
 // fp32 accumulate in TMEM), configs 3 / 5-w128 (SURVEY 8a S3-S5, 7.3 hard parts 3-5).
 //
-// One CTA per SM (128 threads = 4 warps; thread t owns tile row t = TMEM lane t) walks a
-// contiguous range of 128-row tiles (18 stencil points x 7 vertices, or 128 rows).
-// Per tile, for hidden width W and NH hidden layers:
-//   layer 1 (K = 3) on the CUDA cores -> bf16 h1 in shared memory (core-matrix layout)
-//   for l = 2..NH: tcgen05.mma  acc = h_{l-1} W_l^T  (M=128, N=W, K=W)  -> epilogue
-//       (TMEM -> registers: bias, tanh, bf16 -> shared memory) ...
-//   output layer u = wo . h_NH + bo in each thread's registers -> residual epilogue
+// One CTA per SM walks a contiguous range of 128-row tiles (18 stencil points x 7
+// vertices, or 128 independent rows).  4 * W/32 warps: warp w owns rows 32*(w%4)..+31
+// (its TMEM lane quadrant) and columns 32*(w/4)..+31 of every activation, so the
+// epilogues are spread over 16 warps at W = 128.  Per tile, for NH hidden layers:
+//   layer 1 (K = 3) on the CUDA cores -> bf16 h1 (shared memory, core-matrix layout)
+//   for l = 2..NH: tcgen05.mma  acc = h_{l-1} W_l^T   (M=128, N=W, K=W) -> epilogue
+//       (tcgen05.ld -> bias, tanh -> bf16 operand for the next GEMM)
+//   output layer u = wo . h_NH + bo (per-chunk partials) -> residual epilogue
 //   (r = M^-1 A u - M^-1 b; cotangents 2 r chat_j / N)
 //   backward: G_NH = u_bar wo (1 - h_NH^2);  for l = NH..2:
-//       tcgen05.mma  dW_l += G_l^T h_{l-1}   (M=W, N=W, K=128; dW stays in TMEM across
-//                                             all the CTA's tiles)
+//       tcgen05.mma  dW_l += G_l^T h_{l-1}   (M=W, N=W, K=128; dW stays in TMEM for all
+//                                             the CTA's tiles and is written out once)
 //       tcgen05.mma  acc   = G_l W_l          (M=128, N=W, K=W)
-//       epilogue G_{l-1} = acc * act'(h_{l-1}) -> bf16 shared memory
-//   layer-1 / output-layer / bias gradients: in-register warp transpose-reductions.
-// TMEM: columns [0,W) working accumulator, [W(l-1), W l) dW_l  (W * NH <= 512).
-// Shared memory (W=128, NH=4): 3 hidden weight matrices + 3 activation buffers in bf16,
-// 96 KB + 96 KB.  h1 is recomputed (K = 3) for dW_2 instead of being kept.
-// Rounding points (G16): GEMM operands bf16 (RNE), everything else fp32;
-// tanh' = 1 - h^2 from the bf16 operand copy for layers 2..NH-1, exact fp32 for 1 and NH.
+//       epilogue G_{l-1} = acc * (1 - h~_{l-1}^2) -> bf16 operand
+//   bias / layer-1 / output-layer gradients: warp transpose-reductions into registers.
+// TMEM columns: [0,W) working accumulator, [W(l-1), W l) dW_l  (W * NH <= 512).
+// Shared memory (W=128, NH=4): 3 bf16 hidden weight matrices + 3 bf16 activation
+// buffers = 192 KB.  h1 is recomputed (K = 3) for dW_2 instead of being kept.
+// Rounding points (G16): GEMM operands bf16 (RNE), accumulators and everything
+// else fp32; tanh' = 1 - h~^2 from the bf16 operand copy for hidden layers 1..NH-1,
+// exact fp32 for layer NH; activation = hardware tanh.approx.f32.
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -31,33 +33,33 @@ namespace nbm {
 
 namespace {
 
-constexpr int kTB = 128;        // rows per tile (= MMA M = TMEM lanes)
-constexpr int kTPT = 18;        // stencil points per tile
-constexpr int kTThreads = 128;  // 4 warps, one TMEM lane quadrant each
+constexpr int kTB = 128;   // rows per tile (= MMA M = TMEM lanes)
+constexpr int kTPT = 18;   // stencil points per tile
 
 template <int W, int NH>
 struct TcLayout {
   static constexpr int NHH = NH - 1;
+  static constexpr int CH = W / 32;                        // 32-column chunks per row
+  static constexpr int THREADS = 128 * CH;                 // 4 lane quadrants x CH chunks
   static constexpr int NBUF = NH - 1 > 2 ? NH - 1 : 2;
-  static constexpr int CH = W / 32;                         // 32-column chunks per row
-  static constexpr uint32_t ACT_BYTES = kTB * W * 2;        // one bf16 activation buffer
-  static constexpr uint32_t WMAT_BYTES = W * W * 2;         // one bf16 weight matrix
-  // byte offsets in dynamic shared memory (1024-aligned regions first)
+  static constexpr int NV = NH + 4;                        // small-gradient vectors
+  static constexpr uint32_t ACT_BYTES = kTB * W * 2;       // one bf16 activation buffer
+  static constexpr uint32_t WMAT_BYTES = W * W * 2;        // one bf16 weight matrix
   static constexpr uint32_t oAct = 0;
   static constexpr uint32_t oWh = oAct + NBUF * ACT_BYTES;
-  static constexpr uint32_t oW1 = oWh + NHH * WMAT_BYTES;   // fp32 [W][3]
-  static constexpr uint32_t oBias = oW1 + 4 * 3 * W;        // fp32 [NH][W]
-  static constexpr uint32_t oWo = oBias + 4 * NH * W;       // fp32 [W] + bo
-  static constexpr uint32_t oX = oWo + 4 * (W + 4);         // fp32 [kTB][4]
-  static constexpr uint32_t oU = oX + 4 * 4 * kTB;          // fp32 [kTB]
-  static constexpr uint32_t oUb = oU + 4 * kTB;             // fp32 [kTB]
-  static constexpr uint32_t oAux = oUb + 4 * kTB;           // fp32 [kTB]
-  static constexpr uint32_t oItem = oAux + 4 * kTB;         // int  [kTB]
-  static constexpr int NV = NH + 4;                         // small-gradient vectors
-  static constexpr uint32_t oSmall = oItem + 4 * kTB;       // fp32 [4 warps][NV][W] + [4] bo
-  static constexpr uint32_t oBar = oSmall + 4 * (4 * NV * W + 4);   // mbarrier (8 B) + tmem base
+  static constexpr uint32_t oW1 = oWh + NHH * WMAT_BYTES;  // fp32 [W][3]
+  static constexpr uint32_t oBias = oW1 + 4 * 3 * W;       // fp32 [NH][W]
+  static constexpr uint32_t oWo = oBias + 4 * NH * W;      // fp32 [W] + bo
+  static constexpr uint32_t oX = oWo + 4 * (W + 4);        // fp32 [kTB][4]
+  static constexpr uint32_t oUp = oX + 4 * 4 * kTB;        // fp32 [CH][kTB] u partials
+  static constexpr uint32_t oU = oUp + 4 * CH * kTB;       // fp32 [kTB]
+  static constexpr uint32_t oUb = oU + 4 * kTB;            // fp32 [kTB]
+  static constexpr uint32_t oAux = oUb + 4 * kTB;          // fp32 [kTB]
+  static constexpr uint32_t oItem = oAux + 4 * kTB;        // int  [kTB]
+  static constexpr uint32_t oBar = oItem + 4 * kTB;        // mbarrier (8 B) + tmem base
   static constexpr uint32_t bytes = oBar + 64;
   static constexpr uint32_t TMEM_COLS = (W * NH <= 128) ? 128 : (W * NH <= 256) ? 256 : 512;
+  static_assert(4 * (4 * NV * W + 4) <= (int)ACT_BYTES * NBUF, "flush scratch");
   // theta offsets within one network (G17)
   static constexpr int64_t tW1 = 0, tB1 = 3 * W;
   __host__ __device__ static constexpr int64_t tWl(int l) { return 4 * W + (int64_t)(l - 2) * (W * W + W); }
@@ -66,8 +68,8 @@ struct TcLayout {
   static constexpr int64_t tBo = tWo + W;
 };
 
-// core-matrix (8 x 16 B) layout of an [R][C] bf16 tile: element (r, c) at
-// (c/8) * R*16 + r*16 + (c%8)*2 bytes.
+// core-matrix (8 rows x 16 B) layout of an [R][C] bf16 tile: element (r, c) at
+// (c/8)*R*16 + r*16 + (c%8)*2 bytes.
 __device__ __forceinline__ uint32_t core_off(int R, int r, int c8) { return (uint32_t)(c8 * R * 16 + r * 16); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -78,7 +80,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 __device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
-// lane j of the warp receives sum over the warp's 32 rows of v[j] (fixed butterfly order)
+// bf16 path activation: MUFU tanh.approx.f32 (max relative error 2^-10.99, below the bf16
+// operand rounding; the fp32 configs use the accurate tanhf, G15).
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// lane j of the warp receives the sum over the warp's 32 rows of v[j] (fixed butterfly)
 __device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
 #pragma unroll
   for (int s = 16; s >= 1; s >>= 1) {
@@ -93,14 +103,6 @@ __device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
   return v[0];
 }
 
-// bf16 path activation: MUFU tanh.approx.f32 (max relative error 2^-10.99, below the bf16
-// operand rounding; the fp32 configs use the accurate tanhf, G15).
-__device__ __forceinline__ float tanh_fast(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -108,19 +110,42 @@ __device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t& a, uint32_
   asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr) : "memory");
 }
 
+// one thread's 32 columns of a row -> bf16 core-matrix buffer
+__device__ __forceinline__ void store_chunk_bf16(uint32_t buf, int row, int chunk, const float (&h)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    st_shared_v4(buf + core_off(kTB, row, chunk * 4 + q), pack_bf16(h[8 * q], h[8 * q + 1]),
+                 pack_bf16(h[8 * q + 2], h[8 * q + 3]), pack_bf16(h[8 * q + 4], h[8 * q + 5]),
+                 pack_bf16(h[8 * q + 6], h[8 * q + 7]));
+}
+__device__ __forceinline__ void load_chunk_bf16(uint32_t buf, int row, int chunk, float (&h)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t w[4];
+    ld_shared_v4(buf + core_off(kTB, row, chunk * 4 + q), w[0], w[1], w[2], w[3]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      h[8 * q + 2 * e] = bf_lo(w[e]);
+      h[8 * q + 2 * e + 1] = bf_hi(w[e]);
+    }
+  }
+}
+
 }  // namespace
 
 template <int W, int NH, bool TRAIN>
-__global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
+__global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const MlpParams prm) {
   using L = TcLayout<W, NH>;
-  constexpr int CH = L::CH;
   constexpr int NHH = L::NHH;
+  constexpr int NV = L::NV;
+  constexpr int THREADS = L::THREADS;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = tc::smem_u32(smem);
   float* sW1 = reinterpret_cast<float*>(smem + L::oW1);
   float* sBias = reinterpret_cast<float*>(smem + L::oBias);
   float* sWo = reinterpret_cast<float*>(smem + L::oWo);
   float* sX = reinterpret_cast<float*>(smem + L::oX);
+  float* sUp = reinterpret_cast<float*>(smem + L::oUp);
   float* sU = reinterpret_cast<float*>(smem + L::oU);
   float* sUb = reinterpret_cast<float*>(smem + L::oUb);
   float* sAux = reinterpret_cast<float*>(smem + L::oAux);
@@ -130,6 +155,10 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
   __shared__ int segTiles[kNumSeg], segCnt[kNumSeg], segStart[kNumSeg];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quad = warp & 3, chunk = warp >> 2;
+  const int row = quad * 32 + lane;                       // tile row = TMEM lane
+  const uint32_t tlane = (uint32_t)(quad * 32) << 16;
+  const uint32_t ccol = (uint32_t)(chunk * 32);            // this thread's column chunk
   if (tid < kNumSeg) {
     int c = prm.counts[prm.cnt_slot[tid]];
     segCnt[tid] = c;
@@ -146,7 +175,6 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *sTmem;
-  const uint32_t tlane = (uint32_t)(warp * 32) << 16;   // this warp's TMEM lane quadrant
 
   int firstTile[kNumSeg + 1];
   int total = 0;
@@ -156,7 +184,6 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
   const int G = gridDim.x, cta = blockIdx.x;
   const int t0 = (int)((int64_t)total * cta / G), t1 = (int)((int64_t)total * (cta + 1) / G);
 
-  // descriptors' constant parts
   constexpr uint32_t LBO_ACT = kTB * 16, LBO_W = W * 16;
   const uint32_t aAct = sbase + L::oAct, aWh = sbase + L::oWh;
   constexpr uint32_t ID_FWD = tc::idesc_bf16(kTB, W, 0, 0);   // A K-major, B K-major
@@ -164,74 +191,63 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
   constexpr uint32_t ID_DW = tc::idesc_bf16(W, W, 1, 1);      // A MN-major, B MN-major
   uint32_t phase = 0;
 
-  // small gradients (b_l, W1, wo, bo): per-warp partials in shared memory, column =
-  // chunk*32 + lane after a warp transpose-reduction of the warp's 32 rows
-  constexpr int NV = L::NV;
-  float* sSmall = reinterpret_cast<float*>(smem + L::oSmall);
-  float* mySmall = sSmall + warp * NV * W;
-  auto small_add = [&](int vec, int c, float val) { mySmall[vec * W + c * 32 + lane] += val; };
-  // vectors: 0..NH-1 = b_1..b_NH, NH..NH+2 = W1[:, 0..2], NH+3 = wo
+  // small gradients, lane = column chunk*32 + lane, this warp's 32 rows:
+  // g[0..NH-1] = b_1..b_NH, g[NH..NH+2] = W1[:, 0..2], g[NH+3] = wo; gbo = bo (chunk 0)
+  float g[NV];
+  float gbo = 0.0f;
   double lossAcc = 0.0;
   int curNet = -1;
   bool touched[2] = {false, false};
   bool dwFresh = true;
 
-  auto zero_small = [&]() {
-    for (int i = tid; i < 4 * NV * W + 4; i += kTThreads) sSmall[i] = 0.0f;
-  };
-
   auto flush = [&](int net) {
     float* out = prm.part + ((int64_t)net * G + cta) * prm.p_stride;
-    // dW_l rows: TMEM lane = output unit o, columns = input unit i
     if (!dwFresh) {
       tc::tc_fence_after();
 #pragma unroll 1
       for (int l = 2; l <= NH; ++l) {
-        const int o = warp * 32 + lane;
-#pragma unroll 1
-        for (int c = 0; c < CH; ++c) {
-          float v[32];
-          tc::tmem_ld32(tmem + tlane + (uint32_t)(W * (l - 1) + c * 32), v);
-          if (o < W) {
-            float4* dst = reinterpret_cast<float4*>(out + L::tWl(l) + (int64_t)o * W + c * 32);
+        float v[32];
+        tc::tmem_ld32(tmem + tlane + (uint32_t)(W * (l - 1)) + ccol, v);   // dW_l[o = row][i]
+        float4* dst = reinterpret_cast<float4*>(out + L::tWl(l) + (int64_t)row * W + ccol);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          }
-        }
+        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       }
     } else {
       for (int l = 2; l <= NH; ++l)
-        for (int i = tid; i < W * W; i += kTThreads) out[L::tWl(l) + i] = 0.0f;
+        for (int i = tid; i < W * W; i += THREADS) out[L::tWl(l) + i] = 0.0f;
     }
-    // small gradients: sum the 4 warps' partials in fixed order
-    const float* scr = sSmall;
+    // small gradients: 4 quadrant-warps per column chunk, summed in quadrant order
+    float* scr = reinterpret_cast<float*>(smem + L::oAct);   // [4][NV][W] + [4] bo
     __syncthreads();
-    for (int i = tid; i < NV * W; i += kTThreads) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) scr[(quad * NV + v) * W + ccol + lane] = g[v];
+    if (chunk == 0 && lane == 0) scr[4 * NV * W + quad] = gbo;
+    __syncthreads();
+    for (int i = tid; i < NV * W; i += THREADS) {
       const int v = i / W, col = i % W;
-      float s = 0.0f;
-      for (int w = 0; w < 4; ++w) s += scr[(w * NV + v) * W + col];
+      const float s = ((scr[(0 * NV + v) * W + col] + scr[(1 * NV + v) * W + col]) + scr[(2 * NV + v) * W + col]) +
+                      scr[(3 * NV + v) * W + col];
       if (v < NH) out[(v == 0 ? L::tB1 : L::tBl(v + 1)) + col] = s;
       else if (v < NH + 3) out[L::tW1 + 3 * col + (v - NH)] = s;
       else out[L::tWo + col] = s;
     }
-    if (tid == 0) out[L::tBo] = scr[4 * NV * W] + scr[4 * NV * W + 1] + scr[4 * NV * W + 2] + scr[4 * NV * W + 3];
+    if (tid == 0) out[L::tBo] = ((scr[4 * NV * W] + scr[4 * NV * W + 1]) + scr[4 * NV * W + 2]) + scr[4 * NV * W + 3];
     __syncthreads();
     touched[net] = true;
   };
 
   auto load_net = [&](int net) {
     const float* th = prm.theta + (int64_t)net * prm.p_net;
-    for (int i = tid; i < 3 * W; i += kTThreads) sW1[i] = th[L::tW1 + i];
-    for (int i = tid; i < W; i += kTThreads) {
+    for (int i = tid; i < 3 * W; i += THREADS) sW1[i] = th[L::tW1 + i];
+    for (int i = tid; i < W; i += THREADS) {
       sBias[i] = th[L::tB1 + i];
       for (int l = 2; l <= NH; ++l) sBias[(l - 1) * W + i] = th[L::tBl(l) + i];
       sWo[i] = th[L::tWo + i];
     }
     if (tid == 0) sWo[W] = th[L::tBo];
-    // hidden weights -> bf16 core-matrix layout ([o][i], R = W rows)
-    for (int l = 0; l < NHH; ++l) {
+    for (int l = 0; l < NHH; ++l) {   // hidden weights -> bf16 core-matrix layout ([o][i], R = W)
       const float* Wl = th + L::tWl(l + 2);
-      for (int q = tid; q < W * (W / 8); q += kTThreads) {
+      for (int q = tid; q < W * (W / 8); q += THREADS) {
         const int o = q / (W / 8), c8 = q % (W / 8);
         const float* src = Wl + (int64_t)o * W + c8 * 8;   // net+ theta is not 16-B aligned
         st_shared_v4(aWh + l * L::WMAT_BYTES + core_off(W, o, c8), pack_bf16(src[0], src[1]),
@@ -239,9 +255,12 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
       }
     }
     tc::fence_proxy_async_smem();
+#pragma unroll
+    for (int v = 0; v < NV; ++v) g[v] = 0.0f;
+    gbo = 0.0f;
   };
 
-  // issue one GEMM of K = kdim (steps of 16) on the tensor core (single thread)
+  // one GEMM of ksteps x K=16 on the tensor core (single thread)
   auto gemm = [&](uint32_t dcol, uint32_t a0, uint32_t a_step, uint32_t a_lbo, uint32_t a_sbo, uint32_t b0,
                   uint32_t b_step, uint32_t b_lbo, uint32_t b_sbo, uint32_t idesc, int ksteps, bool acc) {
 #pragma unroll 1
@@ -249,22 +268,19 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
       tc::mma_bf16(tmem + dcol, tc::sdesc(a0 + s * a_step, a_lbo, a_sbo), tc::sdesc(b0 + s * b_step, b_lbo, b_sbo),
                    idesc, (acc || s > 0) ? 1u : 0u);
   };
-
-  // this thread's row: layer 1 for columns [c*32, c*32+32): z = W1 x + b1
-  auto layer1 = [&](int c, float x0, float x1, float x2, float (&h)[32]) {
+  auto wait_mma = [&]() {
+    tc::mbar_wait(bar, phase);
+    phase ^= 1;
+    tc::tc_fence_after();
+  };
+  // layer 1 for this thread's 32 columns: h = tanh(W1 x + b1)
+  auto layer1 = [&](float x0, float x1, float x2, float (&h)[32]) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const int n = c * 32 + j;
+      const int n = ccol + j;
       const float z = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, fmaf(sW1[3 * n], x0, sBias[n])));
       h[j] = tanh_fast(z);
     }
-  };
-  auto store_row_bf16 = [&](uint32_t buf, int c, const float (&h)[32]) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      st_shared_v4(buf + core_off(kTB, tid, c * 4 + q), pack_bf16(h[8 * q], h[8 * q + 1]),
-                   pack_bf16(h[8 * q + 2], h[8 * q + 3]), pack_bf16(h[8 * q + 4], h[8 * q + 5]),
-                   pack_bf16(h[8 * q + 6], h[8 * q + 7]));
   };
 
   int seg = 0;
@@ -278,12 +294,11 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
     if (net != curNet) {
       if (TRAIN && curNet >= 0) flush(curNet);
       load_net(net);
-      if (TRAIN) zero_small();
       dwFresh = true;
       curNet = net;
       __syncthreads();
     }
-    // ---- gather ----
+    // ---- gather: items, aux, the row's coordinates ----
     const int* items = prm.seg.items[seg] + segStart[seg];
     if (tid < per) {
       const int it = tid < nvalid ? items[first + tid] : -1;
@@ -293,32 +308,34 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
       sAux[tid] = a;
     }
     __syncthreads();
-    float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
-    if (kind == kSegStencil) {
-      const int j = tid / kTPT, p = tid - j * kTPT;
-      if (j < 7 && p < nvalid) {
-        const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[p];
-        x0 = src[0]; x1 = src[1]; x2 = src[2];
-        if (j > 0) {
-          const float hs = (j & 1) ? prm.h : -prm.h;
-          if (j <= 2) x0 = __fadd_rn(x0, hs); else if (j <= 4) x1 = __fadd_rn(x1, hs); else x2 = __fadd_rn(x2, hs);
+    if (tid < kTB) {
+      float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
+      if (kind == kSegStencil) {
+        const int j = tid / kTPT, p = tid - j * kTPT;
+        if (j < 7 && p < nvalid) {
+          const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[p];
+          x0 = src[0]; x1 = src[1]; x2 = src[2];
+          if (j > 0) {   // arms +x, -x, +y, -y, +z, -z (exact on the lattice)
+            const float hs = (j & 1) ? prm.h : -prm.h;
+            if (j <= 2) x0 = __fadd_rn(x0, hs); else if (j <= 4) x1 = __fadd_rn(x1, hs); else x2 = __fadd_rn(x2, hs);
+          }
         }
+      } else if (tid < nvalid) {
+        const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[tid];
+        x0 = src[0]; x1 = src[1]; x2 = src[2];
       }
-    } else if (tid < nvalid) {
-      const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[tid];
-      x0 = src[0]; x1 = src[1]; x2 = src[2];
+      sX[4 * tid] = x0; sX[4 * tid + 1] = x1; sX[4 * tid + 2] = x2;
     }
-    // ---- layer 1 -> bf16 h1 (buffer 0) ----
-#pragma unroll 1
-    for (int c = 0; c < CH; ++c) {
+    __syncthreads();
+    const float x0 = sX[4 * row], x1 = sX[4 * row + 1], x2 = sX[4 * row + 2];
+    {  // ---- layer 1 -> bf16 h1 (buffer 0) ----
       float h[32];
-      layer1(c, x0, x1, x2, h);
-      store_row_bf16(aAct, c, h);
+      layer1(x0, x1, x2, h);
+      store_chunk_bf16(aAct, row, chunk, h);
     }
     tc::fence_proxy_async_smem();
     __syncthreads();
-    // ---- hidden layers 2..NH (tensor cores) ----
-    float u = 0.0f;
+    // ---- hidden layers 2..NH on the tensor cores ----
 #pragma unroll 1
     for (int l = 2; l <= NH; ++l) {
       if (tid == 0) {
@@ -327,37 +344,36 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
              LBO_W, 128, ID_FWD, W / 16, false);
         tc::mma_commit(bar);
       }
-      tc::mbar_wait(bar, phase);
-      phase ^= 1;
-      tc::tc_fence_after();
-      const float* bl = sBias + (l - 1) * W;
-#pragma unroll 1
-      for (int c = 0; c < CH; ++c) {
-        float v[32];
-        tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
+      wait_mma();
+      float v[32];
+      tc::tmem_ld32(tmem + tlane + ccol, v);
+      const float* bl = sBias + (l - 1) * W + ccol;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = tanh_fast(v[j] + bl[c * 32 + j]);
-        if (l < NH) {
-          store_row_bf16(aAct + (l - 1) * L::ACT_BYTES, c, v);
-        } else {
+      for (int j = 0; j < 32; ++j) v[j] = tanh_fast(v[j] + bl[j]);
+      if (l < NH) {
+        store_chunk_bf16(aAct + (l - 1) * L::ACT_BYTES, row, chunk, v);
+        tc::fence_proxy_async_smem();
+      } else {
+        float up = 0.0f;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) u = fmaf(sWo[c * 32 + j], v[j], u);
-          if (TRAIN) tc::tmem_st32(tmem + tlane + (uint32_t)(c * 32), v);   // keep fp32 h_NH for backward
-        }
+        for (int j = 0; j < 32; ++j) up = fmaf(sWo[ccol + j], v[j], up);
+        sUp[chunk * kTB + row] = up;
+        if (TRAIN) tc::tmem_st32(tmem + tlane + ccol, v);   // keep fp32 h_NH for the backward
       }
       tc::tc_fence_before();
-      if (l < NH) tc::fence_proxy_async_smem();
       __syncthreads();
     }
-    u += sWo[W];
-    if (!TRAIN) {
-      if (tid < nvalid) prm.u_out[sItem[tid]] = u;
-      __syncthreads();
-      continue;
+    if (tid < kTB) {
+      float u = sUp[tid];
+#pragma unroll
+      for (int c = 1; c < L::CH; ++c) u += sUp[c * kTB + tid];
+      u += sWo[W];
+      if (!TRAIN && tid < nvalid) prm.u_out[sItem[tid]] = u;
+      sU[tid] = u;
     }
-    sU[tid] = u;
     __syncthreads();
-    // ---- residual epilogue -> cotangents ----
+    if (!TRAIN) continue;
+    // ---- residual epilogue -> cotangents (S4) ----
     if (kind == kSegStencil) {
       if (tid < kTPT) {
         float r = 0.0f;
@@ -374,10 +390,10 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
         const float rj = rc * prm.seg.chat[seg];
 #pragma unroll
         for (int j = 1; j < 7; ++j) sUb[j * kTPT + tid] = rj;
-      } else if (tid >= 7 * kTPT) {
+      } else if (tid >= 7 * kTPT && tid < kTB) {
         sUb[tid] = 0.0f;
       }
-    } else {
+    } else if (tid < kTB) {
       float ub = 0.0f;
       if (tid < nvalid) {
         if (kind == kSegBRows) {
@@ -391,27 +407,25 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
       sUb[tid] = ub;
     }
     __syncthreads();
-    const float ub = sUb[tid];
-    {  // output bias
+    const float ub = sUb[row];
+    if (chunk == 0) {   // output bias
       float b = ub;
 #pragma unroll
       for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
-      if (lane == 0) sSmall[4 * NV * W + warp] += b;
+      gbo += b;
     }
-    // ---- output layer backward: G_NH = ub wo (1 - h^2) -> bf16 ----
+    // ---- output layer backward: dwo += ub h_NH; G_NH = ub wo (1 - h_NH^2) -> bf16 ----
     const uint32_t gbufNH = (NH == 2) ? aAct + L::ACT_BYTES : aAct;
-    tc::tc_fence_after();
-#pragma unroll 1
-    for (int c = 0; c < CH; ++c) {
+    {
       float hv[32], v[32];
-      tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), hv);
+      tc::tmem_ld32(tmem + tlane + ccol, hv);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = ub * hv[j];
-      small_add(NH + 3, c, warp_transpose_sum(v, lane));
+      g[NH + 3] += warp_transpose_sum(v, lane);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
-      store_row_bf16(gbufNH, c, hv);
-      small_add(NH - 1, c, warp_transpose_sum(hv, lane));
+      for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[ccol + j] * (1.0f - hv[j] * hv[j]);
+      store_chunk_bf16(gbufNH, row, chunk, hv);
+      g[NH - 1] += warp_transpose_sum(hv, lane);
     }
     tc::tc_fence_before();
     tc::fence_proxy_async_smem();
@@ -429,78 +443,52 @@ __global__ void __launch_bounds__(kTThreads, 1) k_mlp_tc(const MlpParams prm) {
         gemm(0, gbuf, 2 * LBO_ACT, LBO_ACT, 128, aWh + (l - 2) * L::WMAT_BYTES, 256, 128, LBO_W, ID_DH, W / 16, false);
         tc::mma_commit(bar);
       }
-      tc::mbar_wait(bar, phase);
-      phase ^= 1;
-      tc::tc_fence_after();
+      wait_mma();
+      // G_{l-1} = acc * (1 - h~^2), h~ = the bf16 operand copy of h_{l-1} (own row, chunk)
+      float v[32], hq[32];
+      tc::tmem_ld32(tmem + tlane + ccol, v);
+      load_chunk_bf16(hbuf, row, chunk, hq);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= 1.0f - hq[j] * hq[j];
       if (l - 1 >= 2) {
-        // G_{l-1} = acc * (1 - h~^2), h~ = bf16 h_{l-1} (own row), written in place
-#pragma unroll 1
-        for (int c = 0; c < CH; ++c) {
-          float v[32];
-          tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t w0, w1, w2, w3;
-            const uint32_t adr = hbuf + core_off(kTB, tid, c * 4 + q);
-            ld_shared_v4(adr, w0, w1, w2, w3);
-            const uint32_t ws[4] = {w0, w1, w2, w3};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float a = bf_lo(ws[e]), b = bf_hi(ws[e]);
-              v[8 * q + 2 * e] *= 1.0f - a * a;
-              v[8 * q + 2 * e + 1] *= 1.0f - b * b;
-            }
-          }
-          store_row_bf16(hbuf, c, v);
-          small_add(l - 2, c, warp_transpose_sum(v, lane));
+        store_chunk_bf16(hbuf, row, chunk, v);   // in place: h_{l-1} is consumed
+        g[l - 2] += warp_transpose_sum(v, lane);
+        if (l - 1 == 2 && NH >= 3) {   // h1 again for dW_2 (buffer 0's G_NH is consumed)
+          float h[32];
+          layer1(x0, x1, x2, h);
+          store_chunk_bf16(aAct, row, chunk, h);
         }
-        if (l - 1 == 2 && NH >= 3) {   // h1 again for dW_2 (buffer 0 is free: G_NH consumed)
-#pragma unroll 1
-          for (int c = 0; c < CH; ++c) {
-            float h[32];
-            layer1(c, x0, x1, x2, h);
-            store_row_bf16(aAct, c, h);
-          }
-        }
-        tc::tc_fence_before();
         tc::fence_proxy_async_smem();
-        __syncthreads();
       } else {
-        // layer 1: G1 = acc * (1 - h1^2) (exact fp32 h1); dW1 += G1 x^T; db1 += G1
-#pragma unroll 1
-        for (int c = 0; c < CH; ++c) {
-          float v[32], h[32], t[32];
-          tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
-          layer1(c, x0, x1, x2, h);
+        // layer 1: G1 -> dW1 += G1 x^T, db1 += G1
+        float tv[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= 1.0f - h[j] * h[j];
+        for (int j = 0; j < 32; ++j) tv[j] = v[j] * x0;
+        g[NH + 0] += warp_transpose_sum(tv, lane);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) t[j] = v[j] * x0;
-          small_add(NH + 0, c, warp_transpose_sum(t, lane));
+        for (int j = 0; j < 32; ++j) tv[j] = v[j] * x1;
+        g[NH + 1] += warp_transpose_sum(tv, lane);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) t[j] = v[j] * x1;
-          small_add(NH + 1, c, warp_transpose_sum(t, lane));
-#pragma unroll
-          for (int j = 0; j < 32; ++j) t[j] = v[j] * x2;
-          small_add(NH + 2, c, warp_transpose_sum(t, lane));
-          small_add(0, c, warp_transpose_sum(v, lane));
-        }
-        tc::tc_fence_before();
-        __syncthreads();
+        for (int j = 0; j < 32; ++j) tv[j] = v[j] * x2;
+        g[NH + 2] += warp_transpose_sum(tv, lane);
+        g[0] += warp_transpose_sum(v, lane);
       }
+      tc::tc_fence_before();
+      __syncthreads();
     }
     dwFresh = false;
   }
   if (TRAIN) {
     if (curNet >= 0) flush(curNet);
     if (tid < 2) prm.touched[tid * G + cta] = touched[tid] ? 1 : 0;
+#pragma unroll
     for (int o = 16; o; o >>= 1) lossAcc += __shfl_xor_sync(0xffffffffu, lossAcc, o);
-    __shared__ double wl[kTThreads / 32];
+    __shared__ double wl[32];
     if (lane == 0) wl[warp] = lossAcc;
     __syncthreads();
     if (tid == 0) {
       double s = 0.0;
-      for (int w = 0; w < kTThreads / 32; ++w) s += wl[w];
+      for (int w = 0; w < THREADS / 32; ++w) s += wl[w];
       prm.lpart[cta] = s;
     }
   }
@@ -520,7 +508,7 @@ static cudaError_t launch_tc_t(const MlpParams& p, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<grid, kTThreads, L::bytes, s>>>(p);
+  kern<<<grid, L::THREADS, L::bytes, s>>>(p);
   return cudaGetLastError();
 }
 
