@@ -525,13 +525,18 @@ static void bwd_tape(const orc_arch* a, const double* theta, int net, double cot
     double* gW = grad + off[l];
     double* gb = gW + (int64_t)fi * fo;
     int gemm = (mode == ORC_MODE_BF16) && l >= 2 && l <= L - 2;
+    /* bf16 path (G16): the bias gradients of hidden layers 1..NH-1 and the layer-1 weight
+     * gradient are tensor-core reductions of the bf16 delta; layer-1 inputs enter as a
+     * two-term bf16 split x = bf16(x) + bf16(x - bf16(x)). */
+    int tail = (mode == ORC_MODE_BF16) && l <= L - 3;
     for (int o = 0; o < fo; ++o) {                     /* dW_l += delta_l h_{l-1}^T, db_l += delta_l */
-      double dv = gemm ? rbf16(dl[o]) : dl[o];
+      double dv = (gemm || (tail && l == 1)) ? rbf16(dl[o]) : dl[o];
       for (int i = 0; i < fi; ++i) {
         double hv = gemm ? rbf16(T->h[l - 1][i]) : T->h[l - 1][i];
+        if (tail && l == 1) { double hi = rbf16(hv); hv = hi + rbf16(hv - hi); }
         gW[(int64_t)o * fi + i] += rnd(mode, dv * hv);
       }
-      gb[o] += dl[o];
+      gb[o] += tail ? rbf16(dl[o]) : dl[o];
     }
     if (l == 1) break;
     for (int i = 0; i < fi; ++i) {                     /* delta_{l-1} = (W_l^T delta_l) . act'(z_{l-1}) */
@@ -541,10 +546,16 @@ static void bwd_tape(const orc_arch* a, const double* theta, int net, double cot
         if (gemm) { w = rbf16(w); dv = rbf16(dv); }
         acc = rnd(mode, acc + rnd(mode, w * dv));
       }
-      /* bf16 path (G16): tanh' of hidden layers 1..NH-1 is taken from the bf16 operand copy */
-      double hv = T->h[l - 1][i];
-      if (mode == ORC_MODE_BF16 && l - 1 <= L - 3) hv = rbf16(hv);
-      dn[i] = rnd(mode, acc * rnd(mode, act_d(a->act, T->z[l - 1][i], hv)));
+      /* bf16 path (G16): tanh' of hidden layers 1..NH-1 from the bf16 operand copy of h;
+       * SiLU' of hidden layers 2..NH-1 stored (rounded) in bf16; others exact */
+      double hv = T->h[l - 1][i], ad;
+      if (mode == ORC_MODE_BF16 && l - 1 <= L - 3 && a->act == ORC_ACT_TANH)
+        ad = act_d(a->act, T->z[l - 1][i], rbf16(hv));
+      else if (mode == ORC_MODE_BF16 && l - 1 >= 2 && l - 1 <= L - 3 && a->act == ORC_ACT_SILU)
+        ad = rbf16(act_d(a->act, T->z[l - 1][i], hv));
+      else
+        ad = act_d(a->act, T->z[l - 1][i], hv);
+      dn[i] = rnd(mode, acc * rnd(mode, ad));
     }
     memcpy(dl, dn, sizeof(double) * fi);
   }

