@@ -68,6 +68,10 @@ struct TcLayout {
   static constexpr uint32_t oBar = oItem + 4 * kTB;        // mbarriers (MMA, weights) + tmem base
   static constexpr uint32_t bytes = oBar + 64;
   static constexpr uint32_t TMEM_COLS = (W * NH <= 128) ? 128 : (W * NH <= 256) ? 256 : 512;
+  static constexpr int MINB = (TMEM_COLS <= 256) ? 2 : 1;  // CTAs per SM (TMEM / smem permitting)
+  static constexpr int MDW = W < 128 ? 128 : W;            // M of the dW / tail MMAs: rows o >= W of
+                                                           // the MN-major A run into the next buffer
+                                                           // and land in TMEM lanes that are never read
   static_assert(4 * (4 * 2 * W + 4) <= (int)ACT_BYTES * NBUF, "flush scratch");
   // theta offsets within one network (G17)
   static constexpr int64_t tW1 = 0, tB1 = 3 * W;
@@ -160,7 +164,7 @@ __device__ long long g_tc_trace[8][32];
 #endif
 
 template <int W, int NH, int ACT, bool TRAIN>
-__global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, 1) k_mlp_tc(const MlpParams prm) {
+__global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH, ACT>::MINB) k_mlp_tc(const MlpParams prm) {
   using L = TcLayout<W, NH, ACT>;
   constexpr bool SILU = L::SILU, STREAM = L::STREAM;
   constexpr int NHH = L::NHH;
@@ -217,8 +221,8 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, 1) k_mlp_tc(con
   const uint32_t aAct = sbase + L::oAct, aWh = sbase + L::oWh;
   constexpr uint32_t ID_FWD = tc::idesc_bf16(kTB, W, 0, 0);   // A K-major, B K-major
   constexpr uint32_t ID_DH = tc::idesc_bf16(kTB, W, 0, 1);    // A K-major, B MN-major
-  constexpr uint32_t ID_DW = tc::idesc_bf16(W, W, 1, 1);      // A MN-major, B MN-major
-  constexpr uint32_t ID_TAIL = tc::idesc_bf16(W, 16, 1, 1);   // M = W, N = 16, both MN-major
+  constexpr uint32_t ID_DW = tc::idesc_bf16(L::MDW, W, 1, 1);    // A MN-major, B MN-major
+  constexpr uint32_t ID_TAIL = tc::idesc_bf16(L::MDW, 16, 1, 1); // M = W, N = 16, both MN-major
   const uint32_t aOnes = sbase + L::oOnes, aXm = sbase + L::oXm;
   uint32_t phase = 0;
   // streamed weights (SiLU): the stage holds W_{wl} of net wnet once wbar completes
@@ -271,16 +275,18 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, 1) k_mlp_tc(con
       for (int l = 2; l <= NH; ++l) {
         float v[32];
         tc::tmem_ld32(tmem + tlane + (uint32_t)(W * (l - 1)) + ccol, v);   // dW_l[o = row][i]
-        float4* dst = reinterpret_cast<float4*>(out + L::tWl(l) + (int64_t)row * W + ccol);
+        if (row < W) {
+          float4* dst = reinterpret_cast<float4*>(out + L::tWl(l) + (int64_t)row * W + ccol);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
       }
     } else {
       for (int l = 2; l <= NH; ++l)
         for (int i = tid; i < W * W; i += THREADS) out[L::tWl(l) + i] = 0.0f;
     }
     // tensor-core reduced gradients: one thread per unit o (chunk-0 warps)
-    if (chunk == 0) {
+    if (chunk == 0 && row < W) {
       const int o = row;
 #pragma unroll
       for (int l = 2; l <= NH - 1; ++l) out[L::tBl(l) + o] = tg[l - 2];
@@ -662,7 +668,7 @@ static cudaError_t launch_tc_t(const MlpParams& p, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<grid, L::THREADS, L::bytes, s>>>(p);
+  kern<<<grid * L::MINB, L::THREADS, L::bytes, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -673,18 +679,24 @@ extern "C" int nbm_debug_tc_trace(long long* out) {
 #endif
 
 int mlp_tc_supported(int width, int n_hidden, int act) {
-  return width == 128 && n_hidden >= 2 && n_hidden <= 4 && (act == NBM_ACT_TANH || act == NBM_ACT_SILU);
+  return (width == 64 || width == 128) && n_hidden >= 2 && n_hidden <= 4 &&
+         (act == NBM_ACT_TANH || act == NBM_ACT_SILU);
 }
+
+// CTAs per SM of the tensor-core kernel (2 when a CTA needs <= 256 TMEM columns)
+int mlp_tc_ctas_per_sm(int width, int n_hidden) { return width * n_hidden <= 256 ? 2 : 1; }
 
 template <int ACT>
 static cudaError_t launch_tc_act(int width, int n_hidden, bool train, const MlpParams& p, int grid, cudaStream_t s) {
-  if (width == 128) {
-    switch (n_hidden) {
-      case 2: return train ? launch_tc_t<128, 2, ACT, true>(p, grid, s) : launch_tc_t<128, 2, ACT, false>(p, grid, s);
-      case 3: return train ? launch_tc_t<128, 3, ACT, true>(p, grid, s) : launch_tc_t<128, 3, ACT, false>(p, grid, s);
-      case 4: return train ? launch_tc_t<128, 4, ACT, true>(p, grid, s) : launch_tc_t<128, 4, ACT, false>(p, grid, s);
-    }
+#define NBM_TC_CASES(WW)                                                                                      \
+  switch (n_hidden) {                                                                                         \
+    case 2: return train ? launch_tc_t<WW, 2, ACT, true>(p, grid, s) : launch_tc_t<WW, 2, ACT, false>(p, grid, s); \
+    case 3: return train ? launch_tc_t<WW, 3, ACT, true>(p, grid, s) : launch_tc_t<WW, 3, ACT, false>(p, grid, s); \
+    case 4: return train ? launch_tc_t<WW, 4, ACT, true>(p, grid, s) : launch_tc_t<WW, 4, ACT, false>(p, grid, s); \
   }
+  if (width == 128) { NBM_TC_CASES(128) }
+  if (width == 64) { NBM_TC_CASES(64) }
+#undef NBM_TC_CASES
   return cudaErrorInvalidValue;
 }
 

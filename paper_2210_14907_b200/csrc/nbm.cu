@@ -239,7 +239,8 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   w.xcap = max_points;
   int64_t items = 2 * max_points;
   w.nblk_cls = (int)((items + 1023) / 1024);
-  w.grid_mlp = sms;
+  w.grid_base = sms;
+  w.grid_mlp = sms * ((ai.prec == NBM_PREC_BF16) ? mlp_tc_ctas_per_sm(ai.width, ai.n_hidden) : 1);
   std::vector<void**> ptrs;
   size_t sizes[32];
   int k = 0;
@@ -390,7 +391,7 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
     pa.aux_by_item[k] = 1;
   }
   pa.u_out = w.xrow_u;
-  if (e == cudaSuccess) e = launch_mlp(A, false, pa, w.grid_mlp, s);
+  if (e == cudaSuccess) e = launch_mlp(A, false, pa, w.grid_base, s);
   launches += 1;
   if (e == cudaSuccess) e = launch_crossed_residual(h, n_global > 0 ? n_global : 1, s);
   launches += 1;
@@ -427,7 +428,7 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
     pm.seg.a[s0 + 2] = (float)(2.0 * P.lambda_b / nbg);
   }
   if (ev) cudaEventRecord(ev[1], s);
-  if (e == cudaSuccess) e = launch_mlp(A, true, pm, w.grid_mlp, s);
+  if (e == cudaSuccess) e = launch_mlp(A, true, pm, w.grid_base, s);
   launches += 1;
   if (ev) cudaEventRecord(ev[2], s);
   if (e == cudaSuccess) e = launch_reduce(h, grad_dev, loss_dev, s);
@@ -479,7 +480,7 @@ int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_
     p.seg.aux[k] = w.list_aux;
   }
   p.u_out = u_dev;
-  if (e == cudaSuccess) e = launch_mlp(A, false, p, w.grid_mlp, s);
+  if (e == cudaSuccess) e = launch_mlp(A, false, p, w.grid_base, s);
   return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_eval");
 }
 

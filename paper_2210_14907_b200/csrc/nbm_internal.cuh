@@ -84,7 +84,8 @@ struct Workspace {
   float* xrec;          // [xcap][8]  chat[7] (chat[0] = 1), rhs_hat
   int* xlist;           // [2][7 xcap] row ids partitioned by network
   // fused-MLP partials
-  int grid_mlp;         // CTAs of the fused kernel
+  int grid_mlp;         // CTAs of the fused kernel (partial slots)
+  int grid_base;        // launch argument: SMs (the kernel multiplies by its CTAs per SM)
   float* part;          // [2][grid_mlp][Pnet]
   int* touched;         // [2][grid_mlp]
   double* lpart;        // [grid_mlp + 1]  (+1: crossed rows' loss)
@@ -158,6 +159,7 @@ int mlp_fp32_supported(int width, int n_hidden);
 cudaError_t launch_mlp_tc(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
                           cudaStream_t s);
 int mlp_tc_supported(int width, int n_hidden, int act);
+int mlp_tc_ctas_per_sm(int width, int n_hidden);
 cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t* wimg, cudaStream_t s);
 // reduce
 cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s);

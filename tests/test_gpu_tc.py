@@ -28,12 +28,15 @@ def _run(s, th, p, b, terms=nbm.TERM_ALL):
     return float(loss.item()), grad.double().cpu().numpy().copy()
 
 
-@pytest.mark.parametrize("name,nh", [("c5", 2), ("c5", 3), ("c5", 4), ("c3", 2), ("c3", 3), ("c3", 4)])
-def test_tc_parity_w128(orc, name, nh):
+@pytest.mark.parametrize("name,w,nh", [("c5", 128, 2), ("c5", 128, 3), ("c5", 128, 4), ("c3", 128, 2),
+                                        ("c3", 128, 3), ("c3", 128, 4), ("c5", 64, 2), ("c5", 64, 4),
+                                        ("c3", 64, 4)])
+def test_tc_parity(orc, name, w, nh):
     """c5: 32-sphere union, tanh (resident weights); c3: star interface, Gaussian charges,
-    SiLU (weights streamed by TMA bulk copies, bf16 SiLU' buffers)."""
-    cfg = inputs.config(name, width=128) if name == "c5" else inputs.config(name)
-    cfg["sizes"] = [3] + [128] * nh + [1]
+    SiLU (weights streamed by TMA bulk copies, bf16 SiLU' buffers); W = 64 runs two CTAs
+    per SM and M = 128 dW MMAs over the 64 real output units."""
+    cfg = inputs.config(name, width=w) if name == "c5" else inputs.config(name)
+    cfg["sizes"] = [3] + [w] * nh + [1]
     n, nb = 1 << 13, 1 << 10
     s = nbm.Solver(cfg, 0, max_points=n)
     pb, ar = orc.from_config(cfg)
