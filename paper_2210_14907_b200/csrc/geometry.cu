@@ -70,8 +70,54 @@ __device__ double d_phi(const DevProblem& P, const double x[3]) {
   }
 }
 
-__device__ __forceinline__ int d_side(const DevProblem& P, const double x[3]) {
+__device__ __forceinline__ int d_side_exact(const DevProblem& P, const double x[3]) {
   return d_phi(P, x) <= 0.0 ? 0 : 1;
+}
+
+// side(x) = (phi(x) > 0), tie -> Omega- (S:84), identical to the fp64 definition: an fp32
+// filter decides whenever its margin exceeds its error bound, else the fp64 formula runs.
+//  spheres: |x-c|^2 vs r^2 in fp32 (relative error < 4e-7) with a 1e-5 relative margin;
+//  star:    the fp32 formula with a margin above its error bound (>= 1e-5 (2 + r)).
+__device__ __forceinline__ int d_side(const DevProblem& P, const double x[3]) {
+  if (P.ls_kind == NBM_LS_SPHERES) {
+    const float x0 = (float)x[0], x1 = (float)x[1], x2 = (float)x[2];
+    bool unsure = false;
+    for (int k = 0; k < P.n_spheres; ++k) {
+      const float dx = x0 - P.centers_f[k][0], dy = x1 - P.centers_f[k][1], dz = x2 - P.centers_f[k][2];
+      const float d2 = (dx * dx + dy * dy) + dz * dz;
+      const float r2 = P.radii_f[k] * P.radii_f[k];
+      if (d2 < r2 * (1.0f - 1e-5f)) return 0;          // certainly inside sphere k
+      if (d2 <= r2 * (1.0f + 1e-5f)) unsure = true;
+    }
+    if (!unsure) return 1;                              // certainly outside all spheres
+    return d_side_exact(P, x);
+  }
+  if (P.ls_kind == NBM_LS_STAR) {
+    const float x0 = (float)x[0], x1 = (float)x[1], x2 = (float)x[2];
+    const float rho = sqrtf(x0 * x0 + x1 * x1), r = sqrtf(rho * rho + x2 * x2);
+    if (r > 1e-3f && rho > 1e-3f) {
+      const float ct = x2 / r, st = rho / r, cp = x0 / rho;
+      float um = 1.0f;
+      if (P.star_m > 1) {
+        float ua = 1.0f, ub = 2.0f * ct;
+        for (int k = 2; k < P.star_m; ++k) { const float uc = 2.0f * ct * ub - ua; ua = ub; ub = uc; }
+        um = ub;
+      }
+      float tn = 1.0f;
+      if (P.star_n > 0) {
+        float ta = 1.0f, tb = cp;
+        for (int k = 1; k < P.star_n; ++k) { const float tc = 2.0f * cp * tb - ta; ta = tb; tb = tc; }
+        tn = tb;
+      }
+      const float ph = (r - (float)P.star_r0) - (float)P.star_amp * ((st * um) * tn);
+      const float mm = (float)(P.star_m + 1), nn = (float)(P.star_n + 1);
+      const float margin = 1e-5f * (2.0f + r) + 1e-6f * fabsf((float)P.star_amp) * (mm * mm) * (nn * nn);
+      if (ph > margin) return 1;
+      if (ph < -margin) return 0;
+    }
+    return d_side_exact(P, x);
+  }
+  return d_side_exact(P, x);
 }
 
 // Unit normal Omega- -> Omega+ at x (G7). Returns false if degenerate.
@@ -371,37 +417,35 @@ cudaError_t launch_classify(const nbm_handle* h, const float* pts, int64_t n, co
 }
 
 // ------------------------------------------------------------------ K2x crossed rows
-// One thread per crossed point: the sharp-interface row in fp64 (G3, G6),
-// normalised by the diagonal: chat_j = c_j / d (chat_0 = 1), rhs_hat = b / d, so the
-// residual r = sum_j chat_j u_j - rhs_hat is M^-1 A u - M^-1 b.  Writes the 7
-// evaluation rows (position, network tag).
+// One warp per crossed point, lane j < 7 owns stencil position j: the sharp-interface row in
+// fp64 (G3, G6), normalised by the diagonal: chat_j = c_j / d (chat_0 = 1),
+// rhs_hat = b / d, so the residual r = sum_j chat_j u_j - rhs_hat is M^-1 A u - M^-1 b
+// (P:60).  Lane 0 sums the arm contributions in arm order.  Writes the 7 evaluation rows
+// (position, network tag).
 __global__ void __launch_bounds__(128) k_assemble_crossed(
     const DevProblem* __restrict__ Pp, const float* __restrict__ pts, float hf,
     const int* __restrict__ counts, const int* __restrict__ list, float* __restrict__ xrec,
     float* __restrict__ xrow_x, uint8_t* __restrict__ xrow_tag, int* __restrict__ err) {
   const DevProblem& P = *Pp;
-  int nx = counts[kClsCrossed];
-  int start = counts[kNumCls + kClsCrossed];
-  for (int ci = blockIdx.x * blockDim.x + threadIdx.x; ci < nx; ci += gridDim.x * blockDim.x) {
+  const int nx = counts[kClsCrossed];
+  const int start = counts[kNumCls + kClsCrossed];
+  const int lane = threadIdx.x & 31, j = lane;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int ci = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ci < nx; ci += warps) {
     const float* p = pts + 3 * list[start + ci];
-    double pd[3] = {p[0], p[1], p[2]};
-    double h = hf, h2 = h * h;
-    int s = d_side(P, pd), so = 1 - s;
-    double bs = P.beta[s], bo = P.beta[so];
-    double c0 = P.k[s], corr = 0.0;
-    double coef[7];
-    int tag[7];
-    tag[0] = s;
-    xrow_x[(7 * (int64_t)ci) * 3 + 0] = p[0];
-    xrow_x[(7 * (int64_t)ci) * 3 + 1] = p[1];
-    xrow_x[(7 * (int64_t)ci) * 3 + 2] = p[2];
-    for (int j = 1; j <= 6; ++j) {
-      int dd = (j - 1) >> 1;
-      float q[3] = {p[0], p[1], p[2]};
-      q[dd] = (j & 1) ? __fadd_rn(p[dd], hf) : __fsub_rn(p[dd], hf);
-      for (int c = 0; c < 3; ++c) xrow_x[(7 * (int64_t)ci + j) * 3 + c] = q[c];
-      double qd[3] = {q[0], q[1], q[2]};
-      int sq = d_side(P, qd);
+    const double pd[3] = {p[0], p[1], p[2]};
+    const double h = hf, h2 = h * h;
+    const int s = d_side(P, pd), so = 1 - s;
+    const double bs = P.beta[s], bo = P.beta[so];
+    // this lane's position
+    float q[3] = {p[0], p[1], p[2]};
+    const int dd = (j - 1) >> 1;
+    if (j >= 1 && j <= 6) q[dd] = (j & 1) ? __fadd_rn(p[dd], hf) : __fsub_rn(p[dd], hf);
+    double coef = 0.0, cc = 0.0, corr = 0.0;   // arm coefficient, centre contribution, rhs correction
+    int tag = s;
+    if (j >= 1 && j <= 6) {
+      const double qd[3] = {q[0], q[1], q[2]};
+      const int sq = d_side(P, qd);
       bool crossed = false;
       double th = 0.0, n[3] = {0, 0, 0}, xg[3];
       if (sq != s) {
@@ -412,37 +456,47 @@ __global__ void __launch_bounds__(128) k_assemble_crossed(
           else atomicOr(err, kErrDegenerate);
         }
       }
-      if (!crossed) {                       // (a) uncrossed arm
-        coef[j] = -bs / h2;
-        c0 += bs / h2;
-        tag[j] = s;
-        continue;
+      if (!crossed) {                             // (a) uncrossed arm
+        coef = -bs / h2;
+        cc = bs / h2;
+      } else {                                    // (b) crossed arm, S:257 with rhs = f - corrections (G3)
+        const double muh = bs * bo / (th * bo + (1.0 - th) * bs);
+        const double sg = (s == 0) ? 1.0 : -1.0;
+        const double ne = (j & 1) ? n[dd] : -n[dd];   // n . e_j
+        double um, up, gm[3], gp[3], alpha = 0.0, sigma = 0.0;
+        if (d_exact(P, 0, xg, &um, gm)) {
+          d_exact(P, 1, xg, &up, gp);
+          alpha = up - um;
+          const double dp = gp[0] * n[0] + gp[1] * n[1] + gp[2] * n[2];
+          const double dm = gm[0] * n[0] + gm[1] * n[1] + gm[2] * n[2];
+          sigma = P.beta[1] * dp - P.beta[0] * dm;
+        }
+        const double a = sg * alpha, ba = sg * sigma * ne;
+        cc = muh / h2;
+        coef = -muh / h2;
+        tag = so;
+        corr = muh * (a / h2 + (1.0 - th) * ba / (h * bo));
       }
-      // (b) crossed arm, S:257 with rhs = f - corrections (G3)
-      double muh = bs * bo / (th * bo + (1.0 - th) * bs);
-      double sg = (s == 0) ? 1.0 : -1.0;
-      double ne = (j & 1) ? n[dd] : -n[dd];  // n . e_j
-      double um, up, gm[3], gp[3], alpha = 0.0, sigma = 0.0;
-      if (d_exact(P, 0, xg, &um, gm)) {
-        d_exact(P, 1, xg, &up, gp);
-        alpha = up - um;
-        double dp = gp[0] * n[0] + gp[1] * n[1] + gp[2] * n[2];
-        double dm = gm[0] * n[0] + gm[1] * n[1] + gm[2] * n[2];
-        sigma = P.beta[1] * dp - P.beta[0] * dm;
-      }
-      double a = sg * alpha, ba = sg * sigma * ne;
-      c0 += muh / h2;
-      coef[j] = -muh / h2;
-      tag[j] = so;
-      corr += muh * (a / h2 + (1.0 - th) * ba / (h * bo));
     }
-    double d = c0;
-    double rhs = d_source(P, s, pd) - corr;
-    float* rec = xrec + 8 * (int64_t)ci;
-    rec[0] = 1.0f;
-    for (int j = 1; j < 7; ++j) rec[j] = (float)(coef[j] / d);
-    rec[7] = (float)(rhs / d);
-    for (int j = 0; j < 7; ++j) xrow_tag[7 * (int64_t)ci + j] = (uint8_t)tag[j];
+    if (j < 7) {
+      for (int c = 0; c < 3; ++c) xrow_x[(7 * (int64_t)ci + j) * 3 + c] = q[c];
+      xrow_tag[7 * (int64_t)ci + j] = (uint8_t)tag;
+    }
+    // lane 0: d = k_s + sum_j cc_j, rhs = f_s(p) - sum_j corr_j (arm order), normalise
+    double c0 = P.k[s], cs = 0.0, coefs[7];
+    for (int a = 1; a <= 6; ++a) {
+      c0 += __shfl_sync(0xffffffffu, cc, a);
+      cs += __shfl_sync(0xffffffffu, corr, a);
+      coefs[a] = __shfl_sync(0xffffffffu, coef, a);
+    }
+    if (lane == 0) {
+      const double d = c0;
+      const double rhs = d_source(P, s, pd) - cs;
+      float* rec = xrec + 8 * (int64_t)ci;
+      rec[0] = 1.0f;
+      for (int a = 1; a < 7; ++a) rec[a] = (float)(coefs[a] / d);
+      rec[7] = (float)(rhs / d);
+    }
   }
 }
 
@@ -487,7 +541,7 @@ cudaError_t launch_assemble_crossed(const nbm_handle* h, const float* pts, int64
                                     cudaStream_t s) {
   const Workspace& w = h->ws;
   float hf = (float)((double)H / kLattice);
-  int grid = 148 * 4;
+  int grid = 148 * 8;   // one warp per crossed point (grid-stride)
   k_assemble_crossed<<<grid, 128, 0, s>>>(h->d_problem, pts, hf, w.counts, w.list, w.xrec,
                                           w.xrow_x, w.xrow_tag, w.err);
   k_partition_xrows<<<1, 1024, 0, s>>>(w.counts, w.xrow_tag, h->arch.n_nets, 7 * w.xcap,

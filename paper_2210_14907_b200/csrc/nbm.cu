@@ -104,8 +104,8 @@ int check_problem(const nbm_problem* p, DevProblem* out, std::string* why) {
     if (ls.kind == NBM_LS_SPHERES) {
       out->n_spheres = ls.n;
       for (int k = 0; k < ls.n; ++k) {
-        for (int d = 0; d < 3; ++d) out->centers[k][d] = ls.centers[3 * k + d];
-        out->radii[k] = ls.radii[k];
+        for (int d = 0; d < 3; ++d) out->centers[k][d] = out->centers_f[k][d] = ls.centers[3 * k + d];
+        out->radii[k] = out->radii_f[k] = ls.radii[k];
       }
     }
     out->star_r0 = ls.star_r0; out->star_amp = ls.star_amp;
@@ -128,26 +128,38 @@ int check_problem(const nbm_problem* p, DevProblem* out, std::string* why) {
   return NBM_OK;
 }
 
-// K4r: grad[net][j] = sum over CTAs (fixed order) of the touched partials; loss = sum of
-// the CTA loss partials and the crossed rows' loss.  fp64 accumulation of fp32 partials.
-__global__ void k_reduce(const float* __restrict__ part, const int* __restrict__ touched, int G,
-                         int64_t p_net, int64_t p_stride, int n_nets, const double* __restrict__ lpart,
-                         float* __restrict__ grad, float* __restrict__ loss, int* __restrict__ err) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n_nets * p_net) {
-    int net = (int)(i / p_net);
-    int64_t j = i - net * p_net;
-    double s = 0.0;
-    for (int g = 0; g < G; ++g)
+// K4r: grad[net][j] = sum over CTAs of the touched partials, in fixed order: 8 CTA groups
+// (g = 8 m + k) summed per thread, then the 8 group sums in order; loss = the CTA loss
+// partials plus the crossed rows' loss.  fp64 accumulation of the fp32 partials.
+constexpr int kRedCols = 32, kRedGroups = 8;
+__global__ void __launch_bounds__(kRedCols * kRedGroups) k_reduce(
+    const float* __restrict__ part, const int* __restrict__ touched, int G, int64_t p_net, int64_t p_stride,
+    int n_nets, const double* __restrict__ lpart, float* __restrict__ grad, float* __restrict__ loss,
+    int* __restrict__ err) {
+  __shared__ double acc[kRedGroups][kRedCols];
+  const int col = threadIdx.x % kRedCols, grp = threadIdx.x / kRedCols;
+  const int64_t i = (int64_t)blockIdx.x * kRedCols + col;
+  const int64_t P = n_nets * p_net;
+  double s = 0.0;
+  if (i < P) {
+    const int net = (int)(i / p_net);
+    const int64_t j = i - net * p_net;
+    for (int g = grp; g < G; g += kRedGroups)
       if (touched[net * G + g]) s += part[((int64_t)net * G + g) * p_stride + j];
-    float v = (float)s;
+  }
+  acc[grp][col] = s;
+  __syncthreads();
+  if (grp == 0 && i < P) {
+    double t = 0.0;
+    for (int k = 0; k < kRedGroups; ++k) t += acc[k][col];
+    const float v = (float)t;
     grad[i] = v;
     if (!isfinite(v)) atomicOr(err, kErrNonfinite);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double s = 0.0;
-    for (int g = 0; g <= G; ++g) s += lpart[g];
-    float v = (float)s;
+    double t = 0.0;
+    for (int g = 0; g <= G; ++g) t += lpart[g];
+    const float v = (float)t;
     *loss = v;
     if (!isfinite(v)) atomicOr(err, kErrNonfinite);
   }
@@ -183,7 +195,7 @@ cudaError_t launch_mlp(const ArchInfo& A, bool train, const MlpParams& p, int gr
 namespace nbm {
 cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s) {
   int64_t P = h->arch.p_net * h->arch.n_nets;
-  k_reduce<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(h->ws.part, h->ws.touched, h->ws.grid_mlp,
+  k_reduce<<<(unsigned)((P + kRedCols - 1) / kRedCols), kRedCols * kRedGroups, 0, s>>>(h->ws.part, h->ws.touched, h->ws.grid_mlp,
                                                        h->arch.p_net, (h->arch.p_net + 3) & ~3ll,
                                                        h->arch.n_nets, h->ws.lpart,
                                                        grad, loss, h->ws.err);

@@ -35,6 +35,8 @@ struct DevProblem {
   double charge_centers[kMaxCharges][3];
   double charge_sigma;
   double lambda_b;
+  float centers_f[kMaxSpheres][3];   // fp32 copies (exact: the inputs are fp32) for the filter
+  float radii_f[kMaxSpheres];
 };
 
 // Point classes produced by the classification stage (S2).
