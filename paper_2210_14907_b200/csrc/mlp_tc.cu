@@ -361,6 +361,41 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     }
   };
 
+  // global loads of one tile for thread tid < kTB: the item slot `tid` (index + aux) and the
+  // coordinates of tile row `tid` (stencil arm generated on the fly).  Issued one tile ahead.
+  struct Fetch { int item; float aux, x0, x1, x2; };
+  auto fetch = [&](int tt) -> Fetch {
+    Fetch f{-1, 0.0f, 0.0f, 0.0f, 0.0f};
+    if (tt >= t1 || tid >= kTB) return f;
+    int sg = 0;
+    while (tt >= firstTile[sg + 1]) ++sg;
+    const int knd = prm.seg.kind[sg];
+    const int pr = knd == kSegStencil ? kTPT : kTB;
+    const int fst = (tt - firstTile[sg]) * pr;
+    const int nv = min(pr, segCnt[sg] - fst);
+    const int* its = prm.seg.items[sg] + segStart[sg];
+    if (tid < pr && tid < nv) {
+      f.item = its[fst + tid];
+      f.aux = prm.aux_by_item[sg] ? prm.seg.aux[sg][f.item] : prm.seg.aux[sg][segStart[sg] + fst + tid];
+    }
+    if (knd == kSegStencil) {
+      const int j = tid / kTPT, p = tid - j * kTPT;
+      if (j < 7 && p < nv) {
+        const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + p];
+        f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
+        if (j > 0) {   // arms +x, -x, +y, -y, +z, -z (exact on the lattice)
+          const float hs = (j & 1) ? prm.h : -prm.h;
+          if (j <= 2) f.x0 = __fadd_rn(f.x0, hs); else if (j <= 4) f.x1 = __fadd_rn(f.x1, hs); else f.x2 = __fadd_rn(f.x2, hs);
+        }
+      }
+    } else if (tid < nv) {
+      const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + tid];
+      f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
+    }
+    return f;
+  };
+  Fetch cur = fetch(t0);
+
   int seg = 0;
   for (int t = t0; t < t1; ++t) {
     while (t >= firstTile[seg + 1]) ++seg;
@@ -376,33 +411,13 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       curNet = net;
       __syncthreads();
     }
-    // ---- gather: items, aux, the row's coordinates ----
-    const int* items = prm.seg.items[seg] + segStart[seg];
-    if (tid < per) {
-      const int it = tid < nvalid ? items[first + tid] : -1;
-      sItem[tid] = it;
-      float a = 0.0f;
-      if (it >= 0) a = prm.aux_by_item[seg] ? prm.seg.aux[seg][it] : prm.seg.aux[seg][segStart[seg] + first + tid];
-      sAux[tid] = a;
-    }
-    __syncthreads();
+    // ---- gather: items, aux and the row's coordinates were prefetched during the previous tile ----
     if (tid < kTB) {
-      float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
-      if (kind == kSegStencil) {
-        const int j = tid / kTPT, p = tid - j * kTPT;
-        if (j < 7 && p < nvalid) {
-          const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[p];
-          x0 = src[0]; x1 = src[1]; x2 = src[2];
-          if (j > 0) {   // arms +x, -x, +y, -y, +z, -z (exact on the lattice)
-            const float hs = (j & 1) ? prm.h : -prm.h;
-            if (j <= 2) x0 = __fadd_rn(x0, hs); else if (j <= 4) x1 = __fadd_rn(x1, hs); else x2 = __fadd_rn(x2, hs);
-          }
-        }
-      } else if (tid < nvalid) {
-        const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[tid];
-        x0 = src[0]; x1 = src[1]; x2 = src[2];
+      if (tid < per) {
+        sItem[tid] = cur.item;
+        sAux[tid] = cur.aux;
       }
-      sX[4 * tid] = x0; sX[4 * tid + 1] = x1; sX[4 * tid + 2] = x2;
+      sX[4 * tid] = cur.x0; sX[4 * tid + 1] = cur.x1; sX[4 * tid + 2] = cur.x2;
     }
     __syncthreads();
     TR(0);
@@ -416,6 +431,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     __syncthreads();
     TR(1);
     // ---- hidden layers 2..NH on the tensor cores ----
+    Fetch nxt;
 #pragma unroll 1
     for (int l = 2; l <= NH; ++l) {
       if (tid == 0) {
@@ -425,6 +441,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
              W / 16, false);
         tc::mma_commit(bar);
       }
+      if (l == 2) nxt = fetch(t + 1);   // the next tile's loads overlap this tile
       wait_mma();
       if (tid == 0 && l < NH) wload(curNet, l + 1);   // prefetch the next layer's weights
       TR(2 + 2 * (l - 2));
@@ -480,6 +497,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     }
     __syncthreads();
     TR(8);
+    cur = nxt;
     if (!TRAIN) continue;
     // ---- residual epilogue -> cotangents (S4) ----
     if (kind == kSegStencil) {
