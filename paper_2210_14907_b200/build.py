@@ -23,6 +23,7 @@ SOURCES = {
     "geometry.cu": ["-fmad=false"],
     "mlp_fp32.cu": [],
     "mlp_tc.cu": [],
+    "mlp_w256.cu": [],
     "nbm.cu": [],
 }
 HEADERS = ["nbm_internal.cuh", "tc_ptx.cuh"]

@@ -54,7 +54,7 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
   int nh = a->n_layers - 2;
   bool ok = false;
   if (a->prec == NBM_PREC_FP32 && a->act == NBM_ACT_TANH) ok = mlp_fp32_supported(W, nh);
-  if (a->prec == NBM_PREC_BF16) ok = mlp_tc_supported(W, nh, a->act);
+  if (a->prec == NBM_PREC_BF16) ok = mlp_tc_supported(W, nh, a->act) || (W == 256 && nh >= 2 && nh <= 4 && a->act == NBM_ACT_TANH);
   if (!ok) {
     *why = "arch: unsupported (prec, act, width, depth) combination in this build";
     return NBM_E_INVALID_ARCH;
@@ -185,10 +185,17 @@ void fill_common(const nbm_handle* h, MlpParams& p, const float* theta, float hf
   for (int s = 0; s < kNumSeg; ++s) { p.cnt_slot[s] = kSlotZero; p.start_slot[s] = -1; p.seg.kind[s] = kSegXRows; }
 }
 
-cudaError_t launch_mlp(const ArchInfo& A, bool train, const MlpParams& p, int grid, cudaStream_t s) {
-  if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, A.act, train, p, grid, s);
-  return launch_mlp_fp32(A.width, A.n_hidden, train, p, grid, s);
+bool is_w256(const ArchInfo& A) { return A.prec == NBM_PREC_BF16 && A.width == 256; }
+
+cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cudaStream_t s) {
+  const ArchInfo& A = h->arch;
+  const Workspace& w = h->ws;
+  if (is_w256(A))
+    return launch_mlp_w256(A.n_hidden, train, p, w.wimg, w.wimg_b, w.hscr, w.rep, w.nrep, w.grid_base, s);
+  if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, A.act, train, p, w.grid_base, s);
+  return launch_mlp_fp32(A.width, A.n_hidden, train, p, w.grid_base, s);
 }
+
 
 }  // namespace
 
@@ -275,7 +282,13 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   ALLOC(w.touched, 2 * (size_t)w.grid_mlp * sizeof(int));
   ALLOC(w.lpart, ((size_t)w.grid_mlp + 1) * sizeof(double));
   ALLOC(w.err, sizeof(int));
-  ALLOC(w.wimg, (size_t)2 * (ai.n_hidden > 1 ? ai.n_hidden - 1 : 1) * ai.width * ai.width * sizeof(uint16_t));
+  const size_t nhh = ai.n_hidden > 1 ? ai.n_hidden - 1 : 1;
+  ALLOC(w.wimg, (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t));
+  const bool w256 = is_w256(ai);
+  w.nrep = w256 ? 4 : 0;
+  ALLOC(w.wimg_b, w256 ? (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t) : 16);
+  ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * nhh * 128 * ai.width * 2 : 16);
+  ALLOC(w.rep, w256 ? (size_t)w.nrep * 2 * ((ai.p_net + 3) & ~3ll) * sizeof(float) : 16);
 #undef ALLOC
   for (size_t i = 0; i < ptrs.size(); ++i) {
     e = cudaMalloc(ptrs[i], sizes[i]);
@@ -305,7 +318,7 @@ void nbm_destroy(nbm_handle* h) {
   void* ps[] = {h->d_problem, h->ws.cls, h->ws.aux_tmp, h->ws.blk_counts, h->ws.blk_offsets,
                 h->ws.counts, h->ws.list, h->ws.list_aux, h->ws.xrow_x, h->ws.xrow_u, h->ws.xrow_cot,
                 h->ws.xrow_tag, h->ws.xrec, h->ws.xlist, h->ws.part, h->ws.touched, h->ws.lpart,
-                h->ws.err, h->ws.wimg};
+                h->ws.err, h->ws.wimg, h->ws.wimg_b, h->ws.hscr, h->ws.rep};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : h->ev) cudaEventDestroy(ev);
@@ -384,8 +397,11 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
   cudaError_t e = launch_classify(h, pts_dev, n, bpts_dev, nb, H, dm, dpl, terms, false, s);
   launches += 3;
   if (e == cudaSuccess && A.prec == NBM_PREC_BF16) {
-    e = launch_pack_weights(A, theta_dev, w.wimg, s);
+    e = is_w256(A) ? launch_pack_w256(A, theta_dev, w.wimg, w.wimg_b, s) : launch_pack_weights(A, theta_dev, w.wimg, s);
     launches += 1;
+  }
+  if (e == cudaSuccess && is_w256(A)) {
+    e = cudaMemsetAsync(w.rep, 0, (size_t)w.nrep * 2 * ((A.p_net + 3) & ~3ll) * sizeof(float), s);
   }
   if (e == cudaSuccess) e = launch_assemble_crossed(h, pts_dev, n, H, s);
   launches += 2;
@@ -403,7 +419,7 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
     pa.aux_by_item[k] = 1;
   }
   pa.u_out = w.xrow_u;
-  if (e == cudaSuccess) e = launch_mlp(A, false, pa, w.grid_base, s);
+  if (e == cudaSuccess) e = launch_mlp_h(h, false, pa, s);
   launches += 1;
   if (e == cudaSuccess) e = launch_crossed_residual(h, n_global > 0 ? n_global : 1, s);
   launches += 1;
@@ -440,10 +456,13 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
     pm.seg.a[s0 + 2] = (float)(2.0 * P.lambda_b / nbg);
   }
   if (ev) cudaEventRecord(ev[1], s);
-  if (e == cudaSuccess) e = launch_mlp(A, true, pm, w.grid_base, s);
+  if (e == cudaSuccess) e = launch_mlp_h(h, true, pm, s);
   launches += 1;
   if (ev) cudaEventRecord(ev[2], s);
-  if (e == cudaSuccess) e = launch_reduce(h, grad_dev, loss_dev, s);
+  if (e == cudaSuccess)
+    e = is_w256(A) ? launch_reduce_rep(w.rep, w.nrep, A.p_net, (A.p_net + 3) & ~3ll, A.n_nets, w.lpart,
+                                       w.grid_mlp, grad_dev, loss_dev, w.err, s)
+                   : launch_reduce(h, grad_dev, loss_dev, s);
   launches += 1;
   if (ev) {
     cudaEventRecord(ev[3], s);
@@ -479,7 +498,8 @@ int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_
   const ArchInfo& A = h->arch;
   const Workspace& w = h->ws;
   cudaError_t e = launch_classify(h, pts_dev, n, nullptr, 0, 1, 1.0, 1.0, NBM_TERM_ALL, true, s);
-  if (e == cudaSuccess && A.prec == NBM_PREC_BF16) e = launch_pack_weights(A, theta_dev, w.wimg, s);
+  if (e == cudaSuccess && A.prec == NBM_PREC_BF16)
+    e = is_w256(A) ? launch_pack_w256(A, theta_dev, w.wimg, w.wimg_b, s) : launch_pack_weights(A, theta_dev, w.wimg, s);
   MlpParams p;
   fill_common(h, p, theta_dev, 0.0f);
   for (int k = 0; k < 2; ++k) {
@@ -492,7 +512,7 @@ int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_
     p.seg.aux[k] = w.list_aux;
   }
   p.u_out = u_dev;
-  if (e == cudaSuccess) e = launch_mlp(A, false, p, w.grid_base, s);
+  if (e == cudaSuccess) e = launch_mlp_h(h, false, p, s);
   return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_eval");
 }
 

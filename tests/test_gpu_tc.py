@@ -30,12 +30,13 @@ def _run(s, th, p, b, terms=nbm.TERM_ALL):
 
 @pytest.mark.parametrize("name,w,nh", [("c5", 128, 2), ("c5", 128, 3), ("c5", 128, 4), ("c3", 128, 2),
                                         ("c3", 128, 3), ("c3", 128, 4), ("c5", 64, 2), ("c5", 64, 4),
-                                        ("c3", 64, 4)])
+                                        ("c3", 64, 4), ("c4", 256, 2), ("c4", 256, 4)])
 def test_tc_parity(orc, name, w, nh):
     """c5: 32-sphere union, tanh (resident weights); c3: star interface, Gaussian charges,
     SiLU (weights streamed by TMA bulk copies, bf16 SiLU' buffers); W = 64 runs two CTAs
-    per SM and M = 128 dW MMAs over the 64 real output units."""
-    cfg = inputs.config(name, width=w) if name == "c5" else inputs.config(name)
+    per SM and M = 128 dW MMAs over the 64 real output units; c4 (W = 256) streams weights,
+    parks activations and flushes per-tile dW by vector reductions."""
+    cfg = inputs.config(name, width=w) if name in ("c4", "c5") else inputs.config(name)
     cfg["sizes"] = [3] + [w] * nh + [1]
     n, nb = 1 << 13, 1 << 10
     s = nbm.Solver(cfg, 0, max_points=n)
