@@ -1,20 +1,24 @@
 // mlp_w256.cu -- K3w: fused bf16 tensor-core MLP kernel for hidden width 256 (config 4,
-// c5-w256; SURVEY 7.3 hard part 4).  At W = 256 neither the weights (128 KB per matrix)
-// nor three activation buffers (64 KB each) nor one layer's dW (256 KB fp32 = all of TMEM)
-// fit on chip, so this kernel:
-//   * streams the hidden weights through a 2-stage shared-memory ring in 32 KB K-slices
-//     (cp.async.bulk + mbarrier complete_tx) from two packed bf16 images (forward slices
-//     along the input index, backward slices along the output index);
-//   * keeps two 64 KB activation buffers on chip and parks h_1..h_{NH-1} (bf16) in a
-//     per-CTA global scratch (L2-resident) that is brought back by bulk copies for the
-//     backward pass;
-//   * computes each tile's dW_l = G_l^T h_{l-1} in two 128-output halves into a TMEM
-//     scratch (columns [256,512); the working accumulator uses [0,256)) and flushes it with
-//     vector reductions (red.global.add.v4.f32) into a few replica buffers.  The flush order
-//     across CTAs is not fixed: W = 256 is deterministic only within tolerance (G21).
-// 512 threads: warp w owns TMEM lane quadrant w % 4 (tile rows) and columns
-// [64 (w/4), 64 (w/4) + 64).  Rounding points as the W <= 128 kernel (G16),
-// tanh only.
+// c5-w256; SURVEY 7.3 hard part 4), run by CTA PAIRS (thread-block clusters of 2, tcgen05
+// cta_group::2).  At W = 256 neither the weights (128 KB per matrix) nor three activation
+// tiles nor one layer's dW (256 KB fp32 = all of one SM's TMEM) fit on one SM, and a
+// per-CTA dW flush of 256 KB per layer per 128-row tile saturates the SM->L2 write path
+// (measured: scripts/red_bench.cu).  The pair therefore works as one 256-row tile:
+//   * forward / dH GEMMs are M = 256 pair MMAs (each CTA holds its own 128 rows as A); each
+//     CTA streams only ITS N-half of every 64-deep weight K-slice (16 KB) through a 4-stage
+//     ring, halving the weight traffic per row; the peer forwards its slice arrivals to the
+//     leader's barrier (remote mbarrier arrive), the leader issues, completion is multicast;
+//   * dW_l = G_l^T h_{l-1} is ONE pair MMA with M = 256 outputs (CTA r owns outputs
+//     [128 r, 128 r + 128) in TMEM columns [256, 512)), N = 256 inputs and K = the pair's 256
+//     rows: each CTA bulk-loads, from the parked (L2-resident) copies of both CTAs, the
+//     o-half of G_l and the i-half of h_{l-1} it owns.  Per row, the fp32 dW flush is half
+//     of the single-CTA design's, and it overlaps the next dH GEMM;
+//   * h_1..h_{NH-1} and G_2..G_NH are parked as bf16 in per-CTA global scratch; act'(h) in
+//     the backward epilogue is read back from there (ld.global.cg, coalesced).
+// The flush order across pairs is not fixed: W = 256 is deterministic only within
+// tolerance (G21).  512 threads: warp w owns TMEM lane quadrant w % 4 (tile rows / dW
+// outputs) and columns [64 (w/4), 64 (w/4) + 64).  Rounding points as the W <= 128 kernel
+// (G16), tanh only.
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -26,29 +30,32 @@ namespace nbm {
 namespace {
 
 constexpr int W = 256;
-constexpr int kB = 128;        // tile rows
+constexpr int kB = 128;        // tile rows per CTA (256 per pair)
 constexpr int kPT = 18;        // stencil points per tile
 constexpr int kThreads = 512;
-constexpr uint32_t ACT = kB * W * 2;      // 64 KB bf16 activation buffer
-constexpr uint32_t SLICE = 64 * W * 2;    // 32 KB weight K-slice
-constexpr uint32_t LBO_ACT = kB * 16;     // 2048: K-core stride of activation buffers
+constexpr int kStages = 4;     // weight ring: one whole GEMM's slices in flight
+constexpr uint32_t ACT = kB * W * 2;        // 64 KB bf16 activation tile
+constexpr uint32_t QTR = ACT / 2;           // 32 KB: one 128-column half of it
+constexpr uint32_t HSLICE = 64 * 128 * 2;   // 16 KB: one CTA's N-half of a 64-deep K-slice
+constexpr uint32_t LBO_ACT = kB * 16;       // 2048: K-core stride of activation tiles
 
 template <int NH>
 struct Lay {
-  static constexpr uint32_t oX = 0;                     // activation buffer 0
-  static constexpr uint32_t oY = oX + ACT;              // activation buffer 1
-  static constexpr uint32_t oW = oY + ACT;              // 2 weight stages
-  static constexpr uint32_t oW1 = oW + 2 * SLICE;       // fp32 [W][3]
-  static constexpr uint32_t oBias = oW1 + 4 * 3 * W;    // fp32 [NH][W]
-  static constexpr uint32_t oWo = oBias + 4 * NH * W;   // fp32 [W] + bo
-  static constexpr uint32_t oX3 = oWo + 4 * (W + 4);    // fp32 [kB][4]
-  static constexpr uint32_t oUp = oX3 + 16 * kB;        // fp32 [4][kB]
+  static constexpr uint32_t oX = 0;                       // activation tile 0
+  static constexpr uint32_t oY = oX + ACT;                // activation tile 1
+  static constexpr uint32_t oW = oY + ACT;                // weight ring
+  static constexpr uint32_t oW1 = oW + kStages * HSLICE;  // fp32 [W][3]
+  static constexpr uint32_t oBias = oW1 + 4 * 3 * W;      // fp32 [NH][W]
+  static constexpr uint32_t oWo = oBias + 4 * NH * W;     // fp32 [W] + bo
+  static constexpr uint32_t oX3 = oWo + 4 * (W + 4);      // fp32 [kB][4]
+  static constexpr uint32_t oUp = oX3 + 16 * kB;          // fp32 [4][kB]
   static constexpr uint32_t oU = oUp + 16 * kB;
   static constexpr uint32_t oUb = oU + 4 * kB;
   static constexpr uint32_t oAux = oUb + 4 * kB;
   static constexpr uint32_t oItem = oAux + 4 * kB;
-  static constexpr uint32_t oBar = oItem + 4 * kB;      // mma, full[2], empty[2], hload + tmem base
-  static constexpr uint32_t bytes = oBar + 64;
+  static constexpr uint32_t oBar = oItem + 4 * kB;        // full[4], empty[4], mma, dw, ld, park + tmem base
+  static constexpr uint32_t bytes = oBar + 128;
+  static constexpr int kScr = NH + 1;                     // parked tiles per CTA: h_1..h_{NH-1}, G x2
   static constexpr int64_t tW1 = 0, tB1 = 3 * W;
   __host__ __device__ static constexpr int64_t tWl(int l) { return 4 * W + (int64_t)(l - 2) * (W * W + W); }
   __host__ __device__ static constexpr int64_t tBl(int l) { return tWl(l) + W * W; }
@@ -82,11 +89,13 @@ __device__ __forceinline__ float tsum(float (&v)[32], int lane) {   // warp tran
 __device__ __forceinline__ void sts4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
-__device__ __forceinline__ void lds4(uint32_t a, uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w) {
-  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(a) : "memory");
-}
 __device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ uint4 ldcg4(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
 }
 // 32 columns (chunk c) of row r: fp32 -> bf16 core layout in shared memory (+ optional global copy)
 __device__ __forceinline__ void put_chunk(uint32_t buf, uint8_t* gbuf, int r, int c, const float (&h)[32]) {
@@ -99,11 +108,12 @@ __device__ __forceinline__ void put_chunk(uint32_t buf, uint8_t* gbuf, int r, in
     if (gbuf) *reinterpret_cast<uint4*>(gbuf + off) = make_uint4(a, b, cc, d);
   }
 }
-__device__ __forceinline__ void get_chunk(uint32_t buf, int r, int c, float (&h)[32]) {
+// chunk c of row r of a parked (global) bf16 tile -> fp32
+__device__ __forceinline__ void get_chunk_g(const uint8_t* gbuf, int r, int c, float (&h)[32]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    uint32_t w[4];
-    lds4(buf + (uint32_t)((c * 4 + q) * LBO_ACT + r * 16), w[0], w[1], w[2], w[3]);
+    const uint4 w4 = ldcg4(gbuf + (c * 4 + q) * LBO_ACT + r * 16);
+    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       h[8 * q + 2 * e] = __uint_as_float(w[e] << 16);
@@ -114,17 +124,30 @@ __device__ __forceinline__ void get_chunk(uint32_t buf, int r, int c, float (&h)
 
 }  // namespace
 
+#ifdef NBM_TC_TRACE
+__device__ long long g_w256_trace[8][48];
+__device__ long long g_w256_ld[2][64][4];   // [cta 0/1][gemm #][queue s0, queue s3, full s0, full s3]
+#define TRW(k)                                                                                           \
+  do {                                                                                                   \
+    if (TRAIN && blockIdx.x == 0 && tid == 0 && u - u0 < 8) g_w256_trace[u - u0][k] = clock64();          \
+  } while (0)
+#else
+#define TRW(k) \
+  do {         \
+  } while (0)
+#endif
+
 struct W256Params {
   MlpParams m;
-  const uint16_t* wfwd;   // [2][NH-1][4 slices][256 o][64 i] K-major core layout
-  const uint16_t* wbwd;   // [2][NH-1][4 slices][64 o][256 i] MN-major core layout
-  uint8_t* hscr;          // [grid][NH-1][64 KB] parked activations
+  const uint16_t* wfwd;   // [2][NH-1][4 slices][2 halves][128 o][64 i] K-major core layout
+  const uint16_t* wbwd;   // [2][NH-1][4 slices][2 halves][64 o][128 i] MN-major core layout
+  uint8_t* hscr;          // [grid][NH+1][64 KB] parked activations / G
   float* rep;             // [R][2][p_stride] gradient replicas (red.global.add)
   int nrep;
 };
 
 template <int NH, bool TRAIN>
-__global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
   using L = Lay<NH>;
   const MlpParams& prm = P.m;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -138,111 +161,144 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
   float* sUb = reinterpret_cast<float*>(smem + L::oUb);
   float* sAux = reinterpret_cast<float*>(smem + L::oAux);
   int* sItem = reinterpret_cast<int*>(smem + L::oItem);
-  uint64_t* bmma = reinterpret_cast<uint64_t*>(smem + L::oBar);
-  uint64_t* bfull = bmma + 1;    // [2]
-  uint64_t* bempty = bmma + 3;   // [2]
-  uint64_t* bh = bmma + 5;       // activation reload
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(smem + L::oBar + 48);
-  __shared__ int segTiles[kNumSeg], segCnt[kNumSeg], segStart[kNumSeg];
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(smem + L::oBar);   // [4]
+  uint64_t* bempty = bfull + 4;                                      // [4]
+  uint64_t* bmma = bfull + 8;
+  uint64_t* bdw = bfull + 9;
+  uint64_t* bld = bfull + 10;
+  uint64_t* bpark = bfull + 11;   // the peer's parked G_l (and h) are complete in global memory
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(smem + L::oBar + 112);
+  __shared__ int segPairs[kNumSeg], segCnt[kNumSeg], segStart[kNumSeg];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quad = warp & 3, cg = warp >> 2;
   const int row = quad * 32 + lane;
   const uint32_t tlane = (uint32_t)(quad * 32) << 16;
+  const uint32_t rank = tc::cluster_rank();
+  const bool leader = rank == 0;
   if (tid < kNumSeg) {
     const int c = prm.counts[prm.cnt_slot[tid]];
+    const int per = prm.seg.kind[tid] == kSegStencil ? kPT : kB;
     segCnt[tid] = c;
     segStart[tid] = prm.start_slot[tid] >= 0 ? prm.counts[prm.start_slot[tid]] : 0;
-    segTiles[tid] = (c + (prm.seg.kind[tid] == kSegStencil ? kPT : kB) - 1) / (prm.seg.kind[tid] == kSegStencil ? kPT : kB);
+    segPairs[tid] = ((c + per - 1) / per + 1) / 2;
   }
   if (tid == 0) {
-    for (int i = 0; i < 6; ++i) tc::mbar_init(bmma + i, 1);
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(bfull + s, leader ? 2 : 1);   // leader: own bytes + the peer's forward
+      tc::mbar_init(bempty + s, 1);
+    }
+    tc::mbar_init(bmma, 1);
+    tc::mbar_init(bdw, 1);
+    tc::mbar_init(bld, leader ? 2 : 1);
+    tc::mbar_init(bpark, 1);
     tc::mbar_fence_init();
   }
-  if (warp == 0) tc::tmem_alloc(sTmem, 512);
+  if (warp == 0) tc::tmem_alloc2(sTmem, 512);
   tc::tc_fence_before();
-  __syncthreads();
+  tc::cluster_sync();
   tc::tc_fence_after();
-  const uint32_t tmem = *sTmem;
-  int firstTile[kNumSeg + 1];
+  const uint32_t tmem = *sTmem;   // [0,256): GEMM accumulator, [256,512): dW
+  int firstPair[kNumSeg + 1];
   int total = 0;
 #pragma unroll
-  for (int s = 0; s < kNumSeg; ++s) { firstTile[s] = total; total += segTiles[s]; }
-  firstTile[kNumSeg] = total;
-  const int G = gridDim.x, cta = blockIdx.x;
-  const int t0 = (int)((int64_t)total * cta / G), t1 = (int)((int64_t)total * (cta + 1) / G);
+  for (int s = 0; s < kNumSeg; ++s) { firstPair[s] = total; total += segPairs[s]; }
+  firstPair[kNumSeg] = total;
+  const int NC = gridDim.x >> 1, q = blockIdx.x >> 1;
+  const int u0 = (int)((int64_t)total * q / NC), u1 = (int)((int64_t)total * (q + 1) / NC);
   const uint32_t aBuf[2] = {sb + L::oX, sb + L::oY};
-  uint8_t* hscr = P.hscr + (int64_t)cta * (NH - 1) * ACT;
-  uint32_t ph_mma = 0, ph_full[2] = {0, 0}, ph_empty[2] = {0, 0}, ph_h = 0;
-  bool empty_armed[2] = {false, false};   // an MMA commit is pending on the stage
-  bool pending_full[2] = {false, false};  // a bulk copy into the stage has not been waited on
+  const uint32_t ring = sb + L::oW;
+  uint8_t* myScr = P.hscr + (int64_t)blockIdx.x * L::kScr * ACT;
+  const uint8_t* pairScr0 = P.hscr + (int64_t)(2 * q) * L::kScr * ACT;
+  auto hslot = [&](int j) -> int64_t { return (int64_t)(j - 1) * ACT; };                 // h_j, j in 1..NH-1
+  auto gslot = [&](int l) -> int64_t { return (int64_t)(NH - 1 + (l & 1)) * ACT; };     // G_l
+  uint32_t ph_full[kStages] = {0, 0, 0, 0}, ph_empty[kStages] = {0, 0, 0, 0};
+  uint32_t ph_mma = 0, ph_dw = 0, ph_ld = 0, ph_park = 0;
+  bool ringUsed = false;
+  int gcount = 0, qcount = 0;   // GEMMs issued / queued (trace)
 
-  // ---- weight slice pipeline (tid 0 only) ----
-  int curNet = -1;
-  auto slice_ptr = [&](bool bwd, int l, int s) -> const uint16_t* {
-    const uint16_t* base = bwd ? P.wbwd : P.wfwd;
-    return base + (((int64_t)curNet * (NH - 1) + (l - 2)) * 4 + s) * (SLICE / 2);
+  auto seg_of = [&](int u) {
+    int s = 0;
+    while (u >= firstPair[s + 1]) ++s;
+    return s;
   };
-  auto load_slice = [&](int st, bool bwd, int l, int s) {
-    if (pending_full[st]) {           // drain an unused prefetch (e.g. on a network switch)
-      tc::mbar_wait(bfull + st, ph_full[st]);
-      ph_full[st] ^= 1;
-      pending_full[st] = false;
+  // ---- weight ring (tid 0 of each CTA) ----
+  auto queue_gemm = [&](bool bwd, int net, int l) {
+    const uint16_t* base = (bwd ? P.wbwd : P.wfwd) + ((int64_t)net * (NH - 1) + (l - 2)) * 4 * 2 * (HSLICE / 2);
+    for (int s = 0; s < kStages; ++s) {
+      if (ringUsed) {   // the previous GEMM's MMAs on this stage are done
+        tc::mbar_wait(bempty + s, ph_empty[s]);
+        ph_empty[s] ^= 1;
+      }
+      tc::mbar_arrive_expect_tx(bfull + s, HSLICE);
+      tc::bulk_copy_g2s(ring + s * HSLICE, base + (int64_t)(s * 2 + rank) * (HSLICE / 2), HSLICE, bfull + s);
+#ifdef NBM_TC_TRACE
+      if (blockIdx.x < 2 && qcount < 64 && (s == 0 || s == 3)) g_w256_ld[blockIdx.x][qcount][s == 0 ? 0 : 1] = clock64();
+#endif
     }
-    if (empty_armed[st]) {            // wait until the MMAs that read this stage are done
-      tc::mbar_wait(bempty + st, ph_empty[st]);
-      ph_empty[st] ^= 1;
-      empty_armed[st] = false;
-    }
-    tc::mbar_arrive_expect_tx(bfull + st, SLICE);
-    tc::bulk_copy_g2s(sb + L::oW + st * SLICE, slice_ptr(bwd, l, s), SLICE, bfull + st);
-    pending_full[st] = true;
+    ++qcount;
   };
-  // GEMM with streamed B: acc[dcol] = A * B over 4 K-slices of 64.  Slices 0 and 1 must
-  // already be loading into stages 0 and 1; the next GEMM's first two slices are queued.
-  auto gemm_streamed = [&](uint32_t a0, bool bwd, int l, uint32_t idesc, int nl, bool nbwd, bool has_next) {
-    for (int s = 0; s < 4; ++s) {
-      const int st = s & 1;
-      tc::mbar_wait(bfull + st, ph_full[st]);
-      ph_full[st] ^= 1;
-      pending_full[st] = false;
+  // acc = A * B over 4 K-slices of 64; the peer forwards its slice arrivals, the leader issues
+  auto issue_gemm = [&](uint32_t a0, bool bwd, uint32_t idesc) {
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_wait(bfull + s, ph_full[s]);
+      ph_full[s] ^= 1;
+#ifdef NBM_TC_TRACE
+      if (blockIdx.x < 2 && gcount < 64 && (s == 0 || s == 3)) g_w256_ld[blockIdx.x][gcount][s == 0 ? 2 : 3] = clock64();
+#endif
+      if (!leader) {
+        tc::arrive_leader(bfull + s);
+        continue;
+      }
       tc::tc_fence_after();
-      const uint32_t wb = sb + L::oW + st * SLICE;
+      const uint32_t wb = ring + s * HSLICE;
+#pragma unroll
       for (int k = 0; k < 4; ++k) {
         const int kk = s * 4 + k;   // global K-step (16)
-        uint64_t ad, bd;
-        if (!bwd) {   // forward: A = h (K-major), B = slice [256 o][64 i] K-major (LBO 4096, SBO 128)
-          ad = tc::sdesc(a0 + kk * 2 * LBO_ACT, LBO_ACT, 128);
-          bd = tc::sdesc(wb + k * 2 * 4096, 4096, 128);
-        } else {      // dH: A = G (K-major over o), B = slice [64 o][256 i] MN-major (LBO 128, SBO 1024)
-          ad = tc::sdesc(a0 + kk * 2 * LBO_ACT, LBO_ACT, 128);
-          bd = tc::sdesc(wb + k * 256, 128, 1024);
-        }
-        tc::mma_bf16(tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+        const uint64_t ad = tc::sdesc(a0 + kk * 2 * LBO_ACT, LBO_ACT, 128);
+        // forward: B = [128 o][64 i] K-major (LBO 2048, SBO 128); dH: B = [64 o][128 i] MN-major
+        const uint64_t bd = bwd ? tc::sdesc(wb + k * 256, 128, 1024) : tc::sdesc(wb + k * 4096, 2048, 128);
+        tc::mma2_bf16(tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
       }
-      tc::mma_commit(bempty + st);
-      empty_armed[st] = true;
-      if (s + 2 < 4) load_slice(st, bwd, l, s + 2);
-      else if (has_next) load_slice(st, nbwd, nl, s - 2);
+      tc::mma2_commit(bempty + s);
     }
-    tc::mma_commit(bmma);
+    if (leader) tc::mma2_commit(bmma);
+    ringUsed = true;
+    ++gcount;
   };
-  auto wait_mma = [&]() {
-    tc::mbar_wait(bmma, ph_mma);
-    ph_mma ^= 1;
+  auto wait_bar = [&](uint64_t* b, uint32_t& ph) {
+    tc::mbar_wait(b, ph);
+    ph ^= 1;
     tc::tc_fence_after();
   };
 
-  constexpr uint32_t ID_FWD = tc::idesc_bf16(kB, W, 0, 0);
-  constexpr uint32_t ID_DH = tc::idesc_bf16(kB, W, 0, 1);
-  constexpr uint32_t ID_DW = tc::idesc_bf16(128, W, 1, 1);
+  constexpr uint32_t ID_FWD = tc::idesc_bf16(2 * kB, W, 0, 0);
+  constexpr uint32_t ID_DH = tc::idesc_bf16(2 * kB, W, 0, 1);
+  constexpr uint32_t ID_DW = tc::idesc_bf16(2 * kB, W, 1, 1);
   // small gradients per lane (column 64 cg + 32 k + lane): b_1..b_NH, W1[:,0..2], wo
   constexpr int NV = NH + 4;
   float g[NV][2];
   float gbo = 0.0f;
   double lossAcc = 0.0;
-  float* rep = P.rep + (int64_t)(cta % P.nrep) * 2 * prm.p_stride;
+  float* rep = P.rep + (int64_t)(q % P.nrep) * 2 * prm.p_stride;
+  bool pend = false;   // TMEM [256,512) holds an unflushed dW
+  int pendNet = 0, pendL = 2;
 
+  // this CTA's 128 outputs x 256 inputs of dW_pendL.  The replicas hold hidden-weight blocks
+  // input-quad-major ([i/4][o][i%4], see k_reduce_rep), so one warp-wide red.v4 covers 32
+  // consecutive outputs = 512 contiguous bytes.
+  auto flush_dw = [&]() {
+    float* out = rep + (int64_t)pendNet * prm.p_stride + L::tWl(pendL) + (int64_t)(kB * rank + row) * 4;
+    for (int k = 0; k < 2; ++k) {
+      const int c = 2 * cg + k;
+      float v[32];
+      tc::tmem_ld32(tmem + tlane + 256u + (uint32_t)(c * 32), v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        red4(out + (int64_t)(c * 8 + i) * (W * 4), v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+    pend = false;
+  };
   auto flush_small = [&](int net) {
     float* out = rep + (int64_t)net * prm.p_stride;
     for (int k = 0; k < 2; ++k) {
@@ -273,22 +329,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
     }
   };
 
-  int seg = 0;
-  for (int t = t0; t < t1; ++t) {
-    while (t >= firstTile[seg + 1]) ++seg;
+  if (u0 < u1 && tid == 0) queue_gemm(false, prm.seg.net[seg_of(u0)], 2);
+  int curNet = -1;
+  for (int u = u0; u < u1; ++u) {
+    const int seg = seg_of(u);
     const int kind = prm.seg.kind[seg], net = prm.seg.net[seg];
     const int per = kind == kSegStencil ? kPT : kB;
-    const int first = (t - firstTile[seg]) * per;
-    const int nvalid = min(per, segCnt[seg] - first);
+    const int first = ((u - firstPair[seg]) * 2 + (int)rank) * per;
+    const int nvalid = max(0, min(per, segCnt[seg] - first));   // 0: the pair's odd tail (all rows void)
+    const int nextNet = u + 1 < u1 ? prm.seg.net[seg_of(u + 1)] : -1;
     if (net != curNet) {
       __syncthreads();
       if (TRAIN && curNet >= 0) flush_small(curNet);
       load_net(net);
       curNet = net;
-      if (tid == 0) {   // queue the first GEMM's slices (stages are idle between tiles)
-        load_slice(0, false, 2, 0);
-        load_slice(1, false, 2, 1);
-      }
       __syncthreads();
     }
     // ---- gather ----
@@ -320,25 +374,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
       sX[4 * tid] = x0; sX[4 * tid + 1] = x1; sX[4 * tid + 2] = x2;
     }
     __syncthreads();
+    TRW(0);
     const float x0 = sX[4 * row], x1 = sX[4 * row + 1], x2 = sX[4 * row + 2];
-    // ---- layer 1 -> h1 (buffer 0, parked copy) ----
+    // ---- layer 1 -> h1 (tile 0, parked copy) ----
     for (int k = 0; k < 2; ++k) {
       float h[32];
       layer1(2 * cg + k, x0, x1, x2, h);
-      put_chunk(aBuf[0], TRAIN ? hscr : nullptr, row, 2 * cg + k, h);
+      put_chunk(aBuf[0], nullptr, row, 2 * cg + k, h);
     }
-    if (TRAIN) asm volatile("fence.proxy.async.global;" ::: "memory");   // parked h1 -> later bulk reads
     tc::fence_proxy_async_smem();
+    tc::tc_fence_before();
     __syncthreads();
+    tc::cluster_sync_relaxed();   // both CTAs' A tiles are written before the leader's pair MMA
+    tc::tc_fence_after();
+    if (TRAIN && tid == 0) {      // park h1 (bulk store; completion waited before the backward)
+      tc::bulk_copy_s2g(myScr + hslot(1), aBuf[0], ACT);
+      tc::bulk_commit();
+    }
+    TRW(1);
     // ---- forward hidden layers ----
     for (int l = 2; l <= NH; ++l) {
-      const uint32_t ain = aBuf[(l - 2) & 1];
-      if (tid == 0) {
-        // next GEMM: forward l+1, or (training) the backward dH of layer NH
-        const bool has_next = (l < NH) || TRAIN;
-        gemm_streamed(ain, false, l, ID_FWD, l < NH ? l + 1 : NH, l == NH, has_next);
+      if (tid == 0) issue_gemm(aBuf[(l - 2) & 1], false, ID_FWD);
+      if (l == 3) TRW(24);
+      if (TRAIN && pend) flush_dw();   // the previous tile's dW_2, under this GEMM
+      if (tid == 0) {                  // the next GEMM's slices
+        if (l < NH) queue_gemm(false, net, l + 1);
+        else if (TRAIN) queue_gemm(true, net, NH);
+        else if (nextNet >= 0) queue_gemm(false, nextNet, 2);
       }
-      wait_mma();
+      if (l == 3) TRW(25);
+      if (TRAIN && tid == 0) tc::bulk_wait_read0();   // parked copies have left the tiles
+      wait_bar(bmma, ph_mma);
+      TRW(2 + 2 * (l - 2));
       float up = 0.0f;
       for (int k = 0; k < 2; ++k) {
         const int c = 2 * cg + k;
@@ -347,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = th(v[j] + sBias[(l - 1) * W + c * 32 + j]);
         if (l < NH) {
-          put_chunk(aBuf[(l - 1) & 1], TRAIN ? hscr + (int64_t)(l - 1) * ACT : nullptr, row, c, v);
+          put_chunk(aBuf[(l - 1) & 1], nullptr, row, c, v);
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) up = fmaf(sWo[c * 32 + j], v[j], up);
@@ -355,24 +422,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
         }
       }
       if (l == NH) sUp[cg * kB + row] = up;
-      if (TRAIN && l < NH) asm volatile("fence.proxy.async.global;" ::: "memory");
       tc::tc_fence_before();
       if (l < NH) tc::fence_proxy_async_smem();
       __syncthreads();
+      if (l < NH) tc::cluster_sync_relaxed();
+      tc::tc_fence_after();
+      if (TRAIN && l < NH && tid == 0) {   // park h_l
+        tc::bulk_copy_s2g(myScr + hslot(l), aBuf[(l - 1) & 1], ACT);
+        tc::bulk_commit();
+      }
+      TRW(3 + 2 * (l - 2));
     }
     if (tid < kB) {
-      const float u = ((sUp[tid] + sUp[kB + tid]) + sUp[2 * kB + tid]) + sUp[3 * kB + tid] + sWo[W];
-      if (!TRAIN && tid < nvalid) prm.u_out[sItem[tid]] = u;
-      sU[tid] = u;
+      const float uu = ((sUp[tid] + sUp[kB + tid]) + sUp[2 * kB + tid]) + sUp[3 * kB + tid] + sWo[W];
+      if (!TRAIN && tid < nvalid) prm.u_out[sItem[tid]] = uu;
+      sU[tid] = uu;
     }
     __syncthreads();
-    if (!TRAIN) {
-      if (tid == 0) {   // restore the next tile's first slices
-        load_slice(0, false, 2, 0);
-        load_slice(1, false, 2, 1);
-      }
-      continue;
-    }
+    if (!TRAIN) continue;
     // ---- residual epilogue ----
     if (kind == kSegStencil) {
       if (tid < kPT) {
@@ -414,7 +481,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
       for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
       gbo += b;
     }
-    // ---- G_NH = ub wo (1 - h_NH^2) -> buffer (NH-1)&1 ----
+    const uint32_t gb = aBuf[(NH - 1) & 1];   // G_l (own rows, all outputs), then the dW operand G-halves
+    const uint32_t hb = aBuf[NH & 1];         // the dW operand h-halves
+    // ---- G_NH = ub wo (1 - h_NH^2) -> gb + parked copy ----
     for (int k = 0; k < 2; ++k) {
       const int c = 2 * cg + k;
       float hv[32], v[32];
@@ -424,57 +493,63 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
       g[NH + 3][k] += tsum(v, lane);
 #pragma unroll
       for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
-      put_chunk(aBuf[(NH - 1) & 1], nullptr, row, c, hv);
+      put_chunk(gb, nullptr, row, c, hv);
       g[NH - 1][k] += tsum(hv, lane);
     }
-    tc::tc_fence_before();
     tc::fence_proxy_async_smem();
+    tc::tc_fence_before();
+    if (tid == 0) {   // all parked h are complete: the epilogues read them back with ld.global
+      tc::bulk_wait0();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
     __syncthreads();
+    tc::cluster_sync_relaxed();
+    tc::tc_fence_after();
+    if (tid == 0) {   // park G_NH
+      tc::bulk_copy_s2g(myScr + gslot(NH), gb, ACT);
+      tc::bulk_commit();
+    }
+    TRW(10);
     // ---- backward hidden layers ----
     for (int l = NH; l >= 2; --l) {
-      const uint32_t gb = aBuf[(l - 1) & 1];   // G_l
-      const uint32_t hb = aBuf[(l - 2) & 1];   // h_{l-1}
-      // dW_l in two 128-output halves through the TMEM scratch, flushed by vector reductions
-      for (int half = 0; half < 2; ++half) {
-        if (tid == 0) {
-          tc::tc_fence_after();
-          for (int kk = 0; kk < kB / 16; ++kk)
-            tc::mma_bf16(tmem + 256, tc::sdesc(gb + half * 16 * LBO_ACT + kk * 256, 128, LBO_ACT),
-                         tc::sdesc(hb + kk * 256, 128, LBO_ACT), ID_DW, kk > 0 ? 1u : 0u);
-          tc::mma_commit(bmma);
-        }
-        wait_mma();
-        float* out = rep + (int64_t)curNet * prm.p_stride + L::tWl(l) + (int64_t)(half * 128 + row) * W;
-        for (int k = 0; k < 2; ++k) {
-          const int c = 2 * cg + k;
-          float v[32];
-          tc::tmem_ld32(tmem + tlane + 256u + (uint32_t)(c * 32), v);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) red4(out + c * 32 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
-        tc::tc_fence_before();
-        __syncthreads();
-      }
-      // acc = G_l W_l (streamed backward slices); then the next slices: dH_{l-1} or the next tile
+      if (tid == 0) issue_gemm(gb, true, ID_DH);   // acc = G_l W_l
+      TRW(26 + 3 * (NH - l));
+      if (pend) flush_dw();            // dW_{l+1} under the dH GEMM
       if (tid == 0) {
-        tc::tc_fence_after();
-        if (l > 2) gemm_streamed(gb, true, l, ID_DH, l - 1, true, true);
-        else gemm_streamed(gb, true, l, ID_DH, 2, false, true);   // next tile's forward W_2
+        if (l > 2) queue_gemm(true, net, l - 1);
+        else if (nextNet >= 0) queue_gemm(false, nextNet, 2);
+        tc::bulk_wait0();                 // parked G_l is complete (and gb has been read)
+        tc::arrive_remote(bpark, rank ^ 1u);
       }
-      wait_mma();
-      if (l > 2 && tid == 0) {   // bring h_{l-2} back into the buffer that held G_l
-        tc::mbar_arrive_expect_tx(bh, ACT);
-        tc::bulk_copy_g2s(gb, hscr + (int64_t)(l - 3) * ACT, ACT, bh);
+      TRW(27 + 3 * (NH - l));
+      wait_bar(bmma, ph_mma);
+      if (tid == 0) {
+        tc::mbar_wait(bpark, ph_park);    // the peer's parked G_l is complete
+        ph_park ^= 1;
+        // the dW operands: h_{l-1}[rows of CTA t][this CTA's input half] and
+        // G_l[rows of CTA t][the outputs this CTA owns], t = 0, 1
+        tc::mbar_arrive_expect_tx(bld, 4 * QTR);
+        for (int t = 0; t < 2; ++t) {
+          const uint8_t* scr = pairScr0 + (int64_t)t * L::kScr * ACT + rank * QTR;
+          tc::bulk_copy_g2s(hb + t * QTR, scr + hslot(l - 1), QTR, bld);
+          tc::bulk_copy_g2s(gb + t * QTR, scr + gslot(l), QTR, bld);
+        }
       }
+      TRW(28 + 3 * (NH - l));
+      TRW(11 + 4 * (NH - l));
+      uint32_t gk[2][16];   // G_{l-1}, bf16, for the next dH GEMM's A tile
+      const uint8_t* hprev = myScr + hslot(l - 1);
+#pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int c = 2 * cg + k;
         float v[32], hq[32];
         tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
-        get_chunk(hb, row, c, hq);
+        get_chunk_g(hprev, row, c, hq);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] *= 1.0f - hq[j] * hq[j];
         if (l - 1 >= 2) {
-          put_chunk(hb, nullptr, row, c, v);   // G_{l-1} in place of h_{l-1}
+#pragma unroll
+          for (int j = 0; j < 16; ++j) gk[k][j] = pk(v[2 * j], v[2 * j + 1]);
           g[l - 2][k] += tsum(v, lane);
         } else {   // layer 1: dW1 += G1 x^T, db1 += G1
           float tv[32];
@@ -490,16 +565,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
           g[0][k] += tsum(v, lane);
         }
       }
-      if (l > 2 && tid == 0) {   // the reload must land before dW_{l-1} reads it
-        tc::mbar_wait(bh, ph_h);
-        ph_h ^= 1;
-      }
-      tc::fence_proxy_async_smem();
       tc::tc_fence_before();
-      __syncthreads();
+      __syncthreads();   // this CTA's TMEM reads (flush, epilogue) are done
+      TRW(12 + 4 * (NH - l));
+      if (tid == 0) {
+        tc::mbar_wait(bld, ph_ld);   // own halves landed (+ the peer's forward, leader)
+        ph_ld ^= 1;
+        if (!leader) {
+          tc::arrive_leader(bld);
+        } else {
+          tc::tc_fence_after();
+          // dW_l[o][i] = sum over the pair's 256 rows: K-steps 0..7 rows of CTA 0, 8..15 of CTA 1
+          for (int t = 0; t < 2; ++t)
+            for (int kk = 0; kk < kB / 16; ++kk)
+              tc::mma2_bf16(tmem + 256, tc::sdesc(gb + t * QTR + kk * 256, 128, LBO_ACT),
+                            tc::sdesc(hb + t * QTR + kk * 256, 128, LBO_ACT), ID_DW, (t | kk) ? 1u : 0u);
+          tc::mma2_commit(bdw);
+        }
+      }
+      wait_bar(bdw, ph_dw);
+      pend = true;
+      pendNet = net;
+      pendL = l;
+      TRW(13 + 4 * (NH - l));
+      if (l > 2) {   // G_{l-1} (own rows, all outputs) -> gb for the next dH GEMM
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int c = 2 * cg + k;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            sts4(gb + (uint32_t)((c * 4 + qq) * LBO_ACT + row * 16), gk[k][4 * qq], gk[k][4 * qq + 1],
+                 gk[k][4 * qq + 2], gk[k][4 * qq + 3]);
+        }
+        tc::fence_proxy_async_smem();
+        tc::tc_fence_before();
+        __syncthreads();
+        tc::cluster_sync_relaxed();   // both A tiles written
+        tc::tc_fence_after();
+        if (tid == 0) {               // park G_{l-1}
+          tc::bulk_copy_s2g(myScr + gslot(l - 1), gb, ACT);
+          tc::bulk_commit();
+        }
+      }
+      TRW(14 + 4 * (NH - l));
     }
   }
   if (TRAIN) {
+    if (pend) flush_dw();
     __syncthreads();
     if (curNet >= 0) flush_small(curNet);
     for (int o = 16; o; o >>= 1) lossAcc += __shfl_xor_sync(0xffffffffu, lossAcc, o);
@@ -509,24 +621,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
     if (tid == 0) {
       double s = 0.0;
       for (int w = 0; w < kThreads / 32; ++w) s += wl[w];
-      prm.lpart[cta] = s;
+      prm.lpart[blockIdx.x] = s;
     }
   }
-  // drain the slice pipeline before exit (queued bulk copies must complete)
-  if (tid == 0) {
-    for (int st = 0; st < 2; ++st) {
-      if (pending_full[st]) tc::mbar_wait(bfull + st, ph_full[st]);
-      if (empty_armed[st]) tc::mbar_wait(bempty + st, ph_empty[st]);
-    }
-  }
+  if (tid == 0) tc::bulk_wait0();
   tc::tc_fence_before();
-  __syncthreads();
+  tc::cluster_sync();   // no pair MMA may still target the peer's TMEM
   tc::tc_fence_after();
-  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+  if (warp == 0) tc::tmem_dealloc2(tmem, 512);
 }
 
-// forward image: slice s of W_l = [256 o][64 i] K-major core layout: (i'/8)*4096 + o*16 + (i'%8)*2
-// backward image: slice s of W_l = [64 o][256 i] MN-major core layout: (i/8)*1024 + o'*16 + (i%8)*2
+// forward image: [net][l][slice s][half r] = W_l[o in [128 r, 128 r + 128)][i in [64 s, 64 s + 64)],
+//   K-major core layout: (i'/8)*2048 B + o'*16 B + (i'%8)*2 B
+// backward image: [net][l][slice s][half r] = W_l[o in [64 s, 64 s + 64)][i in [128 r, 128 r + 128)],
+//   MN-major core layout: (i'/8)*1024 B + o'*16 B + (i'%8)*2 B
 __global__ void k_pack_w256(const float* __restrict__ theta, int64_t p_net, int nhh, int n_nets,
                             uint16_t* __restrict__ wf, uint16_t* __restrict__ wb) {
   const int64_t total = (int64_t)n_nets * nhh * W * W;
@@ -536,17 +644,26 @@ __global__ void k_pack_w256(const float* __restrict__ theta, int64_t p_net, int 
     const int r = (int)(e % (W * W)), o = r / W, i = r % W;
     const uint16_t v = __bfloat16_as_ushort(__float2bfloat16_rn(
         theta[(int64_t)net * p_net + 4 * W + (int64_t)(l - 2) * (W * W + W) + r]));
-    const int64_t base = m * W * W;   // 4 slices of 64*256 elements
+    const int64_t base = m * W * W;   // 4 slices x 2 halves of 8192 elements
     {
-      const int s = i / 64, ip = i % 64;
-      wf[base + (int64_t)s * 64 * W + (ip / 8) * 2048 + o * 8 + (ip % 8)] = v;
+      const int s = i / 64, ip = i % 64, h = o / 128, op = o % 128;
+      wf[base + (int64_t)(s * 2 + h) * 8192 + (ip / 8) * 1024 + op * 8 + (ip % 8)] = v;
     }
     {
-      const int s = o / 64, op = o % 64;
-      wb[base + (int64_t)s * 64 * W + (i / 8) * 512 + op * 8 + (i % 8)] = v;
+      const int s = o / 64, op = o % 64, h = i / 128, ip = i % 128;
+      wb[base + (int64_t)(s * 2 + h) * 8192 + (ip / 8) * 512 + op * 8 + (ip % 8)] = v;
     }
   }
 }
+
+#ifdef NBM_TC_TRACE
+extern "C" int nbm_debug_w256_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_w256_trace, sizeof(g_w256_trace));
+}
+extern "C" int nbm_debug_w256_ld(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_w256_ld, sizeof(g_w256_ld));
+}
+#endif
 
 template <int NH, bool TRAIN>
 static cudaError_t launch_w256_t(const W256Params& p, int grid, cudaStream_t s) {
@@ -564,6 +681,8 @@ static cudaError_t launch_w256_t(const W256Params& p, int grid, cudaStream_t s) 
 cudaError_t launch_mlp_w256(int n_hidden, bool train, const MlpParams& m, const uint16_t* wf,
                             const uint16_t* wb, uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s) {
   W256Params p{m, wf, wb, hscr, rep, nrep};
+  grid &= ~1;   // CTA pairs
+  if (grid < 2 || nrep < 1) return cudaErrorInvalidValue;
   switch (n_hidden) {
     case 2: return train ? launch_w256_t<2, true>(p, grid, s) : launch_w256_t<2, false>(p, grid, s);
     case 3: return train ? launch_w256_t<3, true>(p, grid, s) : launch_w256_t<3, false>(p, grid, s);
@@ -579,16 +698,25 @@ cudaError_t launch_pack_w256(const ArchInfo& a, const float* theta, uint16_t* wf
   return cudaGetLastError();
 }
 
-// K4r for W = 256: grad = sum of the replicas (fixed replica order), loss from lpart.
+// K4r for W = 256: grad = sum of the replicas (fixed replica order), loss from lpart.  The
+// hidden-weight blocks W_l[o][i] sit input-quad-major in the replicas: [i/4][o][i%4].
 __global__ void k_reduce_rep(const float* __restrict__ rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets,
-                             const double* __restrict__ lpart, int G, float* __restrict__ grad,
+                             int n_hidden, const double* __restrict__ lpart, int G, float* __restrict__ grad,
                              float* __restrict__ loss, int* __restrict__ err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n_nets * p_net) {
     const int net = (int)(i / p_net);
     const int64_t j = i - net * p_net;
+    int64_t jr = j;   // position in the replica
+    if (j >= 4 * W && j < 4 * W + (int64_t)(n_hidden - 1) * (W * W + W)) {
+      const int64_t lo = (j - 4 * W) % (W * W + W);
+      if (lo < W * W) {
+        const int o = (int)(lo / W), in = (int)(lo % W);
+        jr = j - lo + ((int64_t)(in / 4) * W + o) * 4 + (in % 4);
+      }
+    }
     double s = 0.0;
-    for (int r = 0; r < nrep; ++r) s += rep[((int64_t)r * 2 + net) * p_stride + j];
+    for (int r = 0; r < nrep; ++r) s += rep[((int64_t)r * 2 + net) * p_stride + jr];
     const float v = (float)s;
     grad[i] = v;
     if (!isfinite(v)) atomicOr(err, kErrNonfinite);
@@ -601,10 +729,11 @@ __global__ void k_reduce_rep(const float* __restrict__ rep, int nrep, int64_t p_
   }
 }
 
-cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets,
+cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets, int n_hidden,
                               const double* lpart, int G, float* grad, float* loss, int* err, cudaStream_t s) {
   const int64_t P = n_nets * p_net;
-  k_reduce_rep<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(rep, nrep, p_net, p_stride, n_nets, lpart, G, grad, loss, err);
+  k_reduce_rep<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(rep, nrep, p_net, p_stride, n_nets, n_hidden, lpart, G,
+                                                           grad, loss, err);
   return cudaGetLastError();
 }
 

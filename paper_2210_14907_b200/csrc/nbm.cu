@@ -3,6 +3,7 @@
 // timing hook.  See DESIGN.md section 5 for the kernel list.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <vector>
@@ -285,9 +286,10 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   const size_t nhh = ai.n_hidden > 1 ? ai.n_hidden - 1 : 1;
   ALLOC(w.wimg, (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t));
   const bool w256 = is_w256(ai);
-  w.nrep = w256 ? 4 : 0;
+  w.nrep = w256 ? 16 : 0;   // replicas of the W = 256 gradient (fewer CTAs per L2 address)
+  if (w256 && getenv("NBM_W256_REPLICAS")) w.nrep = atoi(getenv("NBM_W256_REPLICAS"));
   ALLOC(w.wimg_b, w256 ? (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t) : 16);
-  ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * nhh * 128 * ai.width * 2 : 16);
+  ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * (nhh + 2) * 128 * ai.width * 2 : 16);   // h_1..h_{NH-1}, G x2
   ALLOC(w.rep, w256 ? (size_t)w.nrep * 2 * ((ai.p_net + 3) & ~3ll) * sizeof(float) : 16);
 #undef ALLOC
   for (size_t i = 0; i < ptrs.size(); ++i) {
@@ -460,7 +462,7 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
   launches += 1;
   if (ev) cudaEventRecord(ev[2], s);
   if (e == cudaSuccess)
-    e = is_w256(A) ? launch_reduce_rep(w.rep, w.nrep, A.p_net, (A.p_net + 3) & ~3ll, A.n_nets, w.lpart,
+    e = is_w256(A) ? launch_reduce_rep(w.rep, w.nrep, A.p_net, (A.p_net + 3) & ~3ll, A.n_nets, A.n_hidden, w.lpart,
                                        w.grid_mlp, grad_dev, loss_dev, w.err, s)
                    : launch_reduce(h, grad_dev, loss_dev, s);
   launches += 1;

@@ -94,7 +94,7 @@ struct Workspace {
   int* err;             // sticky error word
   uint16_t* wimg;       // [2][NH-1][W*W] bf16 weight image (tensor-core path)
   uint16_t* wimg_b;     // W = 256: backward-sliced image
-  uint8_t* hscr;        // W = 256: parked activations [grid][NH-1][64 KB]
+  uint8_t* hscr;        // W = 256: parked activations and G [grid][NH+1][64 KB]
   float* rep;           // W = 256: gradient replicas [nrep][2][p_stride]
   int nrep;
   // eval
@@ -171,7 +171,7 @@ cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t*
 cudaError_t launch_mlp_w256(int n_hidden, bool train, const MlpParams& m, const uint16_t* wf, const uint16_t* wb,
                             uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s);
 cudaError_t launch_pack_w256(const ArchInfo& a, const float* theta, uint16_t* wf, uint16_t* wb, cudaStream_t s);
-cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets,
+cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets, int n_hidden,
                               const double* lpart, int G, float* grad, float* loss, int* err, cudaStream_t s);
 // reduce
 cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s);
