@@ -38,6 +38,7 @@ constexpr uint32_t ACT = kB * W * 2;        // 64 KB bf16 activation tile
 constexpr uint32_t QTR = ACT / 2;           // 32 KB: one 128-column half of it
 constexpr uint32_t HSLICE = 64 * 128 * 2;   // 16 KB: one CTA's N-half of a 64-deep K-slice
 constexpr uint32_t LBO_ACT = kB * 16;       // 2048: K-core stride of activation tiles
+static_assert(kThreads * 128 == ACT, "one discarded L2 line per thread per parked tile");
 
 template <int NH>
 struct Lay {
@@ -91,6 +92,10 @@ __device__ __forceinline__ void sts4(uint32_t a, uint32_t x, uint32_t y, uint32_
 }
 __device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+// drop a dead 128-byte line of the parked scratch from L2 without writing it back to HBM
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 __device__ __forceinline__ uint4 ldcg4(const uint8_t* p) {
   uint4 r;
@@ -329,6 +334,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     }
   };
 
+  // global loads of pair-tile uu for thread tid < kB: item slot tid (index + aux) and the
+  // coordinates of this CTA's tile row tid (stencil arm generated on the fly); issued one tile ahead
+  struct Fetch { int item; float aux, x0, x1, x2; };
+  auto fetch = [&](int uu) -> Fetch {
+    Fetch f{-1, 0.0f, 0.0f, 0.0f, 0.0f};
+    if (uu >= u1 || tid >= kB) return f;
+    const int sg = seg_of(uu);
+    const int knd = prm.seg.kind[sg];
+    const int pr = knd == kSegStencil ? kPT : kB;
+    const int fst = ((uu - firstPair[sg]) * 2 + (int)rank) * pr;
+    const int nv = max(0, min(pr, segCnt[sg] - fst));
+    const int* its = prm.seg.items[sg] + segStart[sg];
+    if (tid < pr && tid < nv) {
+      f.item = its[fst + tid];
+      f.aux = prm.aux_by_item[sg] ? prm.seg.aux[sg][f.item] : prm.seg.aux[sg][segStart[sg] + fst + tid];
+    }
+    if (knd == kSegStencil) {
+      const int j = tid / kPT, p = tid - j * kPT;
+      if (j < 7 && p < nv) {
+        const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + p];
+        f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
+        if (j > 0) {   // arms +x, -x, +y, -y, +z, -z (exact on the lattice)
+          const float hs = (j & 1) ? prm.h : -prm.h;
+          if (j <= 2) f.x0 = __fadd_rn(f.x0, hs); else if (j <= 4) f.x1 = __fadd_rn(f.x1, hs); else f.x2 = __fadd_rn(f.x2, hs);
+        }
+      }
+    } else if (tid < nv) {
+      const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + tid];
+      f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
+    }
+    return f;
+  };
+  Fetch cur = fetch(u0), nxt;
   if (u0 < u1 && tid == 0) queue_gemm(false, prm.seg.net[seg_of(u0)], 2);
   int curNet = -1;
   for (int u = u0; u < u1; ++u) {
@@ -345,33 +383,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       curNet = net;
       __syncthreads();
     }
-    // ---- gather ----
-    const int* items = prm.seg.items[seg] + segStart[seg];
-    if (tid < per) {
-      const int it = tid < nvalid ? items[first + tid] : -1;
-      sItem[tid] = it;
-      float a = 0.0f;
-      if (it >= 0) a = prm.aux_by_item[seg] ? prm.seg.aux[seg][it] : prm.seg.aux[seg][segStart[seg] + first + tid];
-      sAux[tid] = a;
-    }
-    __syncthreads();
+    // ---- gather: items, aux and coordinates were prefetched during the previous tile ----
     if (tid < kB) {
-      float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
-      if (kind == kSegStencil) {
-        const int j = tid / kPT, p = tid - j * kPT;
-        if (j < 7 && p < nvalid) {
-          const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[p];
-          x0 = src[0]; x1 = src[1]; x2 = src[2];
-          if (j > 0) {
-            const float hs = (j & 1) ? prm.h : -prm.h;
-            if (j <= 2) x0 = __fadd_rn(x0, hs); else if (j <= 4) x1 = __fadd_rn(x1, hs); else x2 = __fadd_rn(x2, hs);
-          }
-        }
-      } else if (tid < nvalid) {
-        const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[tid];
-        x0 = src[0]; x1 = src[1]; x2 = src[2];
+      if (tid < per) {
+        sItem[tid] = cur.item;
+        sAux[tid] = cur.aux;
       }
-      sX[4 * tid] = x0; sX[4 * tid + 1] = x1; sX[4 * tid + 2] = x2;
+      sX[4 * tid] = cur.x0; sX[4 * tid + 1] = cur.x1; sX[4 * tid + 2] = cur.x2;
     }
     __syncthreads();
     TRW(0);
@@ -396,6 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     for (int l = 2; l <= NH; ++l) {
       if (tid == 0) issue_gemm(aBuf[(l - 2) & 1], false, ID_FWD);
       if (l == 3) TRW(24);
+      if (l == 2) nxt = fetch(u + 1);  // the next tile's loads overlap this tile
       if (TRAIN && pend) flush_dw();   // the previous tile's dW_2, under this GEMM
       if (tid == 0) {                  // the next GEMM's slices
         if (l < NH) queue_gemm(false, net, l + 1);
@@ -439,6 +458,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       sU[tid] = uu;
     }
     __syncthreads();
+    cur = nxt;
     if (!TRAIN) continue;
     // ---- residual epilogue ----
     if (kind == kSegStencil) {
@@ -584,6 +604,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
         }
       }
       wait_bar(bdw, ph_dw);
+      // both CTAs' bulk loads of h_{l-1} and G_l (and this CTA's act' reads) are complete: the
+      // parked copies are dead, so they leave L2 without a write-back to HBM
+      discard_l2(myScr + hslot(l - 1) + tid * 128);
+      discard_l2(myScr + gslot(l) + tid * 128);
       pend = true;
       pendNet = net;
       pendL = l;
