@@ -37,6 +37,13 @@ def mlp_macs(sizes):
     return fwd, 2 * fwd + dh
 
 
+def kernel_name(cfg):
+    w = cfg["sizes"][1]
+    if cfg["prec"] == inputs.PREC_FP32:
+        return "k_mlp_fp32w" if w >= 128 else "k_mlp_fp32"
+    return "k_mlp_w256 (tcgen05 cta_group::2)" if w == 256 else "k_mlp_tc (tcgen05)"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -110,7 +117,7 @@ def cpu_baseline(cfg, seconds_hint=15.0):
         n = min(cfg["N"], n * max(2, int(seconds_hint / 4 / max(dt, 1e-3))))
         nb = max(1, n * cfg["Nb"] // cfg["N"])
     return {"value": n / dt, "unit": "pts/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{n} interior + {nb} boundary points of {cfg['name']} (fp64 loss+grad, "
+            "sample": f"{n} interior + {nb} boundary points of {cfg['label']} (fp64 loss+grad, "
                       f"{dt:.2f} s)"}
 
 
@@ -140,7 +147,7 @@ def run_reference(args, cfg, rank, world):
             "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["name"], "points_per_step": n, "boundary_per_step": nb,
+            "config": {"workload": cfg["label"], "points_per_step": n, "boundary_per_step": nb,
                        "note": "bounded sample of the workload; oracle on host cores"},
             "cpu_baseline": {"value": val, "unit": "pts/s", "cores": oracle.num_threads(),
                              "kind": "oracle", "sample": f"{n} + {nb} points per step"},
@@ -155,6 +162,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--width", type=int, default=None)
+    ap.add_argument("--prec", default=None, choices=["fp32", "bf16"], help="override the config's precision (c4/c5)")
     ap.add_argument("--impl", default="nbm", choices=["nbm", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -163,7 +171,10 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     rank, world, local = dp.env_rank_world()
-    cfg = inputs.config(args.config, width=args.width)
+    prec = None if args.prec is None else (inputs.PREC_FP32 if args.prec == "fp32" else inputs.PREC_BF16)
+    cfg = inputs.config(args.config, width=args.width, prec=prec)
+    cfg["label"] = cfg["name"] + (f"-w{cfg['sizes'][1]}" if cfg["name"] == "c5" else "") + \
+        ("" if prec is None else ("-fp32" if prec == inputs.PREC_FP32 else "-bf16"))
     if args.points:
         cfg["N"] = args.points
         cfg["Nb"] = max(1, args.points // 8)
@@ -285,7 +296,7 @@ def main():
         bound, peak_note = "tensor", f"bf16 dense, {src} (MEASURED_PEAKS.json)"
     achieved = flop_launch / mlp_avg_s / 1e12
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{cfg['name']}.json")
+    tp = os.path.join(ROOT, "profiles", f"traffic_{cfg['label']}.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("bytes_per_launch")
     val = Ng * args.steps / (tot_ms / 1e3)
@@ -296,11 +307,11 @@ def main():
         "loss_grad_pts_per_sec": Ng * calls / (lg_ms_max / 1e3) if calls else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg["prec"] == 0 else "bf16",
         "data": "synthetic (seeded Philox lattice points; manufactured two-phase Poisson)",
-        "config": {"workload": cfg["name"], "points_per_gpu": N, "boundary_per_gpu": Nb,
+        "config": {"workload": cfg["label"], "points_per_gpu": N, "boundary_per_gpu": Nb,
                    "global_points": Ng, "mlp": "x".join(map(str, cfg["sizes"])), "n_nets": cfg["n_nets"],
                    "h": cfg["h"], "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": ("k_mlp_fp32" if cfg["prec"] == inputs.PREC_FP32 else "k_mlp_tc (tcgen05)") + " fused fwd/residual/bwd",
+                     "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name(cfg) + " fused fwd/residual/bwd",
                      "flop_per_launch": flop_launch, "avg_launch_ms": mlp_avg_s * 1e3,
                      "share_of_step": (mlp_ms / max(calls, 1)) / (tot_ms / args.steps), "peak_src": peak_note},
         "gpu_launches": launches_per_step * args.steps,

@@ -722,17 +722,18 @@ cudaError_t launch_pack_w256(const ArchInfo& a, const float* theta, uint16_t* wf
   return cudaGetLastError();
 }
 
-// K4r for W = 256: grad = sum of the replicas (fixed replica order), loss from lpart.  The
-// hidden-weight blocks W_l[o][i] sit input-quad-major in the replicas: [i/4][o][i%4].
+// K4r for the replica paths (bf16 W = 256, fp32 W >= 128): grad = sum of the replicas in fixed
+// replica order, loss from lpart.  quad_major (bf16 W = 256): the hidden-weight blocks W_l[o][i]
+// sit input-quad-major in the replicas, [i/4][o][i%4]; otherwise in the natural layout.
 __global__ void k_reduce_rep(const float* __restrict__ rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets,
-                             int n_hidden, const double* __restrict__ lpart, int G, float* __restrict__ grad,
+                             int n_hidden, int quad_major, const double* __restrict__ lpart, int G, float* __restrict__ grad,
                              float* __restrict__ loss, int* __restrict__ err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n_nets * p_net) {
     const int net = (int)(i / p_net);
     const int64_t j = i - net * p_net;
     int64_t jr = j;   // position in the replica
-    if (j >= 4 * W && j < 4 * W + (int64_t)(n_hidden - 1) * (W * W + W)) {
+    if (quad_major && j >= 4 * W && j < 4 * W + (int64_t)(n_hidden - 1) * (W * W + W)) {
       const int64_t lo = (j - 4 * W) % (W * W + W);
       if (lo < W * W) {
         const int o = (int)(lo / W), in = (int)(lo % W);
@@ -754,9 +755,10 @@ __global__ void k_reduce_rep(const float* __restrict__ rep, int nrep, int64_t p_
 }
 
 cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets, int n_hidden,
-                              const double* lpart, int G, float* grad, float* loss, int* err, cudaStream_t s) {
+                              int quad_major, const double* lpart, int G, float* grad, float* loss, int* err,
+                              cudaStream_t s) {
   const int64_t P = n_nets * p_net;
-  k_reduce_rep<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(rep, nrep, p_net, p_stride, n_nets, n_hidden, lpart, G,
+  k_reduce_rep<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(rep, nrep, p_net, p_stride, n_nets, n_hidden, quad_major, lpart, G,
                                                            grad, loss, err);
   return cudaGetLastError();
 }

@@ -54,7 +54,7 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
   if (a->prec != NBM_PREC_FP32 && a->prec != NBM_PREC_BF16) { *why = "arch: bad precision"; return NBM_E_INVALID_ARCH; }
   int nh = a->n_layers - 2;
   bool ok = false;
-  if (a->prec == NBM_PREC_FP32 && a->act == NBM_ACT_TANH) ok = mlp_fp32_supported(W, nh);
+  if (a->prec == NBM_PREC_FP32 && a->act == NBM_ACT_TANH) ok = mlp_fp32_supported(W, nh) || mlp_fp32w_supported(W, nh);
   if (a->prec == NBM_PREC_BF16) ok = mlp_tc_supported(W, nh, a->act) || (W == 256 && nh >= 2 && nh <= 4 && a->act == NBM_ACT_TANH);
   if (!ok) {
     *why = "arch: unsupported (prec, act, width, depth) combination in this build";
@@ -187,12 +187,25 @@ void fill_common(const nbm_handle* h, MlpParams& p, const float* theta, float hf
 }
 
 bool is_w256(const ArchInfo& A) { return A.prec == NBM_PREC_BF16 && A.width == 256; }
+bool is_fp32w(const ArchInfo& A) { return A.prec == NBM_PREC_FP32 && A.width >= 128; }
+// paths whose gradients go through L2 replicas (per-tile dW flushes) instead of per-CTA partials
+bool uses_rep(const ArchInfo& A) { return is_w256(A) || is_fp32w(A); }
+
+// per-call weight images of the hidden layers (bf16 tensor-core layouts / fp32 wide-path slices)
+cudaError_t launch_pack(const nbm_handle* h, const float* theta, cudaStream_t s) {
+  const ArchInfo& A = h->arch;
+  const Workspace& w = h->ws;
+  if (is_fp32w(A)) return launch_pack_fp32w(A, theta, w.wimg32, s);
+  if (A.prec != NBM_PREC_BF16) return cudaSuccess;
+  return is_w256(A) ? launch_pack_w256(A, theta, w.wimg, w.wimg_b, s) : launch_pack_weights(A, theta, w.wimg, s);
+}
 
 cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cudaStream_t s) {
   const ArchInfo& A = h->arch;
   const Workspace& w = h->ws;
   if (is_w256(A))
     return launch_mlp_w256(A.n_hidden, train, p, w.wimg, w.wimg_b, w.hscr, w.rep, w.nrep, w.grid_base, s);
+  if (is_fp32w(A)) return launch_mlp_fp32w(A.width, A.n_hidden, train, p, w.wimg32, w.rep, w.nrep, w.grid_base, s);
   if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, A.act, train, p, w.grid_base, s);
   return launch_mlp_fp32(A.width, A.n_hidden, train, p, w.grid_base, s);
 }
@@ -285,12 +298,13 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   ALLOC(w.err, sizeof(int));
   const size_t nhh = ai.n_hidden > 1 ? ai.n_hidden - 1 : 1;
   ALLOC(w.wimg, (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t));
-  const bool w256 = is_w256(ai);
-  w.nrep = w256 ? 16 : 0;   // replicas of the W = 256 gradient (fewer CTAs per L2 address)
-  if (w256 && getenv("NBM_W256_REPLICAS")) w.nrep = atoi(getenv("NBM_W256_REPLICAS"));
+  const bool w256 = is_w256(ai), fw = is_fp32w(ai), urep = uses_rep(ai);
+  w.nrep = urep ? 16 : 0;   // gradient replicas (fewer CTAs per L2 address)
+  if (urep && getenv("NBM_W256_REPLICAS")) w.nrep = atoi(getenv("NBM_W256_REPLICAS"));
   ALLOC(w.wimg_b, w256 ? (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t) : 16);
   ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * (nhh + 2) * 128 * ai.width * 2 : 16);   // h_1..h_{NH-1}, G x2
-  ALLOC(w.rep, w256 ? (size_t)w.nrep * 2 * ((ai.p_net + 3) & ~3ll) * sizeof(float) : 16);
+  ALLOC(w.rep, urep ? (size_t)w.nrep * 2 * ((ai.p_net + 3) & ~3ll) * sizeof(float) : 16);
+  ALLOC(w.wimg32, fw ? (size_t)2 * nhh * 2 * ai.width * ai.width * sizeof(float) : 16);
 #undef ALLOC
   for (size_t i = 0; i < ptrs.size(); ++i) {
     e = cudaMalloc(ptrs[i], sizes[i]);
@@ -320,7 +334,7 @@ void nbm_destroy(nbm_handle* h) {
   void* ps[] = {h->d_problem, h->ws.cls, h->ws.aux_tmp, h->ws.blk_counts, h->ws.blk_offsets,
                 h->ws.counts, h->ws.list, h->ws.list_aux, h->ws.xrow_x, h->ws.xrow_u, h->ws.xrow_cot,
                 h->ws.xrow_tag, h->ws.xrec, h->ws.xlist, h->ws.part, h->ws.touched, h->ws.lpart,
-                h->ws.err, h->ws.wimg, h->ws.wimg_b, h->ws.hscr, h->ws.rep};
+                h->ws.err, h->ws.wimg, h->ws.wimg_b, h->ws.hscr, h->ws.rep, h->ws.wimg32};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : h->ev) cudaEventDestroy(ev);
@@ -398,11 +412,11 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
   if (ev) cudaEventRecord(ev[0], s);
   cudaError_t e = launch_classify(h, pts_dev, n, bpts_dev, nb, H, dm, dpl, terms, false, s);
   launches += 3;
-  if (e == cudaSuccess && A.prec == NBM_PREC_BF16) {
-    e = is_w256(A) ? launch_pack_w256(A, theta_dev, w.wimg, w.wimg_b, s) : launch_pack_weights(A, theta_dev, w.wimg, s);
+  if (e == cudaSuccess && (A.prec == NBM_PREC_BF16 || is_fp32w(A))) {
+    e = launch_pack(h, theta_dev, s);
     launches += 1;
   }
-  if (e == cudaSuccess && is_w256(A)) {
+  if (e == cudaSuccess && uses_rep(A)) {
     e = cudaMemsetAsync(w.rep, 0, (size_t)w.nrep * 2 * ((A.p_net + 3) & ~3ll) * sizeof(float), s);
   }
   if (e == cudaSuccess) e = launch_assemble_crossed(h, pts_dev, n, H, s);
@@ -462,8 +476,8 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
   launches += 1;
   if (ev) cudaEventRecord(ev[2], s);
   if (e == cudaSuccess)
-    e = is_w256(A) ? launch_reduce_rep(w.rep, w.nrep, A.p_net, (A.p_net + 3) & ~3ll, A.n_nets, A.n_hidden, w.lpart,
-                                       w.grid_mlp, grad_dev, loss_dev, w.err, s)
+    e = uses_rep(A) ? launch_reduce_rep(w.rep, w.nrep, A.p_net, (A.p_net + 3) & ~3ll, A.n_nets, A.n_hidden,
+                                        is_w256(A) ? 1 : 0, w.lpart, w.grid_mlp, grad_dev, loss_dev, w.err, s)
                    : launch_reduce(h, grad_dev, loss_dev, s);
   launches += 1;
   if (ev) {
@@ -500,8 +514,7 @@ int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_
   const ArchInfo& A = h->arch;
   const Workspace& w = h->ws;
   cudaError_t e = launch_classify(h, pts_dev, n, nullptr, 0, 1, 1.0, 1.0, NBM_TERM_ALL, true, s);
-  if (e == cudaSuccess && A.prec == NBM_PREC_BF16)
-    e = is_w256(A) ? launch_pack_w256(A, theta_dev, w.wimg, w.wimg_b, s) : launch_pack_weights(A, theta_dev, w.wimg, s);
+  if (e == cudaSuccess) e = launch_pack(h, theta_dev, s);
   MlpParams p;
   fill_common(h, p, theta_dev, 0.0f);
   for (int k = 0; k < 2; ++k) {

@@ -94,8 +94,9 @@ struct Workspace {
   int* err;             // sticky error word
   uint16_t* wimg;       // [2][NH-1][W*W] bf16 weight image (tensor-core path)
   uint16_t* wimg_b;     // W = 256: backward-sliced image
+  float* wimg32;        // fp32 W >= 128: [2][NH-1][2][W*W] transposed / natural hidden weights
   uint8_t* hscr;        // W = 256: parked activations and G [grid][NH+1][64 KB]
-  float* rep;           // W = 256: gradient replicas [nrep][2][p_stride]
+  float* rep;           // bf16 W = 256 / fp32 W >= 128: gradient replicas [nrep][2][p_stride]
   int nrep;
   // eval
   float* eval_aux;      // unused placeholder for symmetry
@@ -167,11 +168,17 @@ cudaError_t launch_mlp_tc(int width, int n_hidden, int act, bool train, const Ml
 int mlp_tc_supported(int width, int n_hidden, int act);
 int mlp_tc_ctas_per_sm(int width, int n_hidden);
 cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t* wimg, cudaStream_t s);
+// mlp_fp32w.cu (fp32, W = 128 / 256: streamed weights, per-tile dW flushes into replicas)
+int mlp_fp32w_supported(int width, int n_hidden);
+cudaError_t launch_mlp_fp32w(int width, int n_hidden, bool train, const MlpParams& p, const float* wimg, float* rep,
+                             int nrep, int grid, cudaStream_t s);
+cudaError_t launch_pack_fp32w(const ArchInfo& a, const float* theta, float* img, cudaStream_t s);
 // mlp_w256.cu (tcgen05 bf16, W = 256: streamed weights, parked activations, dW replicas)
 cudaError_t launch_mlp_w256(int n_hidden, bool train, const MlpParams& m, const uint16_t* wf, const uint16_t* wb,
                             uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s);
 cudaError_t launch_pack_w256(const ArchInfo& a, const float* theta, uint16_t* wf, uint16_t* wb, cudaStream_t s);
 cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets, int n_hidden,
+                              int quad_major,
                               const double* lpart, int G, float* grad, float* loss, int* err, cudaStream_t s);
 // reduce
 cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s);
