@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
   int curNet = -1;
   bool touched[2] = {false, false};
   bool dwFresh = true;
+  bool tailPending = false;   // the last tile's tail MMAs are in flight (read before buffer 0 is reused)
 
   auto flush = [&](int net) {
     float* out = prm.part + ((int64_t)net * G + cta) * prm.p_stride;
@@ -395,6 +396,24 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     return f;
   };
   Fetch cur = fetch(t0);
+  // completion of the tile-tail reductions: fold them into the register accumulators
+  auto tail_collect = [&]() {
+    wait_mma();
+    if (chunk == 0) {
+      float v[16];
+#pragma unroll
+      for (int l = 2; l <= NH - 1; ++l) {
+        tc::tmem_ld16(tmem + tlane + (uint32_t)(16 * (l - 2)), v);
+        tg[l - 2] += v[0];
+      }
+      tc::tmem_ld16(tmem + tlane + (uint32_t)(16 * (NH - 2)), v);
+      tg[NH - 2] += v[0];
+      tg[NH - 1] += v[1] + v[2];
+      tg[NH] += v[3] + v[4];
+      tg[NH + 1] += v[5] + v[6];
+    }
+    tailPending = false;
+  };
 
   int seg = 0;
   for (int t = t0; t < t1; ++t) {
@@ -405,6 +424,11 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     const int first = lt * per;
     const int nvalid = min(per, segCnt[seg] - first);
     if (net != curNet) {
+      if (tailPending) {
+        tail_collect();
+        tc::tc_fence_before();
+        __syncthreads();
+      }
       if (TRAIN && curNet >= 0) flush(curNet);
       load_net(net);
       dwFresh = true;
@@ -422,12 +446,14 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     __syncthreads();
     TR(0);
     const float x0 = sX[4 * row], x1 = sX[4 * row + 1], x2 = sX[4 * row + 2];
-    {  // ---- layer 1 -> bf16 h1 (buffer 0) ----
+    {  // ---- layer 1 -> bf16 h1 (buffer 0; the previous tile's tail MMAs may still read it) ----
       float h[32];
       layer1(x0, x1, x2, h);
+      if (tailPending) tail_collect();
       store_chunk_bf16(aAct, row, chunk, h);
     }
     tc::fence_proxy_async_smem();
+    tc::tc_fence_before();
     __syncthreads();
     TR(1);
     // ---- hidden layers 2..NH on the tensor cores ----
@@ -636,27 +662,17 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       gemm((uint32_t)(16 * (NH - 2)), aAct, 256, 128, LBO_ACT, aXm, 256, 128, 2048, ID_TAIL, kTB / 16, false);
       tc::mma_commit(bar);
     }
-    wait_mma();
+    tailPending = true;   // collected under the next tile's gather and layer 1
     TR(20);
-    if (chunk == 0) {
-      float v[16];
-#pragma unroll
-      for (int l = 2; l <= NH - 1; ++l) {
-        tc::tmem_ld16(tmem + tlane + (uint32_t)(16 * (l - 2)), v);
-        tg[l - 2] += v[0];
-      }
-      tc::tmem_ld16(tmem + tlane + (uint32_t)(16 * (NH - 2)), v);
-      tg[NH - 2] += v[0];
-      tg[NH - 1] += v[1] + v[2];
-      tg[NH] += v[3] + v[4];
-      tg[NH + 1] += v[5] + v[6];
-    }
-    tc::tc_fence_before();
-    __syncthreads();
     TR(21);
     dwFresh = false;
   }
   if (TRAIN) {
+    if (tailPending) {
+      tail_collect();
+      tc::tc_fence_before();
+      __syncthreads();
+    }
     if (curNet >= 0) flush(curNet);
     if (tid < 2) prm.touched[tid * G + cta] = touched[tid] ? 1 : 0;
 #pragma unroll

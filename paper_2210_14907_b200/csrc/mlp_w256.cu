@@ -526,7 +526,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     tc::cluster_sync_relaxed();
     tc::tc_fence_after();
     if (tid == 0) {   // park G_NH
-      tc::bulk_copy_s2g(myScr + gslot(NH), gb, ACT);
+      // park only the output half the peer's dW needs (this CTA's rows, outputs of CTA rank ^ 1);
+      // this CTA's own half stays in place in gb for its dW K-steps
+      tc::bulk_copy_s2g(myScr + gslot(NH) + (rank ^ 1u) * QTR, gb + (rank ^ 1u) * QTR, QTR);
       tc::bulk_commit();
     }
     TRW(10);
@@ -546,13 +548,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       if (tid == 0) {
         tc::mbar_wait(bpark, ph_park);    // the peer's parked G_l is complete
         ph_park ^= 1;
-        // the dW operands: h_{l-1}[rows of CTA t][this CTA's input half] and
-        // G_l[rows of CTA t][the outputs this CTA owns], t = 0, 1
-        tc::mbar_arrive_expect_tx(bld, 4 * QTR);
+        // the dW operands: h_{l-1}[rows of CTA t][this CTA's input half], t = 0, 1, and
+        // G_l[rows of the peer][the outputs this CTA owns] (its own rows' block is in place)
+        tc::mbar_arrive_expect_tx(bld, 3 * QTR);
         for (int t = 0; t < 2; ++t) {
           const uint8_t* scr = pairScr0 + (int64_t)t * L::kScr * ACT + rank * QTR;
           tc::bulk_copy_g2s(hb + t * QTR, scr + hslot(l - 1), QTR, bld);
-          tc::bulk_copy_g2s(gb + t * QTR, scr + gslot(l), QTR, bld);
+          if (t != (int)rank) tc::bulk_copy_g2s(gb + t * QTR, scr + gslot(l), QTR, bld);
         }
       }
       TRW(28 + 3 * (NH - l));
@@ -607,7 +609,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       // both CTAs' bulk loads of h_{l-1} and G_l (and this CTA's act' reads) are complete: the
       // parked copies are dead, so they leave L2 without a write-back to HBM
       discard_l2(myScr + hslot(l - 1) + tid * 128);
-      discard_l2(myScr + gslot(l) + tid * 128);
+      if (tid < kThreads / 2) discard_l2(myScr + gslot(l) + (rank ^ 1u) * QTR + tid * 128);
       pend = true;
       pendNet = net;
       pendL = l;
@@ -627,7 +629,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
         tc::cluster_sync_relaxed();   // both A tiles written
         tc::tc_fence_after();
         if (tid == 0) {               // park G_{l-1}
-          tc::bulk_copy_s2g(myScr + gslot(l - 1), gb, ACT);
+          tc::bulk_copy_s2g(myScr + gslot(l - 1) + (rank ^ 1u) * QTR, gb + (rank ^ 1u) * QTR, QTR);
           tc::bulk_commit();
         }
       }
