@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::oBar);
   uint64_t* wbar = reinterpret_cast<uint64_t*>(smem + L::oBar + 8);
   uint32_t* sTmem = reinterpret_cast<uint32_t*>(smem + L::oBar + 16);
+  uint64_t* dwbar = reinterpret_cast<uint64_t*>(smem + L::oBar + 24);   // dW MMA of the backward step
   __shared__ int segTiles[kNumSeg], segCnt[kNumSeg], segStart[kNumSeg];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
   if (tid == 0) {
     tc::mbar_init(bar, 1);
     tc::mbar_init(wbar, 1);
+    tc::mbar_init(dwbar, 1);
     tc::mbar_fence_init();
   }
   if (warp == 0) tc::tmem_alloc(sTmem, L::TMEM_COLS);
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
   constexpr uint32_t ID_DW = tc::idesc_bf16(L::MDW, W, 1, 1);    // A MN-major, B MN-major
   constexpr uint32_t ID_TAIL = tc::idesc_bf16(L::MDW, 16, 1, 1); // M = W, N = 16, both MN-major
   const uint32_t aOnes = sbase + L::oOnes, aXm = sbase + L::oXm;
-  uint32_t phase = 0;
+  uint32_t phase = 0, dwphase = 0;
   // streamed weights (SiLU): the stage holds W_{wl} of net wnet once wbar completes
   uint32_t wphase = 0;
   int wnet = -1, wl = -1;
@@ -606,11 +608,13 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       if (tid == 0) {
         wwait();
         tc::tc_fence_after();
-        // dW_l += G_l^T h_{l-1}: A = G (M = o, MN-major), B = h (N = i, MN-major), K = rows
-        gemm((uint32_t)(W * (l - 1)), gbuf, 256, 128, LBO_ACT, hbuf, 256, 128, LBO_ACT, ID_DW, kTB / 16, !dwFresh);
-        // acc = G_l W_l: A = G (K-major), B = W_l (N = i, K = o: MN-major)
+        // acc = G_l W_l: A = G (K-major), B = W_l (N = i, K = o: MN-major); its epilogue starts
+        // while the dW MMA below still runs
         gemm(0, gbuf, 2 * LBO_ACT, LBO_ACT, 128, wmat(l), 256, 128, LBO_W, ID_DH, W / 16, false);
         tc::mma_commit(bar);
+        // dW_l += G_l^T h_{l-1}: A = G (M = o, MN-major), B = h (N = i, MN-major), K = rows
+        gemm((uint32_t)(W * (l - 1)), gbuf, 256, 128, LBO_ACT, hbuf, 256, 128, LBO_ACT, ID_DW, kTB / 16, !dwFresh);
+        tc::mma_commit(dwbar);
       }
       wait_mma();
       if (tid == 0) wload(curNet, l > 2 ? l - 1 : 2);   // next GEMM's weights (W_2 for the next tile)
@@ -635,6 +639,8 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       }
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] *= hq[j];
+      tc::mbar_wait(dwbar, dwphase);           // dW_l has read h_{l-1} (and G_l)
+      dwphase ^= 1;
       store_chunk_bf16(hbuf, row, chunk, v);   // G_{l-1} in place: h_{l-1} is consumed
       if (l - 1 == 2 && NH >= 3) {   // h1 again for dW_2 (buffer 0's G_NH is consumed)
         float h[32];
