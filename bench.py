@@ -166,6 +166,7 @@ def main():
     ap.add_argument("--impl", default="nbm", choices=["nbm", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
     ap.add_argument("--points", type=int, default=None, help="override interior points per GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -217,29 +218,44 @@ def main():
             tdist.barrier()
         torch.cuda.synchronize()
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+    def timed(fn, first_it):
+        """K steps, CUDA events on the launching stream, L2 flushed between steps (untimed)"""
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        barrier()
+        with ClockSampler(local) as clk:
+            for k in range(args.steps):
+                flush.zero_()
+                ev[k][0].record(stream)
+                fn(first_it + k)
+                ev[k][1].record(stream)
+            barrier()
+        return sum(a.elapsed_time(b) for a, b in ev), clk.summary()
+
+    # eager pass: the library's event hook times the fused MLP kernel for the roofline
     nbm.nbm_timing_enable(s.h, True)
     nbm.nbm_timing_read(s.h)
-    launches_per_step = None
-    barrier()
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.zero_()                        # L2 flush between timed steps (not timed)
-            ev[k][0].record(stream)
-            step(args.warmup + k)
-            ev[k][1].record(stream)
-            if launches_per_step is None:
-                launches_per_step = nbm.nbm_last_launch_count(s.h) + 3   # + 2 samples + Adam
-        barrier()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    eager_ms, clk_eager = timed(step, args.warmup)
+    launches_eager = nbm.nbm_last_launch_count(s.h) + 3          # + 2 samples + Adam
     mlp_ms, lg_ms, calls = nbm.nbm_timing_read(s.h)
     nbm.nbm_timing_enable(s.h, False)
-    tot_ms = sum(step_ms)
+    done = args.warmup + args.steps
+    if args.no_graph:
+        tot_ms, clocks, launches_per_step, mode = eager_ms, clk_eager, launches_eager, "eager"
+    else:
+        # the production step: one CUDA graph of [sample x2, loss_grad, Adam] on the device step
+        # counter (two graphs around the NCCL all-reduce when N > 1), replayed per step
+        s.t_dev.fill_(done)
+        replay = s.capture_step(pts, bpts, first=rank * N, bfirst=rank * Nb, n_global=Ng, nb_global=Nbg,
+                                lr=cfg["lr"], allreduce=dp.allreduce_sum_ if world > 1 else None)
+        for _ in range(args.warmup):
+            replay()
+        tot_ms, clocks = timed(lambda it: replay(), 0)
+        launches_per_step, mode = launches_eager + 1, "cuda-graph"   # Adam: prep + update
     if world > 1:
-        t = torch.tensor([tot_ms, lg_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([tot_ms, lg_ms, eager_ms], device="cuda", dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        tot_ms, lg_ms_max = t.tolist()
+        tot_ms, lg_ms_max, eager_ms = t.tolist()
     else:
         lg_ms_max = lg_ms
 
@@ -313,9 +329,10 @@ def main():
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name(cfg) + " fused fwd/residual/bwd",
                      "flop_per_launch": flop_launch, "avg_launch_ms": mlp_avg_s * 1e3,
-                     "share_of_step": (mlp_ms / max(calls, 1)) / (tot_ms / args.steps), "peak_src": peak_note},
+                     "share_of_step": (mlp_ms / max(calls, 1)) / (eager_ms / args.steps), "peak_src": peak_note},
         "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.summary(),
+        "launch_mode": mode, "ms_per_step_eager": eager_ms / args.steps,
+        "clocks": clocks,
         "e2e": e2e,
     }
     if not args.no_cpu_baseline:

@@ -139,6 +139,11 @@ int nbm_init_params(nbm_handle* h, uint64_t seed, float* theta_dev, void* stream
  * h_cell must be a multiple of 2^-24 in (0, 1).  pts_dev: [n][3] fp32 (AoS). */
 int nbm_sample(nbm_handle* h, uint64_t seed, uint64_t step, int kind, int64_t first_index,
                int64_t n, float h_cell, float* pts_dev, void* stream);
+/* As nbm_sample, with the step word of the Philox counter read from device memory at run
+ * time (*step_dev, int64, 0-based), so a captured CUDA graph replays successive steps
+ * (SURVEY 7.3 hard part 9).  step_dev is caller-owned; the library only reads it. */
+int nbm_sample_at(nbm_handle* h, uint64_t seed, const int64_t* step_dev, int kind,
+                  int64_t first_index, int64_t n, float h_cell, float* pts_dev, void* stream);
 
 /* Loss and gradient (G1-G3, G18).
  * For each interior point p (pts_dev [n][3]): place the implicit cell of width h_cell,
@@ -176,6 +181,13 @@ int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_
 int nbm_adam_step(nbm_handle* h, float* theta_dev, float* m_dev, float* v_dev,
                   const float* grad_dev, int64_t t, float lr, float b1, float b2, float eps,
                   void* stream);
+/* As nbm_adam_step with a device step counter (CUDA-graph replay): t = *t_dev + 1 is used
+ * for the bias corrections (the same fp64 formula, one fp32 rounding), then *t_dev = t.
+ * *t_dev is the number of completed steps, so nbm_sample_at(step_dev = t_dev) earlier in
+ * the same step draws step t - 1, as the host-counter calls do.  Two kernel launches. */
+int nbm_adam_step_at(nbm_handle* h, float* theta_dev, float* m_dev, float* v_dev,
+                     const float* grad_dev, int64_t* t_dev, float lr, float b1, float b2,
+                     float eps, void* stream);
 
 /* ---- measurement hook (bench.py) ----
  * When enabled, nbm_loss_grad records CUDA events around its fused MLP kernel launches

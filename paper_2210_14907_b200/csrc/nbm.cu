@@ -129,10 +129,12 @@ int check_problem(const nbm_problem* p, DevProblem* out, std::string* why) {
   return NBM_OK;
 }
 
-// K4r: grad[net][j] = sum over CTAs of the touched partials, in fixed order: 8 CTA groups
-// (g = 8 m + k) summed per thread, then the 8 group sums in order; loss = the CTA loss
-// partials plus the crossed rows' loss.  fp64 accumulation of the fp32 partials.
-constexpr int kRedCols = 32, kRedGroups = 8;
+// K4r: grad[net][j] = sum over CTAs of the touched partials, in fixed order: 16 CTA groups
+// (g = 16 m + k) summed per thread, then the 16 group sums in order; loss = the CTA loss
+// partials plus the crossed rows' loss.  fp64 accumulation of the fp32 partials.  The
+// partial loads of a thread are issued together (independent, up to kRedBatch in flight)
+// before the fixed-order accumulation: the kernel is latency-bound otherwise.
+constexpr int kRedCols = 32, kRedGroups = 16, kRedBatch = 8;
 __global__ void __launch_bounds__(kRedCols * kRedGroups) k_reduce(
     const float* __restrict__ part, const int* __restrict__ touched, int G, int64_t p_net, int64_t p_stride,
     int n_nets, const double* __restrict__ lpart, float* __restrict__ grad, float* __restrict__ loss,
@@ -145,8 +147,18 @@ __global__ void __launch_bounds__(kRedCols * kRedGroups) k_reduce(
   if (i < P) {
     const int net = (int)(i / p_net);
     const int64_t j = i - net * p_net;
-    for (int g = grp; g < G; g += kRedGroups)
-      if (touched[net * G + g]) s += part[((int64_t)net * G + g) * p_stride + j];
+    const float* base = part + (int64_t)net * G * p_stride + j;
+    const int* tch = touched + net * G;
+    for (int g0 = grp; g0 < G; g0 += kRedGroups * kRedBatch) {
+      float v[kRedBatch];
+#pragma unroll
+      for (int b = 0; b < kRedBatch; ++b) {
+        const int g = g0 + b * kRedGroups;
+        v[b] = (g < G && tch[g]) ? base[(int64_t)g * p_stride] : 0.0f;
+      }
+#pragma unroll
+      for (int b = 0; b < kRedBatch; ++b) s += (double)v[b];
+    }
   }
   acc[grp][col] = s;
   __syncthreads();
@@ -296,6 +308,7 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   ALLOC(w.touched, 2 * (size_t)w.grid_mlp * sizeof(int));
   ALLOC(w.lpart, ((size_t)w.grid_mlp + 1) * sizeof(double));
   ALLOC(w.err, sizeof(int));
+  ALLOC(w.bc, 2 * sizeof(float));
   const size_t nhh = ai.n_hidden > 1 ? ai.n_hidden - 1 : 1;
   ALLOC(w.wimg, (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t));
   const bool w256 = is_w256(ai), fw = is_fp32w(ai), urep = uses_rep(ai);
@@ -334,7 +347,7 @@ void nbm_destroy(nbm_handle* h) {
   void* ps[] = {h->d_problem, h->ws.cls, h->ws.aux_tmp, h->ws.blk_counts, h->ws.blk_offsets,
                 h->ws.counts, h->ws.list, h->ws.list_aux, h->ws.xrow_x, h->ws.xrow_u, h->ws.xrow_cot,
                 h->ws.xrow_tag, h->ws.xrec, h->ws.xlist, h->ws.part, h->ws.touched, h->ws.lpart,
-                h->ws.err, h->ws.wimg, h->ws.wimg_b, h->ws.hscr, h->ws.rep, h->ws.wimg32};
+                h->ws.err, h->ws.bc, h->ws.wimg, h->ws.wimg_b, h->ws.hscr, h->ws.rep, h->ws.wimg32};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : h->ev) cudaEventDestroy(ev);
@@ -376,8 +389,19 @@ int nbm_sample(nbm_handle* h, uint64_t seed, uint64_t step, int kind, int64_t fi
   int64_t H;
   if (!h_on_lattice(h_cell, &H)) return fail(h, NBM_E_INVALID_PROBLEM, "nbm_sample: h must be a multiple of 2^-24 in (0,1) (G9)");
   cudaSetDevice(h->device);
-  cudaError_t e = launch_sample(kind, seed, step, first_index, n, H, pts_dev, (cudaStream_t)stream);
+  cudaError_t e = launch_sample(kind, seed, step, nullptr, first_index, n, H, pts_dev, (cudaStream_t)stream);
   return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_sample");
+}
+
+int nbm_sample_at(nbm_handle* h, uint64_t seed, const int64_t* step_dev, int kind, int64_t first_index, int64_t n,
+                  float h_cell, float* pts_dev, void* stream) {
+  if (!h || !step_dev || (n > 0 && !pts_dev) || n < 0 || first_index < 0) return fail(h, NBM_E_ARG, "nbm_sample_at: bad arguments");
+  if (kind != NBM_POINTS_INTERIOR && kind != NBM_POINTS_BOUNDARY) return fail(h, NBM_E_ARG, "nbm_sample_at: bad kind");
+  int64_t H;
+  if (!h_on_lattice(h_cell, &H)) return fail(h, NBM_E_INVALID_PROBLEM, "nbm_sample_at: h must be a multiple of 2^-24 in (0,1) (G9)");
+  cudaSetDevice(h->device);
+  cudaError_t e = launch_sample(kind, seed, 0, step_dev, first_index, n, H, pts_dev, (cudaStream_t)stream);
+  return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_sample_at");
 }
 
 int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_t n,
@@ -540,6 +564,15 @@ int nbm_adam_step(nbm_handle* h, float* theta_dev, float* m_dev, float* v_dev, c
   cudaError_t e = launch_adam(h->arch.p_net * h->arch.n_nets, theta_dev, m_dev, v_dev, grad_dev, lr,
                               b1, b2, eps, bc1, bc2, (cudaStream_t)stream);
   return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_adam_step");
+}
+
+int nbm_adam_step_at(nbm_handle* h, float* theta_dev, float* m_dev, float* v_dev, const float* grad_dev,
+                     int64_t* t_dev, float lr, float b1, float b2, float eps, void* stream) {
+  if (!h || !theta_dev || !m_dev || !v_dev || !grad_dev || !t_dev) return fail(h, NBM_E_ARG, "nbm_adam_step_at: bad arguments");
+  cudaSetDevice(h->device);
+  cudaError_t e = launch_adam_dev(h->arch.p_net * h->arch.n_nets, theta_dev, m_dev, v_dev, grad_dev, lr, b1, b2, eps,
+                                  t_dev, h->ws.bc, (cudaStream_t)stream);
+  return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_adam_step_at");
 }
 
 int nbm_timing_enable(nbm_handle* h, int enable) {

@@ -92,6 +92,7 @@ struct Workspace {
   int* touched;         // [2][grid_mlp]
   double* lpart;        // [grid_mlp + 1]  (+1: crossed rows' loss)
   int* err;             // sticky error word
+  float* bc;            // [2] Adam bias corrections of the device step counter
   uint16_t* wimg;       // [2][NH-1][W*W] bf16 weight image (tensor-core path)
   uint16_t* wimg_b;     // W = 256: backward-sliced image
   float* wimg32;        // fp32 W >= 128: [2][NH-1][2][W*W] transposed / natural hidden weights
@@ -128,11 +129,13 @@ namespace nbm {
 
 // ---- launchers implemented in the .cu files ----
 // sample_init.cu
-cudaError_t launch_sample(int kind, uint64_t seed, uint64_t step, int64_t first, int64_t n,
-                          int64_t H, float* pts, cudaStream_t s);
+cudaError_t launch_sample(int kind, uint64_t seed, uint64_t step, const int64_t* step_dev, int64_t first,
+                          int64_t n, int64_t H, float* pts, cudaStream_t s);
 cudaError_t launch_init_params(const ArchInfo& a, uint64_t seed, float* theta, cudaStream_t s);
 cudaError_t launch_adam(int64_t P, float* theta, float* m, float* v, const float* g, float lr,
                         float b1, float b2, float eps, float bc1, float bc2, cudaStream_t s);
+cudaError_t launch_adam_dev(int64_t P, float* theta, float* m, float* v, const float* g, float lr, float b1,
+                            float b2, float eps, int64_t* t_dev, float* bc, cudaStream_t s);
 // geometry.cu (compiled without FMA contraction)
 cudaError_t launch_classify(const nbm_handle* h, const float* pts, int64_t n, const float* bpts,
                             int64_t nb, int64_t H, double inv_d_minus, double inv_d_plus,

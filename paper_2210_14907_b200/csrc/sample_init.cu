@@ -28,10 +28,11 @@ __device__ __forceinline__ uint4 philox_ctr(uint64_t seed, uint64_t counter, uin
                   (uint32_t)seed, (uint32_t)(seed >> 32));
 }
 
-__global__ void __launch_bounds__(256) k_sample(int kind, uint64_t seed, uint32_t step,
-                                                int64_t first, int64_t n, int64_t H,
-                                                float* __restrict__ pts) {
+__global__ void __launch_bounds__(256) k_sample(int kind, uint64_t seed, uint32_t step_arg,
+                                                const int64_t* __restrict__ step_dev, int64_t first,
+                                                int64_t n, int64_t H, float* __restrict__ pts) {
   __shared__ float stage[256 * 3];
+  const uint32_t step = step_dev ? (uint32_t)*step_dev : step_arg;   // device counter: graph replay
   int64_t base = (int64_t)blockIdx.x * 256;
   int64_t i = base + threadIdx.x;
   float x[3] = {0.f, 0.f, 0.f};
@@ -75,11 +76,11 @@ __global__ void __launch_bounds__(256) k_sample(int kind, uint64_t seed, uint32_
     if (t < lim) pts[base * 3 + t] = stage[t];
 }
 
-cudaError_t launch_sample(int kind, uint64_t seed, uint64_t step, int64_t first, int64_t n,
-                          int64_t H, float* pts, cudaStream_t s) {
+cudaError_t launch_sample(int kind, uint64_t seed, uint64_t step, const int64_t* step_dev, int64_t first,
+                          int64_t n, int64_t H, float* pts, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
-  k_sample<<<(unsigned)blocks, 256, 0, s>>>(kind, seed, (uint32_t)step, first, n, H, pts);
+  k_sample<<<(unsigned)blocks, 256, 0, s>>>(kind, seed, (uint32_t)step, step_dev, first, n, H, pts);
   return cudaGetLastError();
 }
 
@@ -128,9 +129,13 @@ cudaError_t launch_init_params(const ArchInfo& a, uint64_t seed, float* theta, c
 // ---- K4a Adam (G19).  Each op is one IEEE fp32 rounding in the written order. ----
 __global__ void k_adam(int64_t P, float* __restrict__ th, float* __restrict__ m,
                        float* __restrict__ v, const float* __restrict__ g, float lr, float b1,
-                       float b2, float eps, float bc1, float bc2) {
+                       float b2, float eps, float bc1, float bc2, const float* __restrict__ bc_dev) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= P) return;
+  if (bc_dev) {   // bias corrections of the device step counter (k_adam_prep)
+    bc1 = bc_dev[0];
+    bc2 = bc_dev[1];
+  }
   float ob1 = __fsub_rn(1.0f, b1), ob2 = __fsub_rn(1.0f, b2);
   float gi = g[i];
   float mi = __fadd_rn(__fmul_rn(b1, m[i]), __fmul_rn(ob1, gi));
@@ -145,7 +150,24 @@ __global__ void k_adam(int64_t P, float* __restrict__ th, float* __restrict__ m,
 cudaError_t launch_adam(int64_t P, float* theta, float* m, float* v, const float* g, float lr,
                         float b1, float b2, float eps, float bc1, float bc2, cudaStream_t s) {
   if (P <= 0) return cudaSuccess;
-  k_adam<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(P, theta, m, v, g, lr, b1, b2, eps, bc1, bc2);
+  k_adam<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(P, theta, m, v, g, lr, b1, b2, eps, bc1, bc2, nullptr);
+  return cudaGetLastError();
+}
+
+// Device-counter variant (CUDA-graph replay): t = *t_dev + 1 (1-based step), the same fp32 bias
+// corrections as the host path (1 - b^t in fp64, rounded once), then *t_dev = t.
+__global__ void k_adam_prep(int64_t* __restrict__ t_dev, float b1, float b2, float* __restrict__ bc) {
+  const int64_t t = *t_dev + 1;
+  bc[0] = (float)(1.0 - pow((double)b1, (double)t));
+  bc[1] = (float)(1.0 - pow((double)b2, (double)t));
+  *t_dev = t;
+}
+
+cudaError_t launch_adam_dev(int64_t P, float* theta, float* m, float* v, const float* g, float lr, float b1,
+                            float b2, float eps, int64_t* t_dev, float* bc, cudaStream_t s) {
+  k_adam_prep<<<1, 1, 0, s>>>(t_dev, b1, b2, bc);
+  if (P <= 0) return cudaGetLastError();
+  k_adam<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(P, theta, m, v, g, lr, b1, b2, eps, 1.0f, 1.0f, bc);
   return cudaGetLastError();
 }
 

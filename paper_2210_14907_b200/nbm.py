@@ -82,6 +82,8 @@ def lib():
         L.nbm_eval.argtypes = [v, v, v, i64, v, v]
         L.nbm_classify.argtypes = [v, v, i64, f, v, v, v]
         L.nbm_adam_step.argtypes = [v, v, v, v, v, i64, f, f, f, f, v]
+        L.nbm_sample_at.argtypes = [v, u64, v, C.c_int, i64, i64, f, v, v]
+        L.nbm_adam_step_at.argtypes = [v, v, v, v, v, v, f, f, f, f, v]
         L.nbm_timing_enable.argtypes = [v, C.c_int]
         L.nbm_timing_read.argtypes = [v, P(C.c_double), P(C.c_double), P(i64)]
         L.nbm_last_launch_count.argtypes = [v]
@@ -208,6 +210,18 @@ def nbm_adam_step(h, theta, m, v, grad, t: int, lr: float, b1: float, b2: float,
                                   _stream(stream)))
 
 
+def nbm_sample_at(h, seed: int, step_dev, kind: int, first_index: int, n: int, h_cell: float, pts,
+                  stream=None) -> None:
+    _check(h, lib().nbm_sample_at(h, seed, _ptr(step_dev), kind, first_index, n, h_cell, _ptr(pts),
+                                  _stream(stream)))
+
+
+def nbm_adam_step_at(h, theta, m, v, grad, t_dev, lr: float, b1: float, b2: float, eps: float,
+                     stream=None) -> None:
+    _check(h, lib().nbm_adam_step_at(h, _ptr(theta), _ptr(m), _ptr(v), _ptr(grad), _ptr(t_dev), lr, b1, b2,
+                                     eps, _stream(stream)))
+
+
 def nbm_timing_enable(h, enable: bool) -> None:
     _check(h, lib().nbm_timing_enable(h, int(enable)))
 
@@ -242,6 +256,8 @@ class Solver:
         self.m = torch.zeros_like(self.theta)
         self.v = torch.zeros_like(self.theta)
         self.t = 0
+        # device step counter for graph-captured steps (nbm_sample_at / nbm_adam_step_at)
+        self.t_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
 
     def close(self):
         if self.h is not None:
@@ -275,6 +291,61 @@ class Solver:
     def adam_step(self, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
         self.t += 1
         nbm_adam_step(self.h, self.theta, self.m, self.v, self.grad, self.t, lr, b1, b2, eps)
+
+    def sample_at(self, kind, seed, first, n, out):
+        """sample with the step word read from self.t_dev (graph-capturable)"""
+        nbm_sample_at(self.h, seed, self.t_dev, kind, first, n, self.h_cell, out)
+
+    def adam_step_at(self, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
+        """Adam with t = t_dev + 1 read and t_dev incremented on the device (graph-capturable)"""
+        nbm_adam_step_at(self.h, self.theta, self.m, self.v, self.grad, self.t_dev, lr, b1, b2, eps)
+
+    def capture_step(self, pts, bpts, first=0, bfirst=0, n_global=None, nb_global=None, lr=1e-3, seed=0,
+                     allreduce=None):
+        """Capture one training step [sample interior, sample boundary, loss_grad,
+        (allreduce), Adam] as CUDA graphs on the device counter self.t_dev.  Returns a
+        callable that replays one step.  With `allreduce` (a callable on the [grad, loss]
+        buffer) the step is captured as two graphs around an eagerly launched collective."""
+        import torch
+        n, nb = pts.shape[0], bpts.shape[0]
+
+        def pre():
+            self.sample_at(POINTS_INTERIOR, seed, first, n, pts)
+            self.sample_at(POINTS_BOUNDARY, seed, bfirst, nb, bpts)
+            self.loss_grad(pts, bpts, n_global=n_global, nb_global=nb_global)
+
+        def post():
+            self.adam_step_at(lr=lr)
+
+        t0 = self.t_dev.clone()
+        saved = [x.clone() for x in (self.theta, self.m, self.v)]
+        side = torch.cuda.Stream(self.device)   # warm up the calls outside capture (lazy init)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            pre()
+            post()
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        self.t_dev.copy_(t0)                    # the warm-up step leaves no trace
+        for x, y in zip((self.theta, self.m, self.v), saved):
+            x.copy_(y)
+        if allreduce is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                pre()
+                post()
+            return g.replay
+        g1, g2 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1):
+            pre()
+        with torch.cuda.graph(g2):
+            post()
+
+        def replay():
+            g1.replay()
+            allreduce(self.gbuf)
+            g2.replay()
+        return replay
 
     def eval(self, pts, out=None):
         import torch

@@ -348,3 +348,34 @@ def test_eval_parity_fp32_wide(orc, w):
     want = orc.evaluate(pb, ar, th, pts)
     assert np.allclose(u, want, rtol=1e-5, atol=1e-6 * np.abs(want).max())
     s.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_graph_replay_matches_eager_steps(orc, name):
+    """A training step captured as a CUDA graph on the device step counter
+    (nbm_sample_at / nbm_adam_step_at) replays bit-identically to the host-counter calls
+    (sample step k, loss_grad, Adam t = k + 1) for 4 consecutive steps."""
+    import torch
+    cfg = _cfg(name)
+    N, Nb = cfg["N"], cfg["Nb"]
+    a = nbm.Solver(cfg, 0)
+    b = nbm.Solver(cfg, 0)
+    a.init_params(0)
+    b.init_params(0)
+    pa, ba = torch.empty(N, 3, device="cuda"), torch.empty(Nb, 3, device="cuda")
+    pb_, bb = torch.empty(N, 3, device="cuda"), torch.empty(Nb, 3, device="cuda")
+    step = b.capture_step(pb_, bb, lr=cfg["lr"])
+    for k in range(4):
+        a.sample(nbm.POINTS_INTERIOR, 0, k, 0, N, pa)
+        a.sample(nbm.POINTS_BOUNDARY, 0, k, 0, Nb, ba)
+        a.loss_grad(pa, ba)
+        a.adam_step(lr=cfg["lr"])
+        step()
+        torch.cuda.synchronize()
+        assert torch.equal(pa, pb_) and torch.equal(ba, bb)
+        assert torch.equal(a.gbuf, b.gbuf)
+        assert torch.equal(a.theta, b.theta) and torch.equal(a.m, b.m) and torch.equal(a.v, b.v)
+    assert int(b.t_dev.item()) == 4
+    assert a.status() == 0 and b.status() == 0
+    a.close()
+    b.close()
