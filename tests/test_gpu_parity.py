@@ -350,11 +350,12 @@ def test_eval_parity_fp32_wide(orc, w):
     s.close()
 
 
-@pytest.mark.parametrize("name", ["c1", "c2"])
-def test_graph_replay_matches_eager_steps(orc, name):
+@pytest.mark.parametrize("name,split", [("c1", False), ("c2", False), ("c2", True)])
+def test_graph_replay_matches_eager_steps(orc, name, split):
     """A training step captured as a CUDA graph on the device step counter
     (nbm_sample_at / nbm_adam_step_at) replays bit-identically to the host-counter calls
-    (sample step k, loss_grad, Adam t = k + 1) for 4 consecutive steps."""
+    (sample step k, loss_grad, Adam t = k + 1) for 4 consecutive steps, in one graph and in
+    the two-graph form used around the NCCL all-reduce."""
     import torch
     cfg = _cfg(name)
     N, Nb = cfg["N"], cfg["Nb"]
@@ -364,7 +365,8 @@ def test_graph_replay_matches_eager_steps(orc, name):
     b.init_params(0)
     pa, ba = torch.empty(N, 3, device="cuda"), torch.empty(Nb, 3, device="cuda")
     pb_, bb = torch.empty(N, 3, device="cuda"), torch.empty(Nb, 3, device="cuda")
-    step = b.capture_step(pb_, bb, lr=cfg["lr"])
+    # split: the N > 1 form, two graphs around an eagerly launched collective (here an identity)
+    step = b.capture_step(pb_, bb, lr=cfg["lr"], allreduce=(lambda buf: buf.mul_(1.0)) if split else None)
     for k in range(4):
         a.sample(nbm.POINTS_INTERIOR, 0, k, 0, N, pa)
         a.sample(nbm.POINTS_BOUNDARY, 0, k, 0, Nb, ba)
