@@ -98,7 +98,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(cfg, seconds_hint=15.0):
+def cpu_baseline(cfg, seconds_hint=15.0, levels=1):
     """The oracle as it stands (fp64, OpenMP over all host cores) on a bounded sample of
     the same workload; returns pts/s (loss+grad evaluations per second)."""
     import oracle
@@ -110,7 +110,10 @@ def cpu_baseline(cfg, seconds_hint=15.0):
         pts = oracle.sample(0, 0, 0, 0, n, cfg["H"])
         bpts = oracle.sample(1, 0, 0, 0, nb, cfg["H"])
         t0 = time.perf_counter()
-        oracle.loss_grad(pb, ar, th, pts, bpts, cfg["h"], n_glob=cfg["N"], nb_glob=cfg["Nb"])
+        if levels == 1:
+            oracle.loss_grad(pb, ar, th, pts, bpts, cfg["h"], n_glob=cfg["N"], nb_glob=cfg["Nb"])
+        else:
+            oracle.loss_grad_ml(pb, ar, th, pts, bpts, cfg["h"], levels, n_glob=cfg["N"], nb_glob=cfg["Nb"])
         dt = time.perf_counter() - t0
         if dt > seconds_hint / 4 or n >= cfg["N"]:
             break
@@ -167,6 +170,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
+    ap.add_argument("--levels", type=int, default=1,
+                    help="multi-resolution levels h0/2^l of the loss (S:348; the paper's scaling runs use 3)")
     ap.add_argument("--points", type=int, default=None, help="override interior points per GPU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -202,7 +207,7 @@ def main():
     def step(it):
         s.sample(nbm.POINTS_INTERIOR, 0, it, rank * N, N, pts)
         s.sample(nbm.POINTS_BOUNDARY, 0, it, rank * Nb, Nb, bpts)
-        s.loss_grad(pts, bpts, n_global=Ng, nb_global=Nbg)
+        s.loss_grad(pts, bpts, n_global=Ng, nb_global=Nbg, levels=args.levels)
         dp.allreduce_sum_(s.gbuf)
         s.adam_step(lr=cfg["lr"])
 
@@ -247,7 +252,7 @@ def main():
         # counter (two graphs around the NCCL all-reduce when N > 1), replayed per step
         s.t_dev.fill_(done)
         replay = s.capture_step(pts, bpts, first=rank * N, bfirst=rank * Nb, n_global=Ng, nb_global=Nbg,
-                                lr=cfg["lr"], allreduce=dp.allreduce_sum_ if world > 1 else None)
+                                lr=cfg["lr"], allreduce=dp.allreduce_sum_ if world > 1 else None, levels=args.levels)
         for _ in range(args.warmup):
             replay()
         tot_ms, clocks = timed(lambda it: replay(), 0)
@@ -278,7 +283,7 @@ def main():
             ee[k][0].record(stream)
             pts.copy_(hp, non_blocking=True)
             bpts.copy_(hb, non_blocking=True)
-            s.loss_grad(pts, bpts, n_global=Ng, nb_global=Nbg)
+            s.loss_grad(pts, bpts, n_global=Ng, nb_global=Nbg, levels=args.levels)
             dp.allreduce_sum_(s.gbuf)
             s.adam_step(lr=cfg["lr"])
             hl.copy_(s.loss, non_blocking=True)
@@ -302,7 +307,9 @@ def main():
 
     peaks, src = load_peaks()
     fwd, fb = mlp_macs(cfg["sizes"])
-    flop_launch = 2.0 * fb * (7 * N + Nb)          # algorithmic, per fused-MLP launch
+    # algorithmic FLOP of the fused-MLP launches of one step (levels x 7N stencil evaluations +
+    # the N_b boundary evaluations of level 0), averaged per launch
+    flop_launch = 2.0 * fb * (args.levels * 7 * N + Nb) / args.levels
     mlp_avg_s = mlp_ms / max(calls, 1) / 1e3
     if cfg["prec"] == inputs.PREC_FP32:
         peak = FP32_FFMA_TFLOPS
@@ -320,23 +327,23 @@ def main():
         "metric": "collocation-pt loss+grad evals/sec (full training step)",
         "value": val, "unit": "pts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_ms / args.steps, "steps_per_sec": 1e3 * args.steps / tot_ms,
-        "loss_grad_pts_per_sec": Ng * calls / (lg_ms_max / 1e3) if calls else None,
+        "loss_grad_pts_per_sec": Ng * calls / args.levels / (lg_ms_max / 1e3) if calls else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg["prec"] == 0 else "bf16",
         "data": "synthetic (seeded Philox lattice points; manufactured two-phase Poisson)",
         "config": {"workload": cfg["label"], "points_per_gpu": N, "boundary_per_gpu": Nb,
                    "global_points": Ng, "mlp": "x".join(map(str, cfg["sizes"])), "n_nets": cfg["n_nets"],
-                   "h": cfg["h"], "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
+                   "h": cfg["h"], "levels": args.levels, "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name(cfg) + " fused fwd/residual/bwd",
                      "flop_per_launch": flop_launch, "avg_launch_ms": mlp_avg_s * 1e3,
-                     "share_of_step": (mlp_ms / max(calls, 1)) / (eager_ms / args.steps), "peak_src": peak_note},
+                     "share_of_step": mlp_ms / eager_ms, "peak_src": peak_note},
         "gpu_launches": launches_per_step * args.steps,
         "launch_mode": mode, "ms_per_step_eager": eager_ms / args.steps,
         "clocks": clocks,
         "e2e": e2e,
     }
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg)
+        line["cpu_baseline"] = cpu_baseline(cfg, levels=args.levels)
     print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()

@@ -163,6 +163,19 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
                   int64_t nb_global, unsigned terms, float* loss_dev, float* grad_dev,
                   void* stream);
 
+/* Multi-resolution loss ("placing implicit cells at multi-resolutions", "three
+ * levels of implicit refinement").  The same centres
+ * are evaluated at n_levels cell widths h_l = h0 / 2^l, l = 0..n_levels-1:
+ *   loss = (1/n_global) sum_p sum_l w_l r_p(h_l)^2 + (lambda_b/nb_global) sum_b r_b^2
+ * with level_weights (host, [n_levels]; NULL = all 1) and the boundary term counted
+ * once.  h0 / 2^(n_levels-1) must stay on the 2^-24 lattice (else NBM_E_INVALID_PROBLEM);
+ * 1 <= n_levels <= 8.  nbm_loss_grad is this call with n_levels = 1.  Deterministic like
+ * nbm_loss_grad (the levels are added in level order). */
+int nbm_loss_grad_ml(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_t n,
+                     const float* bpts_dev, int64_t nb, float h0, int n_levels,
+                     const float* level_weights, int64_t n_global, int64_t nb_global,
+                     unsigned terms, float* loss_dev, float* grad_dev, void* stream);
+
 /* Stencil classification alone ("calculating interface-cell crossings"):
  * for each interior point, mask_dev[i] bit 0 = side(p), bit j (1..6) = side(p + arm_j)
  * with arms +x,-x,+y,-y,+z,-z and side = (phi > 0) (tie -> Omega-); cls_dev[i] =

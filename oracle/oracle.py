@@ -333,6 +333,26 @@ def loss_grad(pb, arch, theta, pts, bpts, h, n_glob=None, nb_glob=None, mode=MOD
     return float(lt.sum()), lt, gr, gt
 
 
+def loss_grad_ml(pb, arch, theta, pts, bpts, h0, n_levels, level_weights=None, n_glob=None, nb_glob=None,
+                 mode=MODE_F64):
+    """Multi-resolution loss ("implicit cells at multi-resolutions",
+    P:98 "three levels of implicit refinement"): the same centres at h_l = h0 / 2^l,
+    L = (1/N) sum_p sum_l w_l r_p(h_l)^2 + (lambda_b/N_b) sum_b r_b^2, w_l = 1 by default,
+    boundary term once.  Written as the definition: one single-level loss per level over the
+    interior points (no boundary) plus the boundary-only loss, weighted and summed."""
+    pts = _f32(pts).reshape(-1, 3)
+    bpts = _f32(bpts).reshape(-1, 3)
+    ng = len(pts) if n_glob is None else n_glob
+    nbg = len(bpts) if nb_glob is None else nb_glob
+    none = np.zeros((0, 3), np.float32)
+    L, _, g, _ = loss_grad(pb, arch, theta, none, bpts, h0, n_glob=ng, nb_glob=nbg, mode=mode)
+    for lev in range(n_levels):
+        w = 1.0 if level_weights is None else float(level_weights[lev])
+        Ll, _, gl, _ = loss_grad(pb, arch, theta, pts, none, h0 / 2 ** lev, n_glob=ng, nb_glob=nbg, mode=mode)
+        L, g = L + w * Ll, g + w * gl
+    return L, g
+
+
 def residuals(pb, arch, theta, pts, bpts, h, mode=MODE_F64):
     th = _theta(theta)
     pts = _f32(pts).reshape(-1, 3)

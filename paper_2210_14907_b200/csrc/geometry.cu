@@ -580,10 +580,10 @@ __global__ void __launch_bounds__(1024) k_crossed_residual(const int* __restrict
   }
 }
 
-cudaError_t launch_crossed_residual(const nbm_handle* h, int64_t n_global, cudaStream_t s) {
-  const Workspace& w = h->ws;
+cudaError_t launch_crossed_residual(const nbm_handle* h, int64_t n_global, double weight, cudaStream_t s) {
+  const Workspace& w = h->ws;   // weight: the resolution level's w_l, 1 for one level
   k_crossed_residual<<<1, 1024, 0, s>>>(w.counts, w.xrec, w.xrow_u, w.xrow_cot,
-                                        (float)(2.0 / (double)n_global), 1.0 / (double)n_global,
+                                        (float)(2.0 * weight / (double)n_global), weight / (double)n_global,
                                         w.lpart + w.grid_mlp);
   return cudaGetLastError();
 }

@@ -728,7 +728,7 @@ cudaError_t launch_pack_w256(const ArchInfo& a, const float* theta, uint16_t* wf
 // replica order, loss from lpart.  quad_major (bf16 W = 256): the hidden-weight blocks W_l[o][i]
 // sit input-quad-major in the replicas, [i/4][o][i%4]; otherwise in the natural layout.
 __global__ void k_reduce_rep(const float* __restrict__ rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets,
-                             int n_hidden, int quad_major, const double* __restrict__ lpart, int G, float* __restrict__ grad,
+                             int n_hidden, int quad_major, int accumulate, const double* __restrict__ lpart, int G, float* __restrict__ grad,
                              float* __restrict__ loss, int* __restrict__ err) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n_nets * p_net) {
@@ -742,14 +742,14 @@ __global__ void k_reduce_rep(const float* __restrict__ rep, int nrep, int64_t p_
         jr = j - lo + ((int64_t)(in / 4) * W + o) * 4 + (in % 4);
       }
     }
-    double s = 0.0;
+    double s = accumulate ? (double)grad[i] : 0.0;   // multi-resolution levels add up
     for (int r = 0; r < nrep; ++r) s += rep[((int64_t)r * 2 + net) * p_stride + jr];
     const float v = (float)s;
     grad[i] = v;
     if (!isfinite(v)) atomicOr(err, kErrNonfinite);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double s = 0.0;
+    double s = accumulate ? (double)*loss : 0.0;
     for (int g = 0; g <= G; ++g) s += lpart[g];
     *loss = (float)s;
     if (!isfinite(*loss)) atomicOr(err, kErrNonfinite);
@@ -757,10 +757,10 @@ __global__ void k_reduce_rep(const float* __restrict__ rep, int nrep, int64_t p_
 }
 
 cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets, int n_hidden,
-                              int quad_major, const double* lpart, int G, float* grad, float* loss, int* err,
-                              cudaStream_t s) {
+                              int quad_major, int accumulate, const double* lpart, int G, float* grad, float* loss,
+                              int* err, cudaStream_t s) {
   const int64_t P = n_nets * p_net;
-  k_reduce_rep<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(rep, nrep, p_net, p_stride, n_nets, n_hidden, quad_major, lpart, G,
+  k_reduce_rep<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(rep, nrep, p_net, p_stride, n_nets, n_hidden, quad_major, accumulate, lpart, G,
                                                            grad, loss, err);
   return cudaGetLastError();
 }

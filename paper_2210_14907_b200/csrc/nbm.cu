@@ -137,8 +137,8 @@ int check_problem(const nbm_problem* p, DevProblem* out, std::string* why) {
 constexpr int kRedCols = 32, kRedGroups = 16, kRedBatch = 8;
 __global__ void __launch_bounds__(kRedCols * kRedGroups) k_reduce(
     const float* __restrict__ part, const int* __restrict__ touched, int G, int64_t p_net, int64_t p_stride,
-    int n_nets, const double* __restrict__ lpart, float* __restrict__ grad, float* __restrict__ loss,
-    int* __restrict__ err) {
+    int n_nets, int accumulate, const double* __restrict__ lpart, float* __restrict__ grad,
+    float* __restrict__ loss, int* __restrict__ err) {
   __shared__ double acc[kRedGroups][kRedCols];
   const int col = threadIdx.x % kRedCols, grp = threadIdx.x / kRedCols;
   const int64_t i = (int64_t)blockIdx.x * kRedCols + col;
@@ -163,14 +163,14 @@ __global__ void __launch_bounds__(kRedCols * kRedGroups) k_reduce(
   acc[grp][col] = s;
   __syncthreads();
   if (grp == 0 && i < P) {
-    double t = 0.0;
+    double t = accumulate ? (double)grad[i] : 0.0;   // multi-resolution levels add up
     for (int k = 0; k < kRedGroups; ++k) t += acc[k][col];
     const float v = (float)t;
     grad[i] = v;
     if (!isfinite(v)) atomicOr(err, kErrNonfinite);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    double t = 0.0;
+    double t = accumulate ? (double)*loss : 0.0;
     for (int g = 0; g <= G; ++g) t += lpart[g];
     const float v = (float)t;
     *loss = v;
@@ -226,11 +226,11 @@ cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cu
 }  // namespace
 
 namespace nbm {
-cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s) {
+cudaError_t launch_reduce(const nbm_handle* h, bool accumulate, float* grad, float* loss, cudaStream_t s) {
   int64_t P = h->arch.p_net * h->arch.n_nets;
   k_reduce<<<(unsigned)((P + kRedCols - 1) / kRedCols), kRedCols * kRedGroups, 0, s>>>(h->ws.part, h->ws.touched, h->ws.grid_mlp,
                                                        h->arch.p_net, (h->arch.p_net + 3) & ~3ll,
-                                                       h->arch.n_nets, h->ws.lpart,
+                                                       h->arch.n_nets, accumulate ? 1 : 0, h->ws.lpart,
                                                        grad, loss, h->ws.err);
   return cudaGetLastError();
 }
@@ -404,18 +404,15 @@ int nbm_sample_at(nbm_handle* h, uint64_t seed, const int64_t* step_dev, int kin
   return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_sample_at");
 }
 
-int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_t n,
-                  const float* bpts_dev, int64_t nb, float h_cell, int64_t n_global,
-                  int64_t nb_global, unsigned terms, float* loss_dev, float* grad_dev, void* stream) {
-  if (!h || !theta_dev || !loss_dev || !grad_dev || n < 0 || nb < 0 || (n > 0 && !pts_dev) ||
-      (nb > 0 && !bpts_dev))
-    return fail(h, NBM_E_ARG, "nbm_loss_grad: bad arguments");
-  if (n > h->ws.cap || nb > h->ws.cap) return fail(h, NBM_E_CAPACITY, "nbm_loss_grad: n or nb exceeds max_points");
-  if (n_global < n || nb_global < nb) return fail(h, NBM_E_ARG, "nbm_loss_grad: global counts smaller than local");
-  int64_t H;
-  if (!h_on_lattice(h_cell, &H)) return fail(h, NBM_E_INVALID_PROBLEM, "nbm_loss_grad: h must be a multiple of 2^-24 in (0,1) (G9)");
-  cudaSetDevice(h->device);
-  cudaStream_t s = (cudaStream_t)stream;
+}  // extern "C"
+
+namespace {
+// One resolution level of the loss: interior residuals at cell width h_cell (= H 2^-24)
+// weighted by `weight` (the level weight w_l of S:348; 1 for the single-level loss), the
+// boundary term if `terms` selects it.  accumulate: add to loss/grad instead of writing.
+int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_t n, const float* bpts_dev,
+                    int64_t nb, float h_cell, int64_t H, int64_t n_global, int64_t nb_global, unsigned terms,
+                    double weight, bool accumulate, bool pack, float* loss_dev, float* grad_dev, cudaStream_t s) {
   const DevProblem& P = h->host_problem;
   const ArchInfo& A = h->arch;
   const Workspace& w = h->ws;
@@ -436,7 +433,7 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
   if (ev) cudaEventRecord(ev[0], s);
   cudaError_t e = launch_classify(h, pts_dev, n, bpts_dev, nb, H, dm, dpl, terms, false, s);
   launches += 3;
-  if (e == cudaSuccess && (A.prec == NBM_PREC_BF16 || is_fp32w(A))) {
+  if (e == cudaSuccess && pack && (A.prec == NBM_PREC_BF16 || is_fp32w(A))) {
     e = launch_pack(h, theta_dev, s);
     launches += 1;
   }
@@ -461,12 +458,12 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
   pa.u_out = w.xrow_u;
   if (e == cudaSuccess) e = launch_mlp_h(h, false, pa, s);
   launches += 1;
-  if (e == cudaSuccess) e = launch_crossed_residual(h, n_global > 0 ? n_global : 1, s);
+  if (e == cudaSuccess) e = launch_crossed_residual(h, n_global > 0 ? n_global : 1, weight, s);
   launches += 1;
   // main fused pass over all segments (net- first, then net+)
   MlpParams pm;
   fill_common(h, pm, theta_dev, h_cell);
-  pm.two_over_n = (float)(2.0 / ng);
+  pm.two_over_n = (float)(2.0 * weight / ng);
   for (int k = 0; k < 2; ++k) {
     const int s0 = 3 * k, net = k == 0 ? 0 : net1;
     const int side = k;
@@ -501,8 +498,9 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
   if (ev) cudaEventRecord(ev[2], s);
   if (e == cudaSuccess)
     e = uses_rep(A) ? launch_reduce_rep(w.rep, w.nrep, A.p_net, (A.p_net + 3) & ~3ll, A.n_nets, A.n_hidden,
-                                        is_w256(A) ? 1 : 0, w.lpart, w.grid_mlp, grad_dev, loss_dev, w.err, s)
-                   : launch_reduce(h, grad_dev, loss_dev, s);
+                                        is_w256(A) ? 1 : 0, accumulate ? 1 : 0, w.lpart, w.grid_mlp, grad_dev, loss_dev,
+                                        w.err, s)
+                   : launch_reduce(h, accumulate, grad_dev, loss_dev, s);
   launches += 1;
   if (ev) {
     cudaEventRecord(ev[3], s);
@@ -510,6 +508,46 @@ int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, i
   }
   h->last_launches = launches;
   return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_loss_grad");
+}
+}  // namespace
+
+extern "C" {
+
+int nbm_loss_grad(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_t n,
+                  const float* bpts_dev, int64_t nb, float h_cell, int64_t n_global,
+                  int64_t nb_global, unsigned terms, float* loss_dev, float* grad_dev, void* stream) {
+  return nbm_loss_grad_ml(h, theta_dev, pts_dev, n, bpts_dev, nb, h_cell, 1, nullptr, n_global, nb_global, terms,
+                          loss_dev, grad_dev, stream);
+}
+
+int nbm_loss_grad_ml(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_t n,
+                     const float* bpts_dev, int64_t nb, float h0, int n_levels, const float* level_weights,
+                     int64_t n_global, int64_t nb_global, unsigned terms, float* loss_dev, float* grad_dev,
+                     void* stream) {
+  if (!h || !theta_dev || !loss_dev || !grad_dev || n < 0 || nb < 0 || (n > 0 && !pts_dev) ||
+      (nb > 0 && !bpts_dev) || n_levels < 1 || n_levels > 8)
+    return fail(h, NBM_E_ARG, "nbm_loss_grad: bad arguments");
+  if (n > h->ws.cap || nb > h->ws.cap) return fail(h, NBM_E_CAPACITY, "nbm_loss_grad: n or nb exceeds max_points");
+  if (n_global < n || nb_global < nb) return fail(h, NBM_E_ARG, "nbm_loss_grad: global counts smaller than local");
+  int64_t H0;
+  if (!h_on_lattice(h0, &H0)) return fail(h, NBM_E_INVALID_PROBLEM, "nbm_loss_grad: h must be a multiple of 2^-24 in (0,1) (G9)");
+  if (H0 % (1ll << (n_levels - 1)) != 0)
+    return fail(h, NBM_E_INVALID_PROBLEM, "nbm_loss_grad_ml: h0 / 2^(L-1) must stay on the 2^-24 lattice (G9)");
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  int launches = 0;
+  for (int l = 0; l < n_levels; ++l) {
+    const int64_t Hl = H0 >> l;
+    const double wl = level_weights ? (double)level_weights[l] : 1.0;
+    // the boundary residual does not depend on the cell width: counted once, at level 0
+    const unsigned tl = l == 0 ? terms : (terms & ~(unsigned)NBM_TERM_BOUNDARY);
+    const int rc = loss_grad_level(h, theta_dev, pts_dev, n, bpts_dev, l == 0 ? nb : 0, (float)((double)Hl / kLattice),
+                                   Hl, n_global, nb_global, tl, wl, l > 0, l == 0, loss_dev, grad_dev, s);
+    if (rc != NBM_OK) return rc;
+    launches += h->last_launches;
+  }
+  h->last_launches = launches;
+  return NBM_OK;
 }
 
 int nbm_classify(nbm_handle* h, const float* pts_dev, int64_t n, float h_cell, uint8_t* mask_dev,

@@ -143,7 +143,7 @@ cudaError_t launch_classify(const nbm_handle* h, const float* pts, int64_t n, co
                             uint8_t* mask_out = nullptr);
 cudaError_t launch_assemble_crossed(const nbm_handle* h, const float* pts, int64_t n, int64_t H,
                                     cudaStream_t s);
-cudaError_t launch_crossed_residual(const nbm_handle* h, int64_t n_global, cudaStream_t s);
+cudaError_t launch_crossed_residual(const nbm_handle* h, int64_t n_global, double weight, cudaStream_t s);
 // mlp_fp32.cu
 struct MlpParams {
   SegTable seg;
@@ -181,9 +181,9 @@ cudaError_t launch_mlp_w256(int n_hidden, bool train, const MlpParams& m, const 
                             uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s);
 cudaError_t launch_pack_w256(const ArchInfo& a, const float* theta, uint16_t* wf, uint16_t* wb, cudaStream_t s);
 cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets, int n_hidden,
-                              int quad_major,
+                              int quad_major, int accumulate,
                               const double* lpart, int G, float* grad, float* loss, int* err, cudaStream_t s);
 // reduce
-cudaError_t launch_reduce(const nbm_handle* h, float* grad, float* loss, cudaStream_t s);
+cudaError_t launch_reduce(const nbm_handle* h, bool accumulate, float* grad, float* loss, cudaStream_t s);
 
 }  // namespace nbm

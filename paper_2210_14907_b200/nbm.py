@@ -82,6 +82,7 @@ def lib():
         L.nbm_eval.argtypes = [v, v, v, i64, v, v]
         L.nbm_classify.argtypes = [v, v, i64, f, v, v, v]
         L.nbm_adam_step.argtypes = [v, v, v, v, v, i64, f, f, f, f, v]
+        L.nbm_loss_grad_ml.argtypes = [v, v, v, i64, v, i64, f, C.c_int, v, i64, i64, C.c_uint, v, v, v]
         L.nbm_sample_at.argtypes = [v, u64, v, C.c_int, i64, i64, f, v, v]
         L.nbm_adam_step_at.argtypes = [v, v, v, v, v, v, f, f, f, f, v]
         L.nbm_timing_enable.argtypes = [v, C.c_int]
@@ -196,6 +197,16 @@ def nbm_loss_grad(h, theta, pts, n: int, bpts, nb: int, h_cell: float, n_global:
                                   nb_global, terms, _ptr(loss), _ptr(grad), _stream(stream)))
 
 
+def nbm_loss_grad_ml(h, theta, pts, n: int, bpts, nb: int, h0: float, n_levels: int, level_weights,
+                     n_global: int, nb_global: int, terms: int, loss, grad, stream=None) -> None:
+    w = None
+    if level_weights is not None:
+        w = (C.c_float * n_levels)(*[float(x) for x in level_weights])
+    _check(h, lib().nbm_loss_grad_ml(h, _ptr(theta), _ptr(pts), n, _ptr(bpts), nb, h0, n_levels,
+                                     C.cast(w, C.c_void_p) if w is not None else None, n_global, nb_global,
+                                     terms, _ptr(loss), _ptr(grad), _stream(stream)))
+
+
 def nbm_classify(h, pts, n: int, h_cell: float, mask, cls, stream=None) -> None:
     _check(h, lib().nbm_classify(h, _ptr(pts), n, h_cell, _ptr(mask), _ptr(cls), _stream(stream)))
 
@@ -280,12 +291,18 @@ class Solver:
     def sample(self, kind, seed, step, first, n, out):
         nbm_sample(self.h, seed, step, kind, first, n, self.h_cell, out)
 
-    def loss_grad(self, pts, bpts, n_global=None, nb_global=None, terms=TERM_ALL, theta=None):
+    def loss_grad(self, pts, bpts, n_global=None, nb_global=None, terms=TERM_ALL, theta=None, levels=1,
+                  level_weights=None):
         n = 0 if pts is None else pts.shape[0]
         nb = 0 if bpts is None else bpts.shape[0]
-        nbm_loss_grad(self.h, self.theta if theta is None else theta, pts, n, bpts, nb, self.h_cell,
-                      n if n_global is None else n_global, nb if nb_global is None else nb_global,
-                      terms, self.loss, self.grad)
+        th = self.theta if theta is None else theta
+        ng = n if n_global is None else n_global
+        nbg = nb if nb_global is None else nb_global
+        if levels == 1 and level_weights is None:
+            nbm_loss_grad(self.h, th, pts, n, bpts, nb, self.h_cell, ng, nbg, terms, self.loss, self.grad)
+        else:
+            nbm_loss_grad_ml(self.h, th, pts, n, bpts, nb, self.h_cell, levels, level_weights, ng, nbg, terms,
+                             self.loss, self.grad)
         return self.loss, self.grad
 
     def adam_step(self, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
@@ -301,7 +318,7 @@ class Solver:
         nbm_adam_step_at(self.h, self.theta, self.m, self.v, self.grad, self.t_dev, lr, b1, b2, eps)
 
     def capture_step(self, pts, bpts, first=0, bfirst=0, n_global=None, nb_global=None, lr=1e-3, seed=0,
-                     allreduce=None):
+                     allreduce=None, levels=1):
         """Capture one training step [sample interior, sample boundary, loss_grad,
         (allreduce), Adam] as CUDA graphs on the device counter self.t_dev.  Returns a
         callable that replays one step.  With `allreduce` (a callable on the [grad, loss]
@@ -312,7 +329,7 @@ class Solver:
         def pre():
             self.sample_at(POINTS_INTERIOR, seed, first, n, pts)
             self.sample_at(POINTS_BOUNDARY, seed, bfirst, nb, bpts)
-            self.loss_grad(pts, bpts, n_global=n_global, nb_global=nb_global)
+            self.loss_grad(pts, bpts, n_global=n_global, nb_global=nb_global, levels=levels)
 
         def post():
             self.adam_step_at(lr=lr)

@@ -381,3 +381,33 @@ def test_graph_replay_matches_eager_steps(orc, name, split):
     assert a.status() == 0 and b.status() == 0
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("name,levels,weights,n,nb", [("c1", 3, None, 4096, 512), ("c2", 3, [1.0, 0.5, 0.25], 1 << 13, 1 << 10),
+                                                       ("c2", 2, None, 37, 5)])
+def test_multiresolution_parity(orc, name, levels, weights, n, nb):
+    """Multi-resolution loss ("levels of implicit refinement", SURVEY 8f
+    NEXT-1): nbm_loss_grad_ml at h_l = h0/2^l vs the oracle's loss_grad_ml (fp32 bars; the
+    uncrossed terms' fp32 noise floor from the oracle's emulation)."""
+    cfg = _cfg(name)
+    pb, ar = orc.from_config(cfg)
+    s = nbm.Solver(cfg, 0, max_points=max(n, nb))
+    th = inputs.random_theta(cfg["sizes"], cfg["n_nets"], 3)
+    p_ = orc.sample(0, 8, 0, 0, n, cfg["H"])
+    b_ = orc.sample(1, 8, 0, 0, nb, cfg["H"])
+    loss, grad = s.loss_grad(_dev(p_), _dev(b_), theta=_dev(th), levels=levels, level_weights=weights)
+    torch.cuda.synchronize()
+    gl, gg = float(loss.item()), grad.double().cpu().numpy()
+    L, g = orc.loss_grad_ml(pb, ar, th, p_, b_, cfg["h"], levels, weights)
+    L32, g32 = orc.loss_grad_ml(pb, ar, th, p_, b_, cfg["h"], levels, weights, mode=orc.MODE_F32)
+    ltol = max(LOSS_TOL, 4 * abs(L32 - L) / L)
+    gtol = max(GRAD_TOL, 4 * np.linalg.norm(g32 - g) / np.linalg.norm(g))
+    assert abs(gl - L) <= ltol * L, (gl, L)
+    assert np.linalg.norm(gg - g) <= gtol * np.linalg.norm(g)
+    l1, _ = _gpu_loss_grad(s, _dev(th), _dev(p_), _dev(b_))
+    assert gl >= l1   # the extra levels add non-negative terms
+    with pytest.raises(nbm.NbmError) as e:      # h0 / 2^(L-1) must stay on the lattice
+        s.loss_grad(_dev(p_), _dev(b_), levels=30)
+    assert e.value.code == 5
+    assert s.status() == 0
+    s.close()

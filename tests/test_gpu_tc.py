@@ -128,3 +128,27 @@ def test_tc_full_size_config4(orc):
     assert np.linalg.norm(acc_g - gt) <= 1e-4 * np.linalg.norm(gt)
     assert s.status() == 0
     s.close()
+
+
+@pytest.mark.parametrize("name,w,nh", [("c5", 128, 4), ("c4", 256, 4)])
+def test_tc_multiresolution(orc, name, w, nh):
+    """Multi-resolution loss on the bf16 paths (K3t per-CTA partials, K3w L2 replicas): two
+    levels accumulate in the reduction; 2e-2 vs the fp64 oracle, 3e-3 vs its bf16 emulation."""
+    cfg = inputs.config(name, width=w)
+    cfg["sizes"] = [3] + [w] * nh + [1]
+    n, nb = 1 << 12, 1 << 9
+    s = nbm.Solver(cfg, 0, max_points=n)
+    pb, ar = orc.from_config(cfg)
+    pts = orc.sample(0, 9, 0, 0, n, cfg["H"])
+    bpts = orc.sample(1, 9, 0, 0, nb, cfg["H"])
+    th = orc.init_params(ar, 0)
+    loss, grad = s.loss_grad(_dev(pts), _dev(bpts), theta=_dev(th), levels=2)
+    torch.cuda.synchronize()
+    gl, gg = float(loss.item()), grad.double().cpu().numpy()
+    L, g = orc.loss_grad_ml(pb, ar, th, pts, bpts, cfg["h"], 2)
+    Le, ge = orc.loss_grad_ml(pb, ar, th, pts, bpts, cfg["h"], 2, mode=orc.MODE_BF16)
+    assert abs(gl - L) <= TOL * L, (gl, L)
+    assert np.linalg.norm(gg - g) <= TOL * np.linalg.norm(g)
+    assert abs(gl - Le) <= EMU_TOL * Le, (gl, Le)
+    assert np.linalg.norm(gg - ge) <= EMU_TOL * np.linalg.norm(ge)
+    s.close()

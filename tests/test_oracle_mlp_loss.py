@@ -279,3 +279,30 @@ def test_precision_emulations_are_close_to_fp64(orc):
     assert np.linalg.norm(g32 - g64) < 1e-5 * np.linalg.norm(g64)
     assert abs(Lbf - L64) < 2e-2 * L64
     assert np.linalg.norm(gbf - g64) < 2e-2 * np.linalg.norm(g64)
+
+
+def test_multiresolution_loss_gradient_matches_central_differences(orc):
+    """S:353 example 3 "on a 10-point batch with L=2" (and S:348's multi-level loss, SURVEY 8f
+    NEXT-1): the multi-resolution loss gradient vs central FD over all parameters, with
+    non-unit level weights; the level-1 rows (half the cell width) cross the interface on a
+    different set of arms than level 0.  Also: L = 1 reduces to the single-level loss."""
+    cfg = _cfg([3, 4, 4, 1], act=0)
+    pb, ar, pts, b, h = _mixed_batch(orc, cfg)
+    th = np.random.default_rng(5).normal(size=ar.P) * 0.8
+    w = [1.0, 0.5]
+    L, g = orc.loss_grad_ml(pb, ar, th, pts, b, h, 2, w)
+    L1, _, g1, _ = orc.loss_grad(pb, ar, th, pts, b, h)
+    Lm1, gm1 = orc.loss_grad_ml(pb, ar, th, pts, b, h, 1)
+    assert Lm1 == pytest.approx(L1, rel=1e-14) and np.allclose(gm1, g1, rtol=1e-14, atol=0)
+    _, c0 = orc.classify(pb, pts, h)
+    _, c1 = orc.classify(pb, pts, h / 2)
+    assert (c0 == 2).sum() != (c1 == 2).sum() or not np.array_equal(c0, c1)
+    fd = np.zeros(ar.P)
+    for i in range(ar.P):
+        tp, tm = th.copy(), th.copy()
+        tp[i] += 1e-6
+        tm[i] -= 1e-6
+        fd[i] = (orc.loss_grad_ml(pb, ar, tp, pts, b, h, 2, w)[0] - orc.loss_grad_ml(pb, ar, tm, pts, b, h, 2, w)[0]) / 2e-6
+    scale = np.abs(g).max()
+    assert np.all(np.abs(g - fd) <= 1e-5 * np.maximum(np.abs(g), 1e-3 * scale))
+    assert L > L1   # the level-1 terms add non-negative contributions
