@@ -170,6 +170,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
+    ap.add_argument("--grid", type=int, default=None,
+                    help="replace the level set by its samples on an Nc^3 grid (S:82 Sampled variant, P:60)")
     ap.add_argument("--levels", type=int, default=1,
                     help="multi-resolution levels h0/2^l of the loss (S:348; the paper's scaling runs use 3)")
     ap.add_argument("--points", type=int, default=None, help="override interior points per GPU")
@@ -179,8 +181,11 @@ def main():
     rank, world, local = dp.env_rank_world()
     prec = None if args.prec is None else (inputs.PREC_FP32 if args.prec == "fp32" else inputs.PREC_BF16)
     cfg = inputs.config(args.config, width=args.width, prec=prec)
+    if args.grid:
+        cfg = inputs.with_grid(cfg, args.grid)
     cfg["label"] = cfg["name"] + (f"-w{cfg['sizes'][1]}" if cfg["name"] == "c5" else "") + \
-        ("" if prec is None else ("-fp32" if prec == inputs.PREC_FP32 else "-bf16"))
+        ("" if prec is None else ("-fp32" if prec == inputs.PREC_FP32 else "-bf16")) + \
+        (f"-grid{args.grid}" if args.grid else "")
     if args.points:
         cfg["N"] = args.points
         cfg["Nb"] = max(1, args.points // 8)

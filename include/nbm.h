@@ -44,6 +44,11 @@ extern "C" {
 #define NBM_LS_SPHERES  1  /* phi = min_k (|x - c_k| - r_k), union of n spheres (configs 2, 4) */
 #define NBM_LS_STAR     2  /* phi = r - r0 - amp sin(m th) cos(n ph), th from +z, ph = atan2(y,x) (config 3, G13) */
 #define NBM_LS_PLANE    3  /* phi = n.x - c */
+#define NBM_LS_GRID     4  /* Sampled level set ("a separate coarse mesh"): trilinear
+                            * interpolation of nodal values on an (Nc+1)^3 grid over [-1,1]^3;
+                            * crossings at the root of the linear interpolant between the arm's end
+                            * values; normals by central differences of the interpolant with
+                            * step hc/2 */
 
 /* ---- data families: f, alpha = [u], sigma = [beta d_n u], g derived inside the library ---- */
 #define NBM_SRC_SINE3PI  0  /* u = sin(pi x) sin(pi y) sin(pi z) on both sides (config 1) */
@@ -73,6 +78,9 @@ typedef struct nbm_levelset {
   float star_r0, star_amp;       /* NBM_LS_STAR */
   int star_m, star_n;            /* angular frequencies, 0..16 */
   float plane_n[3], plane_c;     /* NBM_LS_PLANE */
+  int grid_n;                    /* NBM_LS_GRID: Nc cells per axis, 1..1024 */
+  const float* grid_phi;         /* NBM_LS_GRID: host, [(Nc+1)^3] nodal values, x fastest
+                                  * (S:145 order), copied to the device at create */
 } nbm_levelset;
 
 /* Problem descriptor (k u - div(beta grad u) = f, [u] = alpha,

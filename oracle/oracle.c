@@ -126,6 +126,35 @@ static double star_phi(const orc_problem* pb, const double x[3]) {
   return (r - pb->star_r0) - pb->star_amp * ang;
 }
 
+/* Sampled level set ("trilinear interpolation of nodal values", "a separate coarse
+ * mesh encapsulates a level-set function"): nodes x_i = -1 + i hc, hc = 2/Nc, values x-fastest.
+ * Cell index and local coordinate per axis from s = (x + 1) Nc/2 (clamped to the cube), then
+ * seven linear interpolations a + t (b - a): along x, then y, then z. */
+static double grid_lerp(double a, double b, double t) { return a + t * (b - a); }
+static double grid_phi(const orc_problem* pb, const double x[3]) {
+  const int nc = pb->grid_n, n1 = nc + 1;
+  const double half = 0.5 * (double)nc;
+  int i[3];
+  double t[3];
+  for (int d = 0; d < 3; ++d) {
+    double sd = (x[d] + 1.0) * half;
+    if (sd < 0.0) sd = 0.0;
+    if (sd > (double)nc) sd = (double)nc;
+    int id = (int)floor(sd);
+    if (id > nc - 1) id = nc - 1;
+    i[d] = id;
+    t[d] = sd - (double)id;
+  }
+#define GV(a, b, c) pb->grid_phi[(int64_t)(i[0] + (a)) + (int64_t)n1 * ((int64_t)(i[1] + (b)) + (int64_t)n1 * (i[2] + (c)))]
+  double c00 = grid_lerp(GV(0, 0, 0), GV(1, 0, 0), t[0]);
+  double c10 = grid_lerp(GV(0, 1, 0), GV(1, 1, 0), t[0]);
+  double c01 = grid_lerp(GV(0, 0, 1), GV(1, 0, 1), t[0]);
+  double c11 = grid_lerp(GV(0, 1, 1), GV(1, 1, 1), t[0]);
+#undef GV
+  double c0 = grid_lerp(c00, c10, t[1]), c1 = grid_lerp(c01, c11, t[1]);
+  return grid_lerp(c0, c1, t[2]);
+}
+
 double orc_phi(const orc_problem* pb, const double x[3]) {
   switch (pb->ls_kind) {
     case ORC_LS_NONE: return -1.0;                /* everything is Omega- (config 1) */
@@ -137,6 +166,7 @@ double orc_phi(const orc_problem* pb, const double x[3]) {
     case ORC_LS_STAR: return star_phi(pb, x);
     case ORC_LS_PLANE:
       return ((pb->plane_n[0] * x[0] + pb->plane_n[1] * x[1]) + pb->plane_n[2] * x[2]) - pb->plane_c;
+    case ORC_LS_GRID: return grid_phi(pb, x);
   }
   return -1.0;
 }
@@ -155,8 +185,8 @@ int orc_normal(const orc_problem* pb, const double x[3], double nrm[3]) {
     const double* c = pb->centers + 3 * best;
     g[0] = x[0] - c[0]; g[1] = x[1] - c[1]; g[2] = x[2] - c[2];
   } else {
-    /* central differences, step 1e-5 */
-    const double e = 1e-5;
+    /* central differences, step 1e-5 (Analytic) or hc/2 = 1/Nc of the interpolant (Sampled) */
+    const double e = pb->ls_kind == ORC_LS_GRID ? 1.0 / (double)pb->grid_n : 1e-5;
     for (int d = 0; d < 3; ++d) {
       double xp[3] = {x[0], x[1], x[2]}, xm[3] = {x[0], x[1], x[2]};
       xp[d] += e; xm[d] -= e;
@@ -227,6 +257,10 @@ int orc_crossing(const orc_problem* pb, const double a[3], const double b[3],
   } else if (pb->ls_kind == ORC_LS_PLANE) {
     double nd = pb->plane_n[0] * d[0] + pb->plane_n[1] * d[1] + pb->plane_n[2] * d[2];
     th = -orc_phi(pb, a) / nd;
+  } else if (pb->ls_kind == ORC_LS_GRID) {
+    /* S:125 Sampled: root of the linear interpolant between phi(a) and phi(b) */
+    double pa = orc_phi(pb, a), pbv = orc_phi(pb, b);
+    th = pa / (pa - pbv);
   } else {
     double lo = 0.0, hi = 1.0;
     for (int it = 0; it < 60; ++it) {

@@ -23,7 +23,7 @@ extern "C" {
 #endif
 
 /* level-set kinds (configs in BASELINE.json) */
-enum { ORC_LS_NONE = 0, ORC_LS_SPHERES = 1, ORC_LS_STAR = 2, ORC_LS_PLANE = 3 };
+enum { ORC_LS_NONE = 0, ORC_LS_SPHERES = 1, ORC_LS_STAR = 2, ORC_LS_PLANE = 3, ORC_LS_GRID = 4 };
 /* data families: manufactured or physical (BASELINE.json configs 1-4) */
 enum { ORC_SRC_SINE3PI = 0, ORC_SRC_PAIR = 1, ORC_SRC_GAUSS = 2, ORC_SRC_POLY2 = 3 };
 /* activations */
@@ -51,6 +51,8 @@ typedef struct {
   double charge_sigma;
   const double* poly;            /* ORC_SRC_POLY2: [2][10] c, g[3], A00 A01 A02 A11 A12 A22 */
   double lambda_b;               /* boundary weight */
+  int grid_n;                    /* ORC_LS_GRID: Nc cells per axis (S:82 Sampled variant) */
+  const double* grid_phi;        /* [(Nc+1)^3] nodal values over [-1,1]^3, x fastest */
 } orc_problem;
 
 typedef struct {

@@ -43,7 +43,7 @@ class Problem(C.Structure):
                 ("source", C.c_int), ("n_charges", C.c_int),
                 ("q", C.POINTER(C.c_double)), ("charge_centers", C.POINTER(C.c_double)),
                 ("charge_sigma", C.c_double), ("poly", C.POINTER(C.c_double)),
-                ("lambda_b", C.c_double)]
+                ("lambda_b", C.c_double), ("grid_n", C.c_int), ("grid_phi", C.POINTER(C.c_double))]
 
 
 class Arch(C.Structure):
@@ -171,6 +171,12 @@ class OracleProblem:
             self._keep.append(pa)
             p.poly = _ptr(pa, C.c_double)
         p.lambda_b = f32(cfg["lambda_b"])
+        if cfg.get("grid") is not None:   # sampled level set: fp32 nodal values (as the CUDA path gets)
+            gphi = _f64(np.asarray(cfg["grid"], np.float32).reshape(-1))
+            self._keep.append(gphi)
+            p.grid_n = int(round(len(gphi) ** (1.0 / 3.0))) - 1
+            assert (p.grid_n + 1) ** 3 == len(gphi)
+            p.grid_phi = _ptr(gphi, C.c_double)
         self.s = p
         self.ref = C.byref(p)
 

@@ -54,6 +54,35 @@ __device__ double d_star_phi(const DevProblem& P, const double x[3]) {
   return (r - P.star_r0) - P.star_amp * ((st * um) * tn);
 }
 
+// Sampled level set (S:82, P:60 coarse mesh): trilinear interpolation of the nodal values with a
+// fixed operation order (s = (x + 1) Nc/2 clamped to the cube, cell index, then seven
+// a + t (b - a) along x, y, z), bit-identical to the oracle under -fmad=false.
+__device__ __forceinline__ double d_lerp(double a, double b, double t) { return a + t * (b - a); }
+__device__ double d_grid_phi(const DevProblem& P, const double x[3]) {
+  const int nc = P.grid_n, n1 = nc + 1;
+  const double half = 0.5 * (double)nc;
+  int i[3];
+  double t[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    double sd = (x[d] + 1.0) * half;
+    if (sd < 0.0) sd = 0.0;
+    if (sd > (double)nc) sd = (double)nc;
+    int id = (int)floor(sd);
+    if (id > nc - 1) id = nc - 1;
+    i[d] = id;
+    t[d] = sd - (double)id;
+  }
+  const float* g = P.grid_phi + (int64_t)i[0] + (int64_t)n1 * ((int64_t)i[1] + (int64_t)n1 * i[2]);
+  const int64_t sy = n1, sz = (int64_t)n1 * n1;
+  const double c00 = d_lerp((double)__ldg(g), (double)__ldg(g + 1), t[0]);
+  const double c10 = d_lerp((double)__ldg(g + sy), (double)__ldg(g + sy + 1), t[0]);
+  const double c01 = d_lerp((double)__ldg(g + sz), (double)__ldg(g + sz + 1), t[0]);
+  const double c11 = d_lerp((double)__ldg(g + sz + sy), (double)__ldg(g + sz + sy + 1), t[0]);
+  const double c0 = d_lerp(c00, c10, t[1]), c1 = d_lerp(c01, c11, t[1]);
+  return d_lerp(c0, c1, t[2]);
+}
+
 __device__ double d_phi(const DevProblem& P, const double x[3]) {
   switch (P.ls_kind) {
     case NBM_LS_SPHERES: {
@@ -65,6 +94,8 @@ __device__ double d_phi(const DevProblem& P, const double x[3]) {
       return d_star_phi(P, x);
     case NBM_LS_PLANE:
       return ((P.plane_n[0] * x[0] + P.plane_n[1] * x[1]) + P.plane_n[2] * x[2]) - P.plane_c;
+    case NBM_LS_GRID:
+      return d_grid_phi(P, x);
     default:
       return -1.0;
   }
@@ -134,7 +165,7 @@ __device__ bool d_normal(const DevProblem& P, const double x[3], double n[3]) {
     }
     for (int d = 0; d < 3; ++d) g[d] = x[d] - P.centers[best][d];
   } else {
-    const double e = 1e-5;
+    const double e = P.ls_kind == NBM_LS_GRID ? 1.0 / (double)P.grid_n : 1e-5;   // S:116 (Sampled: hc/2)
     for (int d = 0; d < 3; ++d) {
       double xp[3] = {x[0], x[1], x[2]}, xm[3] = {x[0], x[1], x[2]};
       xp[d] += e;
@@ -154,6 +185,10 @@ __device__ double d_crossing_theta(const DevProblem& P, const double a[3], const
   if (P.ls_kind == NBM_LS_PLANE) {
     double nd = P.plane_n[0] * d[0] + P.plane_n[1] * d[1] + P.plane_n[2] * d[2];
     return -d_phi(P, a) / nd;
+  }
+  if (P.ls_kind == NBM_LS_GRID) {   // S:125 Sampled: root of the linear interpolant of the end values
+    const double pa = d_phi(P, a), pb = d_phi(P, b);
+    return pa / (pa - pb);
   }
   if (P.ls_kind == NBM_LS_SPHERES) {
     double best = -1.0;

@@ -84,7 +84,13 @@ int check_problem(const nbm_problem* p, DevProblem* out, std::string* why) {
   if (!(p->k_minus >= 0.0f) || !(p->k_plus >= 0.0f)) { *why = "problem: k must be >= 0"; return NBM_E_INVALID_PROBLEM; }
   if (!(p->lambda_b >= 0.0f)) { *why = "problem: lambda_b must be >= 0"; return NBM_E_INVALID_PROBLEM; }
   const nbm_levelset& ls = p->ls;
-  if (ls.kind < NBM_LS_NONE || ls.kind > NBM_LS_PLANE) { *why = "problem: bad level-set kind"; return NBM_E_INVALID_PROBLEM; }
+  if (ls.kind < NBM_LS_NONE || ls.kind > NBM_LS_GRID) { *why = "problem: bad level-set kind"; return NBM_E_INVALID_PROBLEM; }
+  if (ls.kind == NBM_LS_GRID) {
+    if (ls.grid_n < 1 || ls.grid_n > 1024 || !ls.grid_phi) { *why = "problem: grid level set needs 1..1024 cells and nodal values"; return NBM_E_INVALID_PROBLEM; }
+    const int64_t nn = (int64_t)(ls.grid_n + 1) * (ls.grid_n + 1) * (ls.grid_n + 1);
+    for (int64_t i = 0; i < nn; ++i)
+      if (!isfinite(ls.grid_phi[i])) { *why = "problem: non-finite level-set node"; return NBM_E_INVALID_PROBLEM; }
+  }
   if (ls.kind == NBM_LS_SPHERES) {
     if (ls.n < 1 || ls.n > kMaxSpheres || !ls.centers || !ls.radii) { *why = "problem: spheres need 1..64 centres and radii"; return NBM_E_INVALID_PROBLEM; }
     for (int k = 0; k < ls.n; ++k)
@@ -113,6 +119,8 @@ int check_problem(const nbm_problem* p, DevProblem* out, std::string* why) {
     out->star_m = ls.star_m; out->star_n = ls.star_n;
     for (int d = 0; d < 3; ++d) out->plane_n[d] = ls.plane_n[d];
     out->plane_c = ls.plane_c;
+    out->grid_n = ls.kind == NBM_LS_GRID ? ls.grid_n : 0;
+    out->grid_phi = nullptr;   // device copy made by nbm_create
     out->beta[0] = p->beta_minus; out->beta[1] = p->beta_plus;
     out->k[0] = p->k_minus; out->k[1] = p->k_plus;
     out->source = p->source;
@@ -327,6 +335,18 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
       return NBM_E_CUDA;
     }
   }
+  if (dp.ls_kind == NBM_LS_GRID) {   // the sampled level set's nodes live on the device
+    const size_t gb = (size_t)(dp.grid_n + 1) * (dp.grid_n + 1) * (dp.grid_n + 1) * sizeof(float);
+    e = cudaMalloc(&h->d_grid, gb);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_grid, problem->ls.grid_phi, gb, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      g_create_error = std::string("grid level set: ") + cudaGetErrorString(e);
+      nbm_destroy(h);
+      return NBM_E_CUDA;
+    }
+    dp.grid_phi = h->d_grid;
+    h->host_problem.grid_phi = h->d_grid;
+  }
   e = cudaMemcpy(h->d_problem, &dp, sizeof(dp), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(w.counts, 0, 16 * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(w.err, 0, sizeof(int));
@@ -347,7 +367,7 @@ void nbm_destroy(nbm_handle* h) {
   void* ps[] = {h->d_problem, h->ws.cls, h->ws.aux_tmp, h->ws.blk_counts, h->ws.blk_offsets,
                 h->ws.counts, h->ws.list, h->ws.list_aux, h->ws.xrow_x, h->ws.xrow_u, h->ws.xrow_cot,
                 h->ws.xrow_tag, h->ws.xrec, h->ws.xlist, h->ws.part, h->ws.touched, h->ws.lpart,
-                h->ws.err, h->ws.bc, h->ws.wimg, h->ws.wimg_b, h->ws.hscr, h->ws.rep, h->ws.wimg32};
+                h->ws.err, h->ws.bc, h->d_grid, h->ws.wimg, h->ws.wimg_b, h->ws.hscr, h->ws.rep, h->ws.wimg32};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : h->ev) cudaEventDestroy(ev);

@@ -37,6 +37,8 @@ struct DevProblem {
   double lambda_b;
   float centers_f[kMaxSpheres][3];   // fp32 copies (exact: the inputs are fp32) for the filter
   float radii_f[kMaxSpheres];
+  int grid_n;                        // NBM_LS_GRID: Nc
+  const float* grid_phi;             // NBM_LS_GRID: device copy of the nodal values (handle-owned)
 };
 
 // Point classes produced by the classification stage (S2).
@@ -116,6 +118,7 @@ struct nbm_handle {
   nbm::ArchInfo arch;
   nbm::DevProblem host_problem;
   nbm::DevProblem* d_problem;
+  float* d_grid;                 // NBM_LS_GRID nodal values (device), else null
   nbm::Workspace ws;
   std::string last_error;
   // timing hook

@@ -13,7 +13,7 @@ import numpy as np
 
 LATTICE = 1 << 24  # coordinates and h are multiples of 2^-24 (G9)
 
-LS_NONE, LS_SPHERES, LS_STAR, LS_PLANE = 0, 1, 2, 3
+LS_NONE, LS_SPHERES, LS_STAR, LS_PLANE, LS_GRID = 0, 1, 2, 3, 4
 SRC_SINE3PI, SRC_PAIR, SRC_GAUSS = 0, 1, 2
 ACT_TANH, ACT_SILU, ACT_SINE = 0, 1, 2
 PREC_FP32, PREC_BF16 = 0, 1
@@ -46,13 +46,44 @@ def _config3_charges(seed: int = 0):
     return q, np.asarray(cs, dtype=np.float32)
 
 
+def sampled_levelset(cfg: dict, nc: int) -> np.ndarray:
+    """Nodal values of the configuration's sphere-union level set on the (nc+1)^3 grid over
+    [-1,1]^3, x fastest, fp32 (S:82 Sampled variant, S:145 file order).  This is input data:
+    the paper's level set lives on "a separate coarse mesh" that the method only
+    interpolates; here the mesh is filled from the analytic geometry of the configuration."""
+    if cfg["ls_kind"] == LS_SPHERES:
+        g = np.linspace(-1.0, 1.0, nc + 1)
+        z, y, x = np.meshgrid(g, g, g, indexing="ij")           # x fastest in C order
+        X = np.stack([x, y, z], axis=-1).astype(np.float64)
+        c = np.asarray(cfg["centers"], np.float64)
+        r = np.asarray(cfg["radii"], np.float64)
+        d = np.sqrt(((X[..., None, :] - c) ** 2).sum(-1)) - r
+        return d.min(-1).astype(np.float32).reshape(-1)
+    if cfg["ls_kind"] == LS_PLANE:
+        g = np.linspace(-1.0, 1.0, nc + 1)
+        z, y, x = np.meshgrid(g, g, g, indexing="ij")
+        (a, b, cc), c0 = cfg["plane"]
+        return (a * x + b * y + cc * z - c0).astype(np.float32).reshape(-1)
+    raise ValueError("sampled level sets are built from sphere-union or plane geometries")
+
+
+def with_grid(cfg: dict, nc: int) -> dict:
+    """The configuration with its level set replaced by the sampled one on an nc^3 grid."""
+    out = dict(cfg)
+    out["grid"] = sampled_levelset(cfg, nc)
+    out["ls_kind"] = LS_GRID
+    out["name"] = cfg["name"]
+    out["grid_n"] = nc
+    return out
+
+
 def config(name: str, width: int | None = None, prec: int | None = None) -> dict:
     """Plain parameter dict of a BASELINE.json configuration ('c1'..'c5')."""
     base = dict(box=(-1.0, 1.0), k=(0.0, 0.0), lambda_b=1.0, ls_kind=LS_NONE,
                 centers=np.zeros((0, 3), np.float32), radii=np.zeros(0, np.float32),
                 star=(0.5, 0.15, 5, 3), plane=((1.0, 0.0, 0.0), 0.0),
                 charges_q=np.zeros(0, np.float32), charges_c=np.zeros((0, 3), np.float32),
-                charge_sigma=0.02, seed=0)
+                charge_sigma=0.02, seed=0, grid=None)
     if name == "c1":
         base.update(ls_kind=LS_NONE, beta=(1.0, 1.0), source=SRC_SINE3PI,
                     sizes=[3, 32, 32, 1], act=ACT_TANH, prec=PREC_FP32, n_nets=1,

@@ -37,7 +37,7 @@ class nbm_levelset(C.Structure):
     _fields_ = [("kind", C.c_int), ("n", C.c_int), ("centers", C.POINTER(C.c_float)),
                 ("radii", C.POINTER(C.c_float)), ("star_r0", C.c_float), ("star_amp", C.c_float),
                 ("star_m", C.c_int), ("star_n", C.c_int), ("plane_n", C.c_float * 3),
-                ("plane_c", C.c_float)]
+                ("plane_c", C.c_float), ("grid_n", C.c_int), ("grid_phi", C.POINTER(C.c_float))]
 
 
 class nbm_problem(C.Structure):
@@ -114,6 +114,11 @@ class Descriptors:
         for d in range(3):
             ls.plane_n[d] = pn[d]
         ls.plane_c = pc
+        if cfg.get("grid") is not None:
+            gphi = np.ascontiguousarray(np.asarray(cfg["grid"], np.float32).reshape(-1))
+            self._keep.append(gphi)
+            ls.grid_n = int(round(len(gphi) ** (1.0 / 3.0))) - 1
+            ls.grid_phi = gphi.ctypes.data_as(C.POINTER(C.c_float))
         p.ls = ls
         p.beta_minus, p.beta_plus = cfg["beta"]
         p.k_minus, p.k_plus = cfg["k"]

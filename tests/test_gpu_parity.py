@@ -411,3 +411,37 @@ def test_multiresolution_parity(orc, name, levels, weights, n, nb):
     assert e.value.code == 5
     assert s.status() == 0
     s.close()
+
+
+@pytest.mark.parametrize("name,nc", [("c2", 64), ("c4", 128), ("c4", 37)])
+def test_grid_levelset_classification_bit_exact(orc, name, nc):
+    """Sampled level set (S:82, P:60 coarse mesh): trilinear phi in fp64 with the fixed
+    operation order, so the GPU's stencil masks and classes equal the oracle's bit for bit
+    (Nc = 37: non-power-of-two cell width)."""
+    cfg = inputs.with_grid(_cfg(name), nc)
+    n = 1 << 16
+    s = nbm.Solver(cfg, 0, max_points=n)
+    pb, _ = orc.from_config(cfg)
+    pts = orc.sample(0, 13, 0, 0, n, cfg["H"])
+    mask = torch.empty(n, dtype=torch.uint8, device="cuda")
+    cls = torch.empty(n, dtype=torch.uint8, device="cuda")
+    nbm.nbm_classify(s.h, _dev(pts), n, s.h_cell, mask, cls)
+    om, oc = orc.classify(pb, pts, cfg["h"])
+    assert np.array_equal(mask.cpu().numpy(), om)
+    assert np.array_equal(cls.cpu().numpy(), oc)
+    assert (oc == 2).sum() > 50
+    s.close()
+
+
+@pytest.mark.parametrize("name,nc", [("c2", 64), ("c4", 96)])
+def test_grid_levelset_parity(orc, name, nc):
+    """Loss and gradient per term on a sampled level set: crossings at the linear-interpolant
+    root, normals from the interpolant feeding sigma.  Config 4's geometry at
+    h = 1/64: at its own h_q(2/1023) the uncrossed fp32 terms are noise-dominated (~1e-16,
+    SURVEY 8c) and their per-term noise floor is not a stable statistic."""
+    cfg = inputs.with_grid(_cfg(name), nc)
+    if name == "c4":
+        cfg["H"] = inputs.h_lattice(1 / 64)
+        cfg["h"] = cfg["H"] / inputs.LATTICE
+    lt = _parity(orc, cfg, 1 << 13, 1 << 10, seed=4)
+    assert lt[2] > 0

@@ -152,3 +152,20 @@ def test_tc_multiresolution(orc, name, w, nh):
     assert abs(gl - Le) <= EMU_TOL * Le, (gl, Le)
     assert np.linalg.norm(gg - ge) <= EMU_TOL * np.linalg.norm(ge)
     s.close()
+
+
+def test_tc_grid_levelset_w256(orc):
+    """bf16 W = 256 (K3w) on config 4's 32-sphere union sampled on a 128^3 grid."""
+    cfg = inputs.with_grid(inputs.config("c4"), 128)
+    n, nb = 1 << 12, 1 << 9
+    s = nbm.Solver(cfg, 0, max_points=n)
+    pb, ar = orc.from_config(cfg)
+    pts = orc.sample(0, 3, 0, 0, n, cfg["H"])
+    bpts = orc.sample(1, 3, 0, 0, nb, cfg["H"])
+    th = orc.init_params(ar, 0)
+    L, _, g, _ = orc.loss_grad(pb, ar, th, pts, bpts, cfg["h"])
+    Le, _, ge, _ = orc.loss_grad(pb, ar, th, pts, bpts, cfg["h"], mode=orc.MODE_BF16)
+    gl, gg = _run(s, _dev(th), _dev(pts), _dev(bpts))
+    assert abs(gl - L) <= TOL * L and np.linalg.norm(gg - g) <= TOL * np.linalg.norm(g)
+    assert abs(gl - Le) <= EMU_TOL * Le and np.linalg.norm(gg - ge) <= EMU_TOL * np.linalg.norm(ge)
+    s.close()

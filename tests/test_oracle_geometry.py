@@ -220,3 +220,98 @@ def test_boundary_data_is_side_exact_solution(orc):
     cfg3 = inputs.config("c3")
     pb3, _ = orc.from_config(cfg3)
     assert orc.g(pb3, x) == 0.0                                           # G13: u = 0 on faces
+
+
+# ---- sampled level set ("a separate coarse mesh") ----
+
+def _grid_cfg(nc, base=None):
+    return inputs.with_grid(_sphere_cfg() if base is None else base, nc)
+
+
+def test_grid_reproduces_nodes_and_linear_fields(orc):
+    """Trilinear interpolation equals the nodal values at the nodes and reproduces a linear
+    level set exactly (its fp32 nodes are exact here); the S:133 example "linear phi,
+    a=(0,0,0), b=(1,0,0) -> theta = x0" holds for the linear-interpolant crossing (S:125)."""
+    cfg = _sphere_cfg()
+    cfg.update(ls_kind=inputs.LS_PLANE, plane=((1.0, 0.0, 0.0), 0.125))
+    g = _grid_cfg(32, cfg)
+    pb, _ = orc.from_config(g)
+    nodes = np.asarray(g["grid"]).reshape(33, 33, 33)
+    for i, j, k in [(0, 0, 0), (32, 32, 32), (5, 17, 29), (31, 0, 12)]:
+        x = [-1 + i / 16, -1 + j / 16, -1 + k / 16]
+        assert orc.phi(pb, x) == float(nodes[k, j, i])
+    pts = inputs.random_lattice_points(500, inputs.h_lattice(1 / 64), 3).astype(np.float64)
+    for x in pts:
+        assert abs(orc.phi(pb, x) - (x[0] - 0.125)) <= 1e-15
+    th, xg, n = orc.crossing(pb, [0, 0, 0], [1, 0, 0])
+    assert th == 0.125 and np.allclose(n, [1, 0, 0], atol=1e-12)
+
+
+def test_grid_sphere_interpolation_error_is_second_order(orc):
+    """S:82 example: the sampled sphere's |phi_sampled - phi| <= C hc^2 at random points
+    (C measured; away from the centre where the Hessian of |x| blows up), and the error falls
+    by ~4x per halving of hc (trilinear interpolation is second order)."""
+    pb0, _ = orc.from_config(_sphere_cfg())
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-0.95, 0.95, size=(1000, 3))
+    x = x[np.linalg.norm(x, axis=1) > 0.25]
+    errs = []
+    for nc in (16, 32, 64):
+        pb, _ = orc.from_config(_grid_cfg(nc))
+        e = max(abs(orc.phi(pb, p) - orc.phi(pb0, p)) for p in x)
+        hc = 2.0 / nc
+        assert e <= 1.0 * hc * hc
+        errs.append(e)
+    assert 3.0 < errs[0] / errs[1] < 5.5 and 3.0 < errs[1] / errs[2] < 5.5
+
+
+def test_grid_crossings_and_normals(orc):
+    """theta(a->b) + theta(b->a) = 1, crossing locations within C hc^2 of |x| = 0.5
+    (Sampled), normals of the sampled sphere ~ radial (step hc/2)."""
+    nc = 64
+    pb, _ = orc.from_config(_grid_cfg(nc))
+    rng = np.random.default_rng(11)
+    n_cross = 0
+    for _ in range(3000):
+        a = rng.uniform(-0.8, 0.8, 3)
+        b = a + rng.normal(size=3) * 0.05
+        c1 = orc.crossing(pb, a, b)
+        if c1 is None:
+            continue
+        c2 = orc.crossing(pb, b, a)
+        assert abs(c1[0] + c2[0] - 1.0) <= 1e-12
+        # the linear-interpolant root is off the curved interface by <= |b-a|^2 max|phi''|/8
+        # along the arm (phi'' <= 1/r = 2), plus the trilinear error
+        assert abs(np.linalg.norm(c1[1]) - 0.5) <= 2.0 * (2.0 / nc) ** 2 + np.dot(b - a, b - a) / 4
+        assert np.dot(c1[2], c1[1] / np.linalg.norm(c1[1])) > 0.99
+        n_cross += 1
+    assert n_cross > 20
+    assert np.allclose(orc.normal(pb, [0.5, 0, 0]), [1, 0, 0], atol=1e-3)
+    assert np.allclose(orc.normal(pb, [0, -0.5, 0]), [0, -1, 0], atol=1e-3)
+
+
+def test_grid_jump_suite_exact(orc):
+    """The S:294 jump suite on a sampled plane: with dyadic theta and h the plane's fp32 nodes
+    are exact, the interpolant is the plane itself, and every crossed row reproduces the exact
+    piecewise-linear solution (r ~ round-off), so assembly on the Sampled variant is pinned."""
+    import test_oracle_assembly as A
+    h = 1.0 / 16
+    ex = A.SPEC["jump_suite"]
+    worst, n = 0.0, 0
+    for th in (0.25, 0.5, 0.75):
+        for bm, bp, a, b in [(1.0, 3.0, 2.0, -1.0), (0.5, 1.0, -1.0, 2.0), (3.0, 0.5, 0.0, 2.0), (1.0, 1.0, 2.0, 0.0)]:
+            for axis, orient, cs in [(0, 1, 0), (1, -1, 1), (2, 1, 1), (0, -1, 0)]:
+                pb, poly, p = A._plane_case(orc, axis, orient, th, bm, bp, a, b, cs, h=h)
+                nvec = [0.0, 0.0, 0.0]
+                nvec[axis] = float(orient)
+                x0 = float(np.float32(p[axis] + (orient if cs == 0 else -orient) * th * np.float32(h)))
+                base = A._poly_cfg(beta=(bm, bp))
+                base.update(ls_kind=inputs.LS_PLANE, plane=(nvec, float(orient) * x0))
+                g = inputs.with_grid(base, 32)
+                pbg, _ = orc.from_config(g, poly=poly)
+                row = orc.assemble(pbg, p, h)
+                assert row.side == cs and row.crossed and row.n_crossed_arms == 1
+                raw, scale = A._raw(row, A._poly_u(poly))
+                worst = max(worst, abs(raw / row.d))
+                n += 1
+    assert n == 48 and worst < ex["tol"]
