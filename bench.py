@@ -28,6 +28,9 @@ sys.path.insert(0, ROOT)
 from paper_2210_14907_b200 import dp, inputs  # noqa: E402
 
 FP32_FFMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FFMA lanes x 2 x max clock
+# measured on this pool's B200 (scripts/ffma_peak.cu, 1965 MHz): FFMA with three register
+# operands, the form a GEMM issues, reaches 57.0 TFLOP/s (the immediate form 71.0)
+FP32_FFMA_3REG_MEASURED_TFLOPS = 57.0
 
 
 def mlp_macs(sizes):
@@ -170,6 +173,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA-graph replays")
+    ap.add_argument("--eval", action="store_true", help="also time inference (nbm_eval) at the step's points")
     ap.add_argument("--grid", type=int, default=None,
                     help="replace the level set by its samples on an Nc^3 grid (S:82 Sampled variant, P:60)")
     ap.add_argument("--levels", type=int, default=1,
@@ -301,6 +305,25 @@ def main():
             e_ms = t.item()
         e2e = {"value": Ng * args.steps / (e_ms / 1e3), "unit": "pts/s",
                "h2d_bytes_per_step": 12 * (N + Nb), "d2h_bytes_per_step": 4}
+    # ---- inference at scale: nbm_eval of the surrogate pair at the
+    # step's interior points (side by phi, one evaluation per point), device-resident inputs ----
+    infer = None
+    if args.eval:
+        u = torch.empty(N, device="cuda")
+        for _ in range(args.warmup):
+            s.eval(pts, out=u)
+        ie = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        for k in range(args.steps):
+            flush.zero_()
+            ie[k][0].record(stream)
+            s.eval(pts, out=u)
+            ie[k][1].record(stream)
+        barrier()
+        i_ms = sum(a.elapsed_time(b) for a, b in ie) / args.steps
+        fwd_flop = 2.0 * mlp_macs(cfg["sizes"])[0] * N
+        infer = {"pts_per_sec": N / (i_ms / 1e3), "ms_per_call": i_ms, "points": N,
+                 "tflops": fwd_flop / (i_ms / 1e3) / 1e12}
     st = s.status()
     if st != 0:
         raise RuntimeError(f"device status {st} after the timed region")
@@ -339,6 +362,9 @@ def main():
                    "global_points": Ng, "mlp": "x".join(map(str, cfg["sizes"])), "n_nets": cfg["n_nets"],
                    "h": cfg["h"], "levels": args.levels, "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     **({"measured_ffma_3reg_peak": FP32_FFMA_3REG_MEASURED_TFLOPS,
+                         "frac_of_measured_ffma": achieved / FP32_FFMA_3REG_MEASURED_TFLOPS}
+                        if cfg["prec"] == inputs.PREC_FP32 else {}),
                      "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name(cfg) + " fused fwd/residual/bwd",
                      "flop_per_launch": flop_launch, "avg_launch_ms": mlp_avg_s * 1e3,
                      "share_of_step": mlp_ms / eager_ms, "peak_src": peak_note},
@@ -347,6 +373,8 @@ def main():
         "clocks": clocks,
         "e2e": e2e,
     }
+    if infer is not None:
+        line["inference"] = infer
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, levels=args.levels)
     print(json.dumps(line), flush=True)

@@ -169,3 +169,19 @@ def test_tc_grid_levelset_w256(orc):
     assert abs(gl - L) <= TOL * L and np.linalg.norm(gg - g) <= TOL * np.linalg.norm(g)
     assert abs(gl - Le) <= EMU_TOL * Le and np.linalg.norm(gg - ge) <= EMU_TOL * np.linalg.norm(ge)
     s.close()
+
+
+def test_tc_eval_w256(orc):
+    """nbm_eval on the W = 256 pair kernel (K3w forward-only path) at the bf16 bar."""
+    cfg = inputs.config("c4")
+    n = 3000
+    s = nbm.Solver(cfg, 0, max_points=n)
+    pb, ar = orc.from_config(cfg)
+    th = orc.init_params(ar, 2)
+    pts = np.concatenate([orc.sample(0, 6, 0, 0, n - 100, cfg["H"]), orc.sample(1, 6, 0, 0, 100, cfg["H"])])
+    s.theta.copy_(_dev(th))
+    u = s.eval(_dev(pts)).double().cpu().numpy()
+    want = orc.evaluate(pb, ar, th, pts)
+    assert np.abs(u - want).max() <= TOL * np.abs(want).max()
+    assert s.status() == 0
+    s.close()
