@@ -27,6 +27,7 @@ sys.path.insert(0, ROOT)
 
 from paper_2210_14907_b200 import dp, inputs  # noqa: E402
 
+METRIC = "collocation-pt loss+grad evals/sec (full training step)"
 FP32_FFMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FFMA lanes x 2 x max clock
 # measured on this pool's B200 (scripts/ffma_peak.cu, 1965 MHz): FFMA with three register
 # operands, the form a GEMM issues, reaches 57.0 TFLOP/s (the immediate form 71.0)
@@ -143,18 +144,24 @@ def run_reference(args, cfg, rank, world):
         pts = oracle.sample(0, 0, it, 0, n, cfg["H"])
         bpts = oracle.sample(1, 0, it, 0, nb, cfg["H"])
         t0 = time.perf_counter()
-        _, _, g, _ = oracle.loss_grad(pb, ar, th, pts, bpts, cfg["h"], n_glob=n, nb_glob=nb)
+        if args.levels == 1:
+            _, _, g, _ = oracle.loss_grad(pb, ar, th, pts, bpts, cfg["h"], n_glob=n, nb_glob=nb)
+        else:
+            _, g = oracle.loss_grad_ml(pb, ar, th, pts, bpts, cfg["h"], args.levels, n_glob=n, nb_glob=nb)
         th, m, v = oracle.adam(th, m, v, g, it + 1, lr=cfg["lr"])
         if it >= args.warmup:
             times.append(time.perf_counter() - t0)
     tot = sum(times)
     val = n * len(times) / tot
-    line = {"metric": "collocation-pt loss+grad evals/sec", "value": val, "unit": "pts/s",
+    line = {"metric": METRIC, "value": val, "unit": "pts/s",
             "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["label"], "points_per_step": n, "boundary_per_step": nb,
-                       "note": "bounded sample of the workload; oracle on host cores"},
+            "config": {"workload": cfg["label"], "points_per_gpu": cfg["N"], "boundary_per_gpu": cfg["Nb"],
+                       "mlp": "x".join(map(str, cfg["sizes"])), "n_nets": cfg["n_nets"], "h": cfg["h"],
+                       "levels": args.levels, "parallelism": "host cores",
+                       "sample_points_per_step": n, "sample_boundary_per_step": nb,
+                       "note": "the fp64 oracle on a bounded sample of the workload per step (host cores)"},
             "cpu_baseline": {"value": val, "unit": "pts/s", "cores": oracle.num_threads(),
                              "kind": "oracle", "sample": f"{n} + {nb} points per step"},
             "e2e": {"value": val, "unit": "pts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -352,7 +359,7 @@ def main():
         traffic = json.load(open(tp)).get("bytes_per_launch")
     val = Ng * args.steps / (tot_ms / 1e3)
     line = {
-        "metric": "collocation-pt loss+grad evals/sec (full training step)",
+        "metric": METRIC,
         "value": val, "unit": "pts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_ms / args.steps, "steps_per_sec": 1e3 * args.steps / tot_ms,
         "loss_grad_pts_per_sec": Ng * calls / args.levels / (lg_ms_max / 1e3) if calls else None,
