@@ -54,9 +54,18 @@ extern "C" {
 #define NBM_SRC_SINE3PI  0  /* u = sin(pi x) sin(pi y) sin(pi z) on both sides (config 1) */
 #define NBM_SRC_PAIR     1  /* u- = e^x cos(y) z, u+ = sin(x+y+z) (configs 2, 4, 5; G12) */
 #define NBM_SRC_GAUSS    2  /* f = sum_k q_k N(x; c_k, s^2 I), alpha = sigma = g = 0 (config 3; G13) */
+#define NBM_SRC_PAPER41  4  /* the paper's 4.1 benchmark: u- = e^z, u+ = cos(x) sin(y),
+                             * f = k u - div(mu grad u) with the problem's mu+-, alpha = [u],
+                             * sigma = [mu d_n u], g = u of the side */
+
+/* diffusion coefficient mu+-(x) */
+#define NBM_MU_CONST     0  /* beta_minus / beta_plus */
+#define NBM_MU_PAPER41   1  /* mu- = y^2 ln(x+2) + 4, mu+ = e^{-z} */
+#define NBM_MU_LINEAR    2  /* mu_s(x) = m0 + mx x + my y + mz z (mu_lin[s]); > 0 on the box */
 
 #define NBM_ACT_TANH  0
 #define NBM_ACT_SILU  1
+#define NBM_ACT_SINE  2     /* P:68 "sine-activated neurons"; init +-sqrt(6/fan_in) */
 #define NBM_PREC_FP32 0     /* IEEE fp32 arithmetic throughout (G15) */
 #define NBM_PREC_BF16 1     /* bf16 tensor-core hidden GEMMs, fp32 accumulate (G16) */
 
@@ -96,6 +105,10 @@ typedef struct nbm_problem {
   const float* charge_centers;   /* host, [n_charges][3] */
   float charge_sigma;            /* > 0 */
   float lambda_b;                /* boundary weight, >= 0 */
+  int mu_kind;                   /* NBM_MU_*: variable coefficients are evaluated at the arm's face
+                                  * midpoint (uncrossed arms) and at x_Gamma (crossed arms,
+                                  * S:257); supported by the fp32 kernel (W <= 64) */
+  float mu_lin[2][4];            /* NBM_MU_LINEAR: m0, mx, my, mz for Omega-, Omega+ */
 } nbm_problem;
 
 /* MLP surrogate (P:60 two networks, one per side).  sizes = [3, W, ..., W, 1]

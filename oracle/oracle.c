@@ -275,6 +275,30 @@ int orc_crossing(const orc_problem* pb, const double a[3], const double b[3],
   return orc_normal(pb, xg, nrm) < 0 ? -2 : 1;
 }
 
+/* diffusion coefficient of side s at x and its gradient (P:68 for the 4.1 fields) */
+double orc_mu(const orc_problem* pb, int s, const double x[3], double grad[3]) {
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0, m;
+  if (pb->mu_kind == ORC_MU_PAPER41) {
+    if (s == 0) {                                  /* mu- = y^2 ln(x + 2) + 4 */
+      double lx = log(x[0] + 2.0);
+      m = x[1] * x[1] * lx + 4.0;
+      g0 = x[1] * x[1] / (x[0] + 2.0);
+      g1 = 2.0 * x[1] * lx;
+    } else {                                       /* mu+ = e^{-z} */
+      m = exp(-x[2]);
+      g2 = -m;
+    }
+  } else if (pb->mu_kind == ORC_MU_LINEAR) {
+    const double* c = pb->mu_lin + 4 * s;
+    m = c[0] + (c[1] * x[0] + c[2] * x[1]) + c[3] * x[2];
+    g0 = c[1]; g1 = c[2]; g2 = c[3];
+  } else {
+    m = pb->beta[s];
+  }
+  if (grad) { grad[0] = g0; grad[1] = g1; grad[2] = g2; }
+  return m;
+}
+
 /* ------------------------------------------------------------------------ */
 /* problem data: k u - div(beta grad u) = f, [u] = alpha, [beta d_n u] =     */
 /* sigma; manufactured families of BASELINE.json configs           */
@@ -299,6 +323,17 @@ int orc_exact(const orc_problem* pb, int side, const double x[3], double* u, dou
         if (g) { double c = cos(s); g[0] = c; g[1] = c; g[2] = c; }
       }
       return 0;
+    case ORC_SRC_PAPER41:                          /* u- = e^z, u+ = cos(x) sin(y) */
+      if (side == 0) {
+        double e = exp(x[2]);
+        *u = e;
+        if (g) { g[0] = 0.0; g[1] = 0.0; g[2] = e; }
+      } else {
+        double cx = cos(x[0]), sx = sin(x[0]), cy = cos(x[1]), sy = sin(x[1]);
+        *u = cx * sy;
+        if (g) { g[0] = -sx * sy; g[1] = cx * cy; g[2] = 0.0; }
+      }
+      return 0;
     case ORC_SRC_POLY2: {                          /* test family: c + g.x + x^T A x per side */
       const double* p = pb->poly + 10 * side;
       double A[3][3] = {{p[4], p[5], p[6]}, {p[5], p[7], p[8]}, {p[6], p[8], p[9]}};
@@ -312,8 +347,27 @@ int orc_exact(const orc_problem* pb, int side, const double x[3], double* u, dou
   return -1;                                       /* no exact solution (config 3) */
 }
 
+/* Laplacian of the manufactured solutions */
+static double lap_exact(const orc_problem* pb, int side, const double x[3]) {
+  double u;
+  switch (pb->source) {
+    case ORC_SRC_SINE3PI: orc_exact(pb, side, x, &u, NULL); return -3.0 * M_PI * M_PI * u;
+    case ORC_SRC_PAIR: return side == 0 ? 0.0 : -3.0 * sin(x[0] + x[1] + x[2]);
+    case ORC_SRC_POLY2: { const double* p = pb->poly + 10 * side; return 2.0 * (p[4] + p[7] + p[9]); }
+    case ORC_SRC_PAPER41: return side == 0 ? exp(x[2]) : -2.0 * cos(x[0]) * sin(x[1]);
+  }
+  return 0.0;
+}
+
 double orc_f(const orc_problem* pb, int side, const double x[3]) {
   double ks = pb->k[side], bs = pb->beta[side], u;
+  if (pb->mu_kind != ORC_MU_CONST || pb->source == ORC_SRC_PAPER41) {
+    /* f = k u - div(mu grad u) = k u - mu Lap u - grad mu . grad u */
+    double gu[3], gm[3];
+    if (orc_exact(pb, side, x, &u, gu) < 0) return 0.0;
+    double m = orc_mu(pb, side, x, gm);
+    return ks * u - m * lap_exact(pb, side, x) - ((gm[0] * gu[0] + gm[1] * gu[1]) + gm[2] * gu[2]);
+  }
   switch (pb->source) {
     case ORC_SRC_SINE3PI:                          /* -Lap u = 3 pi^2 u */
       orc_exact(pb, side, x, &u, NULL);
@@ -357,7 +411,7 @@ double orc_sigma(const orc_problem* pb, const double x[3], const double n[3]) {
   orc_exact(pb, 1, x, &up, gp);
   double dp = gp[0] * n[0] + gp[1] * n[1] + gp[2] * n[2];
   double dm = gm[0] * n[0] + gm[1] * n[1] + gm[2] * n[2];
-  return pb->beta[1] * dp - pb->beta[0] * dm;
+  return orc_mu(pb, 1, x, NULL) * dp - orc_mu(pb, 0, x, NULL) * dm;
 }
 
 /* Dirichlet data: the manufactured u of the side containing x (G10) */
@@ -394,8 +448,12 @@ int orc_assemble(const orc_problem* pb, const float p[3], float hf, int sign_mut
     double qd[3] = {q[0], q[1], q[2]};
     int sq = orc_side(pb, qd);
     row->mask |= sq << j;
+    /* mu_s at the arm's face midpoint p + (h/2) e (beta_s when mu is constant) */
+    double xf[3] = {pd[0], pd[1], pd[2]};
+    xf[dd] = pd[dd] + ARM_SGN[j] * 0.5 * h;
+    const double mf = pb->mu_kind == ORC_MU_CONST ? bs : orc_mu(pb, s, xf, NULL);
     if (sq == s) {                                     /* (a) uncrossed arm */
-      row->coef[j] = -bs / h2; c0 += bs / h2; row->tag[j] = s;
+      row->coef[j] = -mf / h2; c0 += mf / h2; row->tag[j] = s;
       continue;
     }
     double th, xg[3], n[3];
@@ -403,11 +461,13 @@ int orc_assemble(const orc_problem* pb, const float p[3], float hf, int sign_mut
     if (rc < 0) return -2;
     row->theta[j] = th;
     if (th < 1e-6 || th > 1.0 - 1e-6) {                /* theta snapping (G6) */
-      row->coef[j] = -bs / h2; c0 += bs / h2; row->tag[j] = s; row->n_snapped++;
+      row->coef[j] = -mf / h2; c0 += mf / h2; row->tag[j] = s; row->n_snapped++;
       continue;
     }
-    /* (b) crossed arm, S:257 with the sign reading G3 */
-    double muh = bs * bo / (th * bo + (1.0 - th) * bs);
+    /* (b) crossed arm, S:257 with the sign reading G3; mu_near = mu_s(x_G), mu_far = mu_s'(x_G) */
+    double mn = bs, mfar = bo;
+    if (pb->mu_kind != ORC_MU_CONST) { mn = orc_mu(pb, s, xg, NULL); mfar = orc_mu(pb, so, xg, NULL); }
+    double muh = mn * mfar / (th * mfar + (1.0 - th) * mn);
     double sg = (s == 0) ? 1.0 : -1.0;
     double e[3] = {0, 0, 0}; e[dd] = ARM_SGN[j];
     double a = sg * orc_alpha(pb, xg);
@@ -415,7 +475,7 @@ int orc_assemble(const orc_problem* pb, const float p[3], float hf, int sign_mut
     c0 += muh / h2;
     row->coef[j] = -muh / h2;
     row->tag[j] = so;
-    corr += muh * (a / h2 + (1.0 - th) * ba / (h * bo));
+    corr += muh * (a / h2 + (1.0 - th) * ba / (h * mfar));
     row->n_crossed_arms++;
   }
   row->coef[0] = c0;
@@ -456,14 +516,15 @@ int64_t orc_param_count(const orc_arch* a) {
   return p * a->n_nets;
 }
 
-/* G11: Glorot-uniform +-sqrt(6/(fan_in+fan_out)), zero biases; Philox stream 2 */
+/* G11: Glorot-uniform +-sqrt(6/(fan_in+fan_out)), zero biases; Philox stream 2.  Sine nets
+ * (S:175): +-sqrt(6/fan_in). */
 void orc_init_params(const orc_arch* a, uint64_t seed, float* theta) {
   uint64_t e = 0;
   int64_t off = 0;
   for (int net = 0; net < a->n_nets; ++net)
     for (int l = 1; l < a->n_layers; ++l) {
       int fi = a->sizes[l - 1], fo = a->sizes[l];
-      float amp = sqrtf(6.0f / (float)(fi + fo));
+      float amp = a->act == ORC_ACT_SINE ? sqrtf(6.0f / (float)fi) : sqrtf(6.0f / (float)(fi + fo));
       for (int64_t k = 0; k < (int64_t)fi * fo; ++k, ++e) {
         uint32_t w[4];
         philox_block(seed, e >> 2, 0u, 2u, w);

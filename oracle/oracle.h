@@ -25,7 +25,10 @@ extern "C" {
 /* level-set kinds (configs in BASELINE.json) */
 enum { ORC_LS_NONE = 0, ORC_LS_SPHERES = 1, ORC_LS_STAR = 2, ORC_LS_PLANE = 3, ORC_LS_GRID = 4 };
 /* data families: manufactured or physical (BASELINE.json configs 1-4) */
-enum { ORC_SRC_SINE3PI = 0, ORC_SRC_PAIR = 1, ORC_SRC_GAUSS = 2, ORC_SRC_POLY2 = 3 };
+enum { ORC_SRC_SINE3PI = 0, ORC_SRC_PAIR = 1, ORC_SRC_GAUSS = 2, ORC_SRC_POLY2 = 3, ORC_SRC_PAPER41 = 4 };
+/* diffusion coefficient mu+-(x) ("k u - div(mu grad u) = f"): constants beta+-, the
+ * paper's 4.1 fields (P:68 mu- = y^2 ln(x+2) + 4, mu+ = e^{-z}), or linear test fields */
+enum { ORC_MU_CONST = 0, ORC_MU_PAPER41 = 1, ORC_MU_LINEAR = 2 };
 /* activations */
 enum { ORC_ACT_TANH = 0, ORC_ACT_SILU = 1, ORC_ACT_SINE = 2 };
 /* arithmetic modes of the MLP: exact fp64 (the oracle proper) and two
@@ -53,6 +56,8 @@ typedef struct {
   double lambda_b;               /* boundary weight */
   int grid_n;                    /* ORC_LS_GRID: Nc cells per axis (S:82 Sampled variant) */
   const double* grid_phi;        /* [(Nc+1)^3] nodal values over [-1,1]^3, x fastest */
+  int mu_kind;                   /* ORC_MU_* */
+  const double* mu_lin;          /* ORC_MU_LINEAR: [2][4] m0, mx, my, mz per side */
 } orc_problem;
 
 typedef struct {
@@ -103,6 +108,7 @@ int orc_normal(const orc_problem* pb, const double x[3], double nrm[3]);
 /* ---- problem data (P:40-41 jump problem, configs) ---- */
 int orc_exact(const orc_problem* pb, int side, const double x[3], double* u, double grad[3]);
 double orc_f(const orc_problem* pb, int side, const double x[3]);
+double orc_mu(const orc_problem* pb, int side, const double x[3], double grad[3]);
 double orc_alpha(const orc_problem* pb, const double x[3]);
 double orc_sigma(const orc_problem* pb, const double x[3], const double n[3]);
 double orc_g(const orc_problem* pb, const double x[3]);

@@ -43,7 +43,8 @@ class Problem(C.Structure):
                 ("source", C.c_int), ("n_charges", C.c_int),
                 ("q", C.POINTER(C.c_double)), ("charge_centers", C.POINTER(C.c_double)),
                 ("charge_sigma", C.c_double), ("poly", C.POINTER(C.c_double)),
-                ("lambda_b", C.c_double), ("grid_n", C.c_int), ("grid_phi", C.POINTER(C.c_double))]
+                ("lambda_b", C.c_double), ("grid_n", C.c_int), ("grid_phi", C.POINTER(C.c_double)),
+                ("mu_kind", C.c_int), ("mu_lin", C.POINTER(C.c_double))]
 
 
 class Arch(C.Structure):
@@ -81,6 +82,8 @@ def lib():
         for fn in ("orc_f",):
             getattr(L, fn).restype = C.c_double
             getattr(L, fn).argtypes = [P(Problem), C.c_int, P(C.c_double)]
+        L.orc_mu.restype = C.c_double
+        L.orc_mu.argtypes = [P(Problem), C.c_int, P(C.c_double), P(C.c_double)]
         L.orc_alpha.restype = C.c_double
         L.orc_alpha.argtypes = [P(Problem), P(C.c_double)]
         L.orc_sigma.restype = C.c_double
@@ -171,6 +174,11 @@ class OracleProblem:
             self._keep.append(pa)
             p.poly = _ptr(pa, C.c_double)
         p.lambda_b = f32(cfg["lambda_b"])
+        p.mu_kind = int(cfg.get("mu_kind", 0))
+        if cfg.get("mu_lin") is not None:
+            ml = _f64(np.asarray(cfg["mu_lin"], np.float32).reshape(2, 4))
+            self._keep.append(ml)
+            p.mu_lin = _ptr(ml, C.c_double)
         if cfg.get("grid") is not None:   # sampled level set: fp32 nodal values (as the CUDA path gets)
             gphi = _f64(np.asarray(cfg["grid"], np.float32).reshape(-1))
             self._keep.append(gphi)
@@ -259,6 +267,13 @@ def exact(pb, s, x):
 
 def f(pb, s, x) -> float:
     return lib().orc_f(pb.ref, s, _ptr(_f64(x), C.c_double))
+
+
+def mu(pb, s, x):
+    """(mu_s(x), grad mu_s(x)) of the problem's diffusion coefficient"""
+    g = np.zeros(3)
+    m = lib().orc_mu(pb.ref, s, _ptr(_f64(x), C.c_double), _ptr(g, C.c_double))
+    return float(m), g
 
 
 def alpha(pb, x) -> float:

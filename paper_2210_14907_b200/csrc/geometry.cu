@@ -228,7 +228,43 @@ __device__ double d_crossing_theta(const DevProblem& P, const double a[3], const
 
 // ------------------------------------------------------------------ data
 // manufactured solutions; returns false for the Gaussian source (no exact solution)
+// diffusion coefficient of side s at x and its gradient (P:68 for the 4.1 fields)
+__device__ double d_mu(const DevProblem& P, int s, const double x[3], double grad[3]) {
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0, m;
+  if (P.mu_kind == NBM_MU_PAPER41) {
+    if (s == 0) {   // mu- = y^2 ln(x + 2) + 4
+      const double lx = log(x[0] + 2.0);
+      m = x[1] * x[1] * lx + 4.0;
+      g0 = x[1] * x[1] / (x[0] + 2.0);
+      g1 = 2.0 * x[1] * lx;
+    } else {        // mu+ = e^{-z}
+      m = exp(-x[2]);
+      g2 = -m;
+    }
+  } else if (P.mu_kind == NBM_MU_LINEAR) {
+    const double* c = P.mu_lin[s];
+    m = c[0] + (c[1] * x[0] + c[2] * x[1]) + c[3] * x[2];
+    g0 = c[1]; g1 = c[2]; g2 = c[3];
+  } else {
+    m = P.beta[s];
+  }
+  if (grad) { grad[0] = g0; grad[1] = g1; grad[2] = g2; }
+  return m;
+}
+
 __device__ bool d_exact(const DevProblem& P, int s, const double x[3], double* u, double g[3]) {
+  if (P.source == NBM_SRC_PAPER41) {   // u- = e^z, u+ = cos(x) sin(y)
+    if (s == 0) {
+      const double e = exp(x[2]);
+      *u = e;
+      g[0] = 0.0; g[1] = 0.0; g[2] = e;
+    } else {
+      const double cx = cos(x[0]), sx = sin(x[0]), cy = cos(x[1]), sy = sin(x[1]);
+      *u = cx * sy;
+      g[0] = -sx * sy; g[1] = cx * cy; g[2] = 0.0;
+    }
+    return true;
+  }
   if (P.source == NBM_SRC_SINE3PI) {
     const double pi = 3.141592653589793;
     double sx = sin(pi * x[0]), sy = sin(pi * x[1]), sz = sin(pi * x[2]);
@@ -253,8 +289,22 @@ __device__ bool d_exact(const DevProblem& P, int s, const double x[3], double* u
   return false;
 }
 
+__device__ double d_lap_exact(const DevProblem& P, int s, const double x[3]) {
+  if (P.source == NBM_SRC_PAPER41) return s == 0 ? exp(x[2]) : -2.0 * cos(x[0]) * sin(x[1]);
+  if (P.source == NBM_SRC_PAIR) return s == 0 ? 0.0 : -3.0 * sin(x[0] + x[1] + x[2]);
+  const double pi = 3.141592653589793;   // SINE3PI
+  return -3.0 * pi * pi * sin(pi * x[0]) * sin(pi * x[1]) * sin(pi * x[2]);
+}
+
 __device__ double d_source(const DevProblem& P, int s, const double x[3]) {
   double u, g[3];
+  if (P.mu_kind != NBM_MU_CONST || P.source == NBM_SRC_PAPER41) {
+    // f = k u - div(mu grad u) = k u - mu Lap u - grad mu . grad u
+    if (!d_exact(P, s, x, &u, g)) return 0.0;
+    double gm[3];
+    const double m = d_mu(P, s, x, gm);
+    return P.k[s] * u - m * d_lap_exact(P, s, x) - ((gm[0] * g[0] + gm[1] * g[1]) + gm[2] * g[2]);
+  }
   if (P.source == NBM_SRC_SINE3PI) {
     d_exact(P, s, x, &u, g);
     const double pi = 3.141592653589793;
@@ -282,7 +332,8 @@ __global__ void __launch_bounds__(kClsBlock) k_classify(
     const DevProblem* __restrict__ Pp, const float* __restrict__ pts, int64_t n,
     const float* __restrict__ bpts, int64_t nb, float hf, double d_minus, double d_plus,
     unsigned terms, int eval_only, uint8_t* __restrict__ cls, float* __restrict__ aux,
-    int* __restrict__ blk_counts, int* __restrict__ err, uint8_t* __restrict__ mask_out) {
+    int* __restrict__ blk_counts, int* __restrict__ err, uint8_t* __restrict__ mask_out,
+    float* __restrict__ pcoef) {
   const DevProblem& P = *Pp;
   __shared__ int cnt[kNumCls];
   if (threadIdx.x < kNumCls) cnt[threadIdx.x] = 0;
@@ -318,7 +369,24 @@ __global__ void __launch_bounds__(kClsBlock) k_classify(
         unsigned bit = (c == kClsUnxMinus) ? NBM_TERM_UNX_MINUS
                      : (c == kClsUnxPlus) ? NBM_TERM_UNX_PLUS : NBM_TERM_CROSSED;
         if (!(terms & bit)) c = kClsSkip;
-        else if (c != kClsCrossed) a = (float)(d_source(P, s, pd) / (s ? d_plus : d_minus));
+        else if (c != kClsCrossed) {
+          if (P.mu_kind == NBM_MU_CONST) {
+            a = (float)(d_source(P, s, pd) / (s ? d_plus : d_minus));
+          } else {   // variable mu: mu_s at the six face midpoints, d = k_s + sum mu_j / h^2
+            const double h = hf, h2 = h * h;
+            double mj[6], d = P.k[s];
+#pragma unroll 1
+            for (int j = 1; j <= 6; ++j) {
+              const int dd = (j - 1) >> 1;
+              double xf[3] = {pd[0], pd[1], pd[2]};
+              xf[dd] = pd[dd] + ((j & 1) ? 0.5 * h : -0.5 * h);
+              mj[j - 1] = d_mu(P, s, xf, nullptr);
+              d += mj[j - 1] / h2;
+            }
+            for (int j = 0; j < 6; ++j) pcoef[6 * it + j] = (float)((-mj[j] / h2) / d);
+            a = (float)(d_source(P, s, pd) / d);
+          }
+        }
       }
     } else {
       const float* p = eval_only ? pts + 3 * it : bpts + 3 * (it - n);
@@ -444,7 +512,7 @@ cudaError_t launch_classify(const nbm_handle* h, const float* pts, int64_t n, co
   float hf = (float)((double)H / kLattice);
   k_classify<<<nblk, kClsBlock, 0, s>>>(h->d_problem, pts, n, bpts, nb, hf, d_minus, d_plus, terms,
                                         eval_only ? 1 : 0, w.cls, w.aux_tmp, w.blk_counts, w.err,
-                                        mask_out);
+                                        mask_out, w.pcoef);
   k_scan<<<1, 1024, 0, s>>>(w.blk_counts, nblk, w.blk_offsets, w.counts);
   k_scatter<<<nblk, kClsBlock, 0, s>>>(w.cls, w.aux_tmp, n, total, eval_only ? 1 : 0,
                                        w.blk_offsets, w.list, w.list_aux);
@@ -491,11 +559,19 @@ __global__ void __launch_bounds__(128) k_assemble_crossed(
           else atomicOr(err, kErrDegenerate);
         }
       }
-      if (!crossed) {                             // (a) uncrossed arm
-        coef = -bs / h2;
-        cc = bs / h2;
+      if (!crossed) {                             // (a) uncrossed arm: mu_s at the face midpoint
+        double mf = bs;
+        if (P.mu_kind != NBM_MU_CONST) {
+          double xf[3] = {pd[0], pd[1], pd[2]};
+          xf[dd] = pd[dd] + ((j & 1) ? 0.5 * h : -0.5 * h);
+          mf = d_mu(P, s, xf, nullptr);
+        }
+        coef = -mf / h2;
+        cc = mf / h2;
       } else {                                    // (b) crossed arm, S:257 with rhs = f - corrections (G3)
-        const double muh = bs * bo / (th * bo + (1.0 - th) * bs);
+        double mn = bs, mfar = bo;                // mu_near = mu_s(x_G), mu_far = mu_s'(x_G)
+        if (P.mu_kind != NBM_MU_CONST) { mn = d_mu(P, s, xg, nullptr); mfar = d_mu(P, so, xg, nullptr); }
+        const double muh = mn * mfar / (th * mfar + (1.0 - th) * mn);
         const double sg = (s == 0) ? 1.0 : -1.0;
         const double ne = (j & 1) ? n[dd] : -n[dd];   // n . e_j
         double um, up, gm[3], gp[3], alpha = 0.0, sigma = 0.0;
@@ -504,13 +580,13 @@ __global__ void __launch_bounds__(128) k_assemble_crossed(
           alpha = up - um;
           const double dp = gp[0] * n[0] + gp[1] * n[1] + gp[2] * n[2];
           const double dm = gm[0] * n[0] + gm[1] * n[1] + gm[2] * n[2];
-          sigma = P.beta[1] * dp - P.beta[0] * dm;
+          sigma = d_mu(P, 1, xg, nullptr) * dp - d_mu(P, 0, xg, nullptr) * dm;
         }
         const double a = sg * alpha, ba = sg * sigma * ne;
         cc = muh / h2;
         coef = -muh / h2;
         tag = so;
-        corr = muh * (a / h2 + (1.0 - th) * ba / (h * bo));
+        corr = muh * (a / h2 + (1.0 - th) * ba / (h * mfar));
       }
     }
     if (j < 7) {

@@ -99,7 +99,18 @@ int check_problem(const nbm_problem* p, DevProblem* out, std::string* why) {
   if (ls.kind == NBM_LS_STAR && (ls.star_m < 0 || ls.star_m > 16 || ls.star_n < 0 || ls.star_n > 16 || !(ls.star_r0 > 0.0f))) {
     *why = "problem: bad star parameters"; return NBM_E_INVALID_PROBLEM;
   }
-  if (p->source < NBM_SRC_SINE3PI || p->source > NBM_SRC_GAUSS) { *why = "problem: bad source"; return NBM_E_INVALID_PROBLEM; }
+  if (!((p->source >= NBM_SRC_SINE3PI && p->source <= NBM_SRC_GAUSS) || p->source == NBM_SRC_PAPER41)) {
+    *why = "problem: bad source"; return NBM_E_INVALID_PROBLEM;
+  }
+  if (p->mu_kind < NBM_MU_CONST || p->mu_kind > NBM_MU_LINEAR) { *why = "problem: bad mu kind"; return NBM_E_INVALID_PROBLEM; }
+  if (p->mu_kind == NBM_MU_LINEAR)   // positive on the box: a linear field attains its minimum at a corner
+    for (int s = 0; s < 2; ++s)
+      for (int c = 0; c < 8; ++c) {
+        const float* m = p->mu_lin[s];
+        const double v = m[0] + ((c & 1) ? m[1] : -m[1]) + ((c & 2) ? m[2] : -m[2]) + ((c & 4) ? m[3] : -m[3]);
+        if (!(v > 0.0)) { *why = "problem: linear mu must be > 0 on the box (S:236)"; return NBM_E_INVALID_PROBLEM; }
+      }
+  if (p->source == NBM_SRC_GAUSS && p->mu_kind != NBM_MU_CONST) { *why = "problem: Gaussian charges need constant mu"; return NBM_E_INVALID_PROBLEM; }
   if (p->source == NBM_SRC_GAUSS) {
     if (p->n_charges < 0 || p->n_charges > kMaxCharges || (p->n_charges > 0 && (!p->q || !p->charge_centers)) || !(p->charge_sigma > 0.0f)) {
       *why = "problem: bad charges"; return NBM_E_INVALID_PROBLEM;
@@ -133,6 +144,9 @@ int check_problem(const nbm_problem* p, DevProblem* out, std::string* why) {
       out->charge_sigma = p->charge_sigma;
     }
     out->lambda_b = p->lambda_b;
+    out->mu_kind = p->mu_kind;
+    for (int s = 0; s < 2; ++s)
+      for (int c = 0; c < 4; ++c) out->mu_lin[s][c] = p->mu_lin[s][c];
   }
   return NBM_OK;
 }
@@ -276,6 +290,10 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   if (rc) { g_create_error = why; return rc; }
   rc = check_arch(arch, &ai, &why);
   if (rc) { g_create_error = why; return rc; }
+  if (dp.mu_kind != NBM_MU_CONST && !(ai.prec == NBM_PREC_FP32 && ai.width <= 64)) {
+    g_create_error = "variable mu: supported by the fp32 kernel with W <= 64 in this build";
+    return NBM_E_INVALID_ARCH;
+  }
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) { g_create_error = cudaGetErrorString(e); return NBM_E_CUDA; }
   nbm_handle* h = new nbm_handle();
@@ -306,6 +324,7 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   ALLOC(w.counts, 16 * sizeof(int));
   ALLOC(w.list, items * sizeof(int));
   ALLOC(w.list_aux, items * sizeof(float));
+  ALLOC(w.pcoef, dp.mu_kind != NBM_MU_CONST ? (size_t)max_points * 6 * sizeof(float) : 16);
   ALLOC(w.xrow_x, 7 * w.xcap * 3 * sizeof(float));
   ALLOC(w.xrow_u, 7 * w.xcap * sizeof(float));
   ALLOC(w.xrow_cot, 7 * w.xcap * sizeof(float));
@@ -367,7 +386,7 @@ void nbm_destroy(nbm_handle* h) {
   void* ps[] = {h->d_problem, h->ws.cls, h->ws.aux_tmp, h->ws.blk_counts, h->ws.blk_offsets,
                 h->ws.counts, h->ws.list, h->ws.list_aux, h->ws.xrow_x, h->ws.xrow_u, h->ws.xrow_cot,
                 h->ws.xrow_tag, h->ws.xrec, h->ws.xlist, h->ws.part, h->ws.touched, h->ws.lpart,
-                h->ws.err, h->ws.bc, h->d_grid, h->ws.wimg, h->ws.wimg_b, h->ws.hscr, h->ws.rep, h->ws.wimg32};
+                h->ws.err, h->ws.bc, h->d_grid, h->ws.pcoef, h->ws.wimg, h->ws.wimg_b, h->ws.hscr, h->ws.rep, h->ws.wimg32};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : h->ev) cudaEventDestroy(ev);
@@ -484,6 +503,7 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
   MlpParams pm;
   fill_common(h, pm, theta_dev, h_cell);
   pm.two_over_n = (float)(2.0 * weight / ng);
+  pm.pcoef = P.mu_kind != NBM_MU_CONST ? w.pcoef : nullptr;
   for (int k = 0; k < 2; ++k) {
     const int s0 = 3 * k, net = k == 0 ? 0 : net1;
     const int side = k;

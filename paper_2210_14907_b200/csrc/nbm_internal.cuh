@@ -37,6 +37,8 @@ struct DevProblem {
   double lambda_b;
   float centers_f[kMaxSpheres][3];   // fp32 copies (exact: the inputs are fp32) for the filter
   float radii_f[kMaxSpheres];
+  int mu_kind;                       // NBM_MU_*
+  double mu_lin[2][4];
   int grid_n;                        // NBM_LS_GRID: Nc
   const float* grid_phi;             // NBM_LS_GRID: device copy of the nodal values (handle-owned)
 };
@@ -80,6 +82,7 @@ struct Workspace {
   int* counts;          // [16]: class counts, then segment counts
   int* list;            // [cap + cap]   class-partitioned indices
   float* list_aux;      // [cap + cap]
+  float* pcoef;         // [cap][6] variable-mu arm coefficients c_j / d of the uncrossed rows
   // crossed rows (7 per crossed point)
   float* xrow_x;        // [7 xcap][3]
   float* xrow_u;        // [7 xcap]
@@ -158,6 +161,7 @@ struct MlpParams {
   int64_t p_net;
   float h;
   float two_over_n;          // 2 / N_global
+  const float* pcoef;        // variable mu: per interior point [n][6] arm coefficients c_j/d (else null)
   int64_t p_stride;          // partial-slot stride (p_net rounded up to 4 floats)
   float* part;               // [2][grid][p_stride]
   int* touched;              // [2][grid]

@@ -14,7 +14,8 @@ import numpy as np
 LATTICE = 1 << 24  # coordinates and h are multiples of 2^-24 (G9)
 
 LS_NONE, LS_SPHERES, LS_STAR, LS_PLANE, LS_GRID = 0, 1, 2, 3, 4
-SRC_SINE3PI, SRC_PAIR, SRC_GAUSS = 0, 1, 2
+SRC_SINE3PI, SRC_PAIR, SRC_GAUSS, SRC_PAPER41 = 0, 1, 2, 4
+MU_CONST, MU_PAPER41, MU_LINEAR = 0, 1, 2
 ACT_TANH, ACT_SILU, ACT_SINE = 0, 1, 2
 PREC_FP32, PREC_BF16 = 0, 1
 
@@ -106,6 +107,14 @@ def config(name: str, width: int | None = None, prec: int | None = None) -> dict
                     source=SRC_PAIR, sizes=[3, w, w, w, w, 1], act=ACT_TANH,
                     prec=PREC_BF16 if prec is None else prec, n_nets=2,
                     N=1 << 22, Nb=1 << 19, H=h_lattice(2 / 1023), lr=1e-3)
+    elif name == "p41":
+        # the paper's 4.1 benchmark: sphere r = 0.5, u- = e^z, u+ = cos(x) sin(y),
+        # mu- = y^2 ln(x+2) + 4, mu+ = e^{-z}; two 5 x 10 sine nets (982 parameters); the
+        # Table 1 resolution N = 2^7 (h = 2/128) with mesh-free points
+        base.update(ls_kind=LS_SPHERES, centers=np.zeros((1, 3), np.float32),
+                    radii=np.array([0.5], np.float32), beta=(1.0, 1.0), source=SRC_PAPER41,
+                    mu_kind=MU_PAPER41, sizes=[3, 10, 10, 10, 10, 10, 1], act=ACT_SINE,
+                    prec=PREC_FP32, n_nets=2, N=1 << 18, Nb=1 << 15, H=h_lattice(2 / 128), lr=1e-3)
     else:
         raise ValueError(name)
     if prec is not None:

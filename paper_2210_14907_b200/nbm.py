@@ -45,7 +45,8 @@ class nbm_problem(C.Structure):
                 ("beta_minus", C.c_float), ("beta_plus", C.c_float), ("k_minus", C.c_float),
                 ("k_plus", C.c_float), ("source", C.c_int), ("n_charges", C.c_int),
                 ("q", C.POINTER(C.c_float)), ("charge_centers", C.POINTER(C.c_float)),
-                ("charge_sigma", C.c_float), ("lambda_b", C.c_float)]
+                ("charge_sigma", C.c_float), ("lambda_b", C.c_float), ("mu_kind", C.c_int),
+                ("mu_lin", (C.c_float * 4) * 2)]
 
 
 class nbm_arch(C.Structure):
@@ -131,6 +132,12 @@ class Descriptors:
         p.charge_centers = qc.ctypes.data_as(C.POINTER(C.c_float))
         p.charge_sigma = cfg["charge_sigma"]
         p.lambda_b = cfg["lambda_b"]
+        p.mu_kind = int(cfg.get("mu_kind", 0))
+        if cfg.get("mu_lin") is not None:
+            ml = np.asarray(cfg["mu_lin"], np.float32).reshape(2, 4)
+            for s_ in range(2):
+                for c_ in range(4):
+                    p.mu_lin[s_][c_] = float(ml[s_, c_])
         sizes = np.ascontiguousarray(np.asarray(cfg["sizes"], np.int32))
         self._keep.append(sizes)
         a = nbm_arch()
