@@ -112,8 +112,12 @@ typedef struct nbm_problem {
 } nbm_problem;
 
 /* MLP surrogate (P:60 two networks, one per side).  sizes = [3, W, ..., W, 1]
- * with uniform hidden width W.  Supported: FP32 W in {32, 64} with 1..4 hidden layers
- * (all-in-shared-memory SIMT kernel); others return NBM_E_INVALID_ARCH. */
+ * with uniform hidden width W.  Supported (others return NBM_E_INVALID_ARCH):
+ *   FP32 tanh: W <= 32 with 1..5 hidden layers, W <= 64 with 1..4 (padded to 16/32/64),
+ *              W in {128, 256} with 2..4;
+ *   FP32 sine: W <= 32 with 1..5 hidden layers (the paper's 5 x 10 nets);
+ *   BF16 (tcgen05): W in {64, 128} tanh or SiLU, W = 256 tanh, 2..4 hidden layers.
+ * Variable mu (nbm_problem.mu_kind) needs the FP32 W <= 64 kernel. */
 typedef struct nbm_arch {
   int n_layers;                  /* entries of sizes[] (>= 3) */
   const int* sizes;              /* host */

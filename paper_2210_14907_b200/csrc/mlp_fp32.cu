@@ -39,6 +39,8 @@ __device__ __forceinline__ void ldv(const float* p, float (&v)[2]) {
   float2 t = *reinterpret_cast<const float2*>(p);
   v[0] = t.x; v[1] = t.y;
 }
+__device__ __forceinline__ void ldv(const float* p, float (&v)[1]) { v[0] = *p; }
+__device__ __forceinline__ void stv(float* p, const float (&v)[1]) { *p = v[0]; }
 __device__ __forceinline__ void stv(float* p, const float (&v)[4]) {
   *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
 }
@@ -46,12 +48,12 @@ __device__ __forceinline__ void stv(float* p, const float (&v)[2]) {
   *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
 }
 
-template <int W, int NH>
+template <int W, int NH, bool SINE = false>
 struct Layout {
   static constexpr int LDA = W + 4;              // padded row stride of activations
   static constexpr int LDW = W + 4;              // padded row stride of hidden weights
   static constexpr int TC = W / 16;              // GEMM columns per thread (rows: kRT)
-  static constexpr int DB = (W == 64) ? 4 : 2;   // dW block per thread: DB x DB
+  static constexpr int DB = W / 16;              // dW block per thread: DB x DB (16 x 16 blocks)
   static constexpr int NHH = NH - 1;             // hidden x hidden layers
   // shared-memory carve (floats)
   static constexpr int oW1 = 0;                          // [W][3]
@@ -68,8 +70,10 @@ struct Layout {
   static constexpr int oAWo = oAB + NH * W;              // [W] + bo
   static constexpr int oAux = oAWo + W + 4;              // [kB]
   static constexpr int oItem = oAux + kB;                // int [kB]
-  static constexpr int total = oItem + kB + 16;
+  static constexpr int oCos = (oItem + kB + 16 + 3) & ~3;   // sine: [NH][kB][LDA] cos(z_l) for act'
+  static constexpr int total = oCos + (SINE ? NH * kB * LDA : 0);
   static constexpr size_t bytes = sizeof(float) * total;
+  static_assert(bytes <= 232448, "shared memory");
   // theta offsets within one network (G17)
   static constexpr int64_t tW1 = 0, tB1 = 3 * W;
   __host__ __device__ static constexpr int64_t tWl(int l) { return 4 * W + (int64_t)(l - 2) * (W * W + W); }
@@ -80,10 +84,10 @@ struct Layout {
 };
 
 // Hout[b][n] = tanh(sum_k Hin[b][k] W[n][k] + bias[n]); thread = 8 rows x TC cols.
-template <int W, int NH>
+template <int W, int NH, bool SINE = false>
 __device__ __forceinline__ void fwd_gemm(const float* __restrict__ Hin, float* __restrict__ Hout,
                                          const float* __restrict__ Ws, const float* __restrict__ bias,
-                                         int tid) {
+                                         int tid, float* __restrict__ CosOut = nullptr) {
   using L = Layout<W, NH>;
   constexpr int TC = L::TC;
   const int tr = tid & 31, tc = tid >> 5;
@@ -111,17 +115,22 @@ __device__ __forceinline__ void fwd_gemm(const float* __restrict__ Hin, float* _
   for (int c = 0; c < TC; ++c) bv[c] = bias[tc * TC + c];
 #pragma unroll
   for (int i = 0; i < kRT; ++i) {
-    float o[TC];
+    float o[TC], oc[TC];
 #pragma unroll
-    for (int c = 0; c < TC; ++c) o[c] = tanhf(acc[i][c] + bv[c]);
+    for (int c = 0; c < TC; ++c) {
+      if (SINE) sincosf(acc[i][c] + bv[c], &o[c], &oc[c]);   // P:68 sine units; cos kept for act'
+      else o[c] = tanhf(acc[i][c] + bv[c]);
+    }
     stv(Hout + (tr + 32 * i) * L::LDA + tc * TC, o);
+    if (SINE) stv(CosOut + (tr + 32 * i) * L::LDA + tc * TC, oc);
   }
 }
 
 // In place: H[b][i] <- (sum_o G[b][o] W[o][i]) * (1 - H[b][i]^2)   (delta_{l-1}, tanh')
-template <int W, int NH>
+template <int W, int NH, bool SINE = false>
 __device__ __forceinline__ void bwd_gemm(const float* __restrict__ G, float* __restrict__ H,
-                                         const float* __restrict__ Ws, int tid) {
+                                         const float* __restrict__ Ws, int tid,
+                                         const float* __restrict__ Cs = nullptr) {
   using L = Layout<W, NH>;
   constexpr int TC = L::TC;
   const int tr = tid & 31, tc = tid >> 5;
@@ -148,9 +157,10 @@ __device__ __forceinline__ void bwd_gemm(const float* __restrict__ G, float* __r
   for (int i = 0; i < kRT; ++i) {
     float hv[TC], o[TC];
     float* p = H + (tr + 32 * i) * L::LDA + tc * TC;
-    ldv(p, hv);
+    if (SINE) ldv(Cs + (tr + 32 * i) * L::LDA + tc * TC, hv);   // act' = cos(z)
+    else ldv(p, hv);
 #pragma unroll
-    for (int c = 0; c < TC; ++c) o[c] = acc[i][c] * (1.0f - hv[c] * hv[c]);
+    for (int c = 0; c < TC; ++c) o[c] = SINE ? acc[i][c] * hv[c] : acc[i][c] * (1.0f - hv[c] * hv[c]);
     stv(p, o);
   }
 }
@@ -195,10 +205,14 @@ __device__ __forceinline__ void colsum(const float* __restrict__ X, float* __res
   __syncthreads();
 }
 
-template <int W, int NH, bool TRAIN>
+// W is the kernel width (16, 32, 64); the network's real width wr <= W (prm.width_real) is
+// embedded with zero weights and biases in the padded units (their activations are 0 for tanh
+// and sine, their deltas 0), and only real parameters are read and written.
+template <int W, int NH, int ACT, bool TRAIN>
 __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
   static_assert(kB % 32 == 0, "tile rows");
-  using L = Layout<W, NH>;
+  constexpr bool SINE = ACT == NBM_ACT_SINE;
+  using L = Layout<W, NH, SINE>;
   constexpr int NHH = L::NHH;
   constexpr int DB = L::DB;
   extern __shared__ __align__(16) float sm[];
@@ -216,9 +230,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
   float* sAWo = sm + L::oAWo;
   float* sAux = sm + L::oAux;
   int* sItem = reinterpret_cast<int*>(sm + L::oItem);
+  float* sCos = sm + L::oCos;   // sine: cos(z_l), layer l at (l-1) kB LDA
   __shared__ int segTiles[kNumSeg + 1], segCnt[kNumSeg], segStart[kNumSeg];
 
   const int tid = threadIdx.x;
+  // theta offsets of the real network (G17) with real width wr
+  const int wr = prm.width_real > 0 ? prm.width_real : W;
+  const int64_t tW1 = 0, tB1 = 3 * wr;
+  auto tWl = [&](int l) -> int64_t { return 4 * wr + (int64_t)(l - 2) * (wr * wr + wr); };
+  auto tBl = [&](int l) -> int64_t { return tWl(l) + (int64_t)wr * wr; };
+  const int64_t tWo = 4 * wr + (int64_t)NHH * (wr * wr + wr), tBo = tWo + wr;
   if (tid < kNumSeg) {
     int c = prm.counts[prm.cnt_slot[tid]];
     segCnt[tid] = c;
@@ -264,33 +285,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
       for (int l = 0; l < NHH; ++l)
 #pragma unroll
         for (int a = 0; a < DB; ++a) {
-          float v[DB];
+          const int o = to * DB + a;
 #pragma unroll
-          for (int c = 0; c < DB; ++c) v[c] = dWh[l][a * DB + c] + scr[(t * (NHH > 0 ? NHH : 1) + l) * DB * DB + a * DB + c];
-          stv(out + L::tWl(l + 2) + (int64_t)(to * DB + a) * W + ti * DB, v);
+          for (int c = 0; c < DB; ++c) {
+            const int i = ti * DB + c;
+            if (o < wr && i < wr)
+              out[tWl(l + 2) + (int64_t)o * wr + i] =
+                  dWh[l][a * DB + c] + scr[(t * (NHH > 0 ? NHH : 1) + l) * DB * DB + a * DB + c];
+          }
         }
     }
-    for (int i = tid; i < 3 * W; i += kThreads) out[L::tW1 + i] = sAW1[i];
-    for (int i = tid; i < W; i += kThreads) {
-      out[L::tB1 + i] = sAB[i];
-      for (int l = 2; l <= NH; ++l) out[L::tBl(l) + i] = sAB[(l - 1) * W + i];
-      out[L::tWo + i] = sAWo[i];
+    for (int i = tid; i < 3 * wr; i += kThreads) out[tW1 + i] = sAW1[i];
+    for (int i = tid; i < wr; i += kThreads) {
+      out[tB1 + i] = sAB[i];
+      for (int l = 2; l <= NH; ++l) out[tBl(l) + i] = sAB[(l - 1) * W + i];
+      out[tWo + i] = sAWo[i];
     }
-    if (tid == 0) out[L::tBo] = sAWo[W];
+    if (tid == 0) out[tBo] = sAWo[W];
     touched[net] = true;
   };
   auto load_net = [&](int net) {
     const float* th = prm.theta + (int64_t)net * prm.p_net;
-    for (int i = tid; i < 3 * W; i += kThreads) sW1[i] = th[L::tW1 + i];
+    for (int i = tid; i < 3 * W; i += kThreads) sW1[i] = i < 3 * wr ? th[tW1 + i] : 0.0f;
     for (int i = tid; i < W; i += kThreads) {
-      sBias[i] = th[L::tB1 + i];
-      for (int l = 2; l <= NH; ++l) sBias[(l - 1) * W + i] = th[L::tBl(l) + i];
-      sWo[i] = th[L::tWo + i];
+      const bool real = i < wr;
+      sBias[i] = real ? th[tB1 + i] : 0.0f;
+      for (int l = 2; l <= NH; ++l) sBias[(l - 1) * W + i] = real ? th[tBl(l) + i] : 0.0f;
+      sWo[i] = real ? th[tWo + i] : 0.0f;
     }
-    if (tid == 0) sWo[W] = th[L::tBo];
+    if (tid == 0) sWo[W] = th[tBo];
     for (int l = 0; l < NHH; ++l)
-      for (int i = tid; i < W * W; i += kThreads)
-        sWh[l * W * L::LDW + (i / W) * L::LDW + (i % W)] = th[L::tWl(l + 2) + i];
+      for (int i = tid; i < W * W; i += kThreads) {
+        const int o = i / W, c = i % W;
+        sWh[l * W * L::LDW + o * L::LDW + c] = (o < wr && c < wr) ? th[tWl(l + 2) + (int64_t)o * wr + c] : 0.0f;
+      }
   };
 
   int seg = 0;
@@ -345,15 +373,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
       const float w0 = sW1[3 * col], w1 = sW1[3 * col + 1], w2 = sW1[3 * col + 2], bb = sBias[col];
       for (int r = r0; r < kB; r += step) {
         float z = fmaf(w2, sX[4 * r + 2], fmaf(w1, sX[4 * r + 1], fmaf(w0, sX[4 * r], bb)));
-        sAct[r * L::LDA + col] = tanhf(z);
+        if (SINE) sincosf(z, &sAct[r * L::LDA + col], &sCos[r * L::LDA + col]);
+        else sAct[r * L::LDA + col] = tanhf(z);
       }
     }
     __syncthreads();
     // ---- hidden GEMMs ----
 #pragma unroll
     for (int l = 0; l < NHH; ++l) {
-      fwd_gemm<W, NH>(sAct + l * kB * L::LDA, sAct + (l + 1) * kB * L::LDA, sWh + l * W * L::LDW,
-                      sBias + (l + 1) * W, tid);
+      fwd_gemm<W, NH, SINE>(sAct + l * kB * L::LDA, sAct + (l + 1) * kB * L::LDA, sWh + l * W * L::LDW,
+                            sBias + (l + 1) * W, tid, sCos + (l + 1) * kB * L::LDA);
       __syncthreads();
     }
     // ---- output layer u = wo . h_NH + bo ----
@@ -433,7 +462,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
       const float wo = sWo[col];
       for (int r = part; r < kB; r += parts) {
         float hv = hTop[r * L::LDA + col];
-        hTop[r * L::LDA + col] = sUb[r] * wo * (1.0f - hv * hv);
+        const float ad = SINE ? sCos[(NH - 1) * kB * L::LDA + r * L::LDA + col] : 1.0f - hv * hv;
+        hTop[r * L::LDA + col] = sUb[r] * wo * ad;
       }
     }
     __syncthreads();
@@ -443,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
       float* Hp = sAct + l * kB * L::LDA;
       dw_gemm<W, NH>(Gl, Hp, dWh[l], tid);
       colsum<W, NH>(Gl, sAB + (l + 1) * W, sRed, tid);   // db (contains __syncthreads)
-      bwd_gemm<W, NH>(Gl, Hp, sWh + l * W * L::LDW, tid);
+      bwd_gemm<W, NH, SINE>(Gl, Hp, sWh + l * W * L::LDW, tid, sCos + l * kB * L::LDA);
       __syncthreads();
     }
     {  // layer 1: dW1[n][c] += sum_b G1[b][n] x[b][c]; db1 += sum_b G1[b][n]
@@ -494,10 +524,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
   }
 }
 
-template <int W, int NH, bool TRAIN>
+template <int W, int NH, int ACT, bool TRAIN>
 static cudaError_t launch_t(const MlpParams& p, int grid, cudaStream_t s) {
-  using L = Layout<W, NH>;
-  auto kern = k_mlp_fp32<W, NH, TRAIN>;
+  using L = Layout<W, NH, ACT == NBM_ACT_SINE>;
+  auto kern = k_mlp_fp32<W, NH, ACT, TRAIN>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
@@ -508,33 +538,50 @@ static cudaError_t launch_t(const MlpParams& p, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-int mlp_fp32_supported(int width, int n_hidden) {
-  return (width == 32 || width == 64) && n_hidden >= 1 && n_hidden <= 4;
+// kernel width for a real hidden width (the smallest of 16 / 32 / 64 that holds it)
+static int kernel_width(int width) { return width <= 16 ? 16 : width <= 32 ? 32 : 64; }
+
+int mlp_fp32_supported(int width, int n_hidden, int act) {
+  if (width < 1 || n_hidden < 1) return 0;
+  if (act == NBM_ACT_TANH) return (width <= 32 && n_hidden <= 5) || (width <= 64 && n_hidden <= 4);
+  if (act == NBM_ACT_SINE) return width <= 32 && n_hidden <= 5;
+  return 0;
 }
 
-template <bool TRAIN>
+template <int ACT, bool TRAIN>
 static cudaError_t dispatch(int W, int NH, const MlpParams& p, int grid, cudaStream_t s) {
-  if (W == 64) {
-    switch (NH) {
-      case 1: return launch_t<64, 1, TRAIN>(p, grid, s);
-      case 2: return launch_t<64, 2, TRAIN>(p, grid, s);
-      case 3: return launch_t<64, 3, TRAIN>(p, grid, s);
-      case 4: return launch_t<64, 4, TRAIN>(p, grid, s);
-    }
-  } else if (W == 32) {
-    switch (NH) {
-      case 1: return launch_t<32, 1, TRAIN>(p, grid, s);
-      case 2: return launch_t<32, 2, TRAIN>(p, grid, s);
-      case 3: return launch_t<32, 3, TRAIN>(p, grid, s);
-      case 4: return launch_t<32, 4, TRAIN>(p, grid, s);
+#define NBM_F32_CASES(WW)                                  \
+  switch (NH) {                                            \
+    case 1: return launch_t<WW, 1, ACT, TRAIN>(p, grid, s); \
+    case 2: return launch_t<WW, 2, ACT, TRAIN>(p, grid, s); \
+    case 3: return launch_t<WW, 3, ACT, TRAIN>(p, grid, s); \
+    case 4: return launch_t<WW, 4, ACT, TRAIN>(p, grid, s); \
+    case 5: return launch_t<WW, 5, ACT, TRAIN>(p, grid, s); \
+  }
+  if (W == 16) { NBM_F32_CASES(16) }
+  if (W == 32) { NBM_F32_CASES(32) }
+  if constexpr (ACT == NBM_ACT_TANH) {
+    if (W == 64) {
+      switch (NH) {
+        case 1: return launch_t<64, 1, ACT, TRAIN>(p, grid, s);
+        case 2: return launch_t<64, 2, ACT, TRAIN>(p, grid, s);
+        case 3: return launch_t<64, 3, ACT, TRAIN>(p, grid, s);
+        case 4: return launch_t<64, 4, ACT, TRAIN>(p, grid, s);
+      }
     }
   }
+#undef NBM_F32_CASES
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_mlp_fp32(int width, int n_hidden, bool train, const MlpParams& p, int grid,
+cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
                             cudaStream_t s) {
-  return train ? dispatch<true>(width, n_hidden, p, grid, s) : dispatch<false>(width, n_hidden, p, grid, s);
+  MlpParams q = p;
+  q.width_real = width;
+  const int W = kernel_width(width);
+  if (act == NBM_ACT_SINE)
+    return train ? dispatch<NBM_ACT_SINE, true>(W, n_hidden, q, grid, s) : dispatch<NBM_ACT_SINE, false>(W, n_hidden, q, grid, s);
+  return train ? dispatch<NBM_ACT_TANH, true>(W, n_hidden, q, grid, s) : dispatch<NBM_ACT_TANH, false>(W, n_hidden, q, grid, s);
 }
 
 }  // namespace nbm

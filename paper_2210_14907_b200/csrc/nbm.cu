@@ -50,11 +50,12 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
   for (int l = 1; l < a->n_layers - 1; ++l)
     if (a->sizes[l] != W) { *why = "arch: hidden widths must be uniform"; return NBM_E_INVALID_ARCH; }
   if (a->n_nets != 1 && a->n_nets != 2) { *why = "arch: n_nets must be 1 or 2"; return NBM_E_INVALID_ARCH; }
-  if (a->act != NBM_ACT_TANH && a->act != NBM_ACT_SILU) { *why = "arch: bad activation"; return NBM_E_INVALID_ARCH; }
+  if (a->act != NBM_ACT_TANH && a->act != NBM_ACT_SILU && a->act != NBM_ACT_SINE) { *why = "arch: bad activation"; return NBM_E_INVALID_ARCH; }
   if (a->prec != NBM_PREC_FP32 && a->prec != NBM_PREC_BF16) { *why = "arch: bad precision"; return NBM_E_INVALID_ARCH; }
   int nh = a->n_layers - 2;
   bool ok = false;
-  if (a->prec == NBM_PREC_FP32 && a->act == NBM_ACT_TANH) ok = mlp_fp32_supported(W, nh) || mlp_fp32w_supported(W, nh);
+  if (a->prec == NBM_PREC_FP32)
+    ok = mlp_fp32_supported(W, nh, a->act) || (a->act == NBM_ACT_TANH && mlp_fp32w_supported(W, nh));
   if (a->prec == NBM_PREC_BF16) ok = mlp_tc_supported(W, nh, a->act) || (W == 256 && nh >= 2 && nh <= 4 && a->act == NBM_ACT_TANH);
   if (!ok) {
     *why = "arch: unsupported (prec, act, width, depth) combination in this build";
@@ -241,7 +242,7 @@ cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cu
     return launch_mlp_w256(A.n_hidden, train, p, w.wimg, w.wimg_b, w.hscr, w.rep, w.nrep, w.grid_base, s);
   if (is_fp32w(A)) return launch_mlp_fp32w(A.width, A.n_hidden, train, p, w.wimg32, w.rep, w.nrep, w.grid_base, s);
   if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, A.act, train, p, w.grid_base, s);
-  return launch_mlp_fp32(A.width, A.n_hidden, train, p, w.grid_base, s);
+  return launch_mlp_fp32(A.width, A.n_hidden, A.act, train, p, w.grid_base, s);
 }
 
 

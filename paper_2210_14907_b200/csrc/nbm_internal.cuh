@@ -161,6 +161,7 @@ struct MlpParams {
   int64_t p_net;
   float h;
   float two_over_n;          // 2 / N_global
+  int width_real;            // fp32 kernel: the network's hidden width (<= the kernel's W)
   const float* pcoef;        // variable mu: per interior point [n][6] arm coefficients c_j/d (else null)
   int64_t p_stride;          // partial-slot stride (p_net rounded up to 4 floats)
   float* part;               // [2][grid][p_stride]
@@ -169,9 +170,9 @@ struct MlpParams {
   float* u_out;              // forward-only mode: u_out[item] = u
   const uint16_t* wimg;      // bf16 hidden weights in the tensor-core smem layout [2][NH-1][W*W]
 };
-cudaError_t launch_mlp_fp32(int width, int n_hidden, bool train, const MlpParams& p, int grid,
+cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
                             cudaStream_t s);
-int mlp_fp32_supported(int width, int n_hidden);
+int mlp_fp32_supported(int width, int n_hidden, int act);
 // mlp_tc.cu (tcgen05 bf16)
 cudaError_t launch_mlp_tc(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
                           cudaStream_t s);

@@ -87,6 +87,7 @@ cudaError_t launch_sample(int kind, uint64_t seed, uint64_t step, const int64_t*
 // ---- Xavier / Glorot-uniform init (G11) ----
 struct InitTable {
   int n;
+  int sine;                        // sine nets: +-sqrt(6/fan_in), else Glorot (G11)
   int64_t off[2 * kMaxLayers];     // theta offset of the layer block
   int64_t ebase[2 * kMaxLayers];   // running weight-element index at the block start
   int fi[2 * kMaxLayers], fo[2 * kMaxLayers];
@@ -104,7 +105,7 @@ __global__ void k_init(InitTable t, int64_t P, uint64_t seed, float* __restrict_
   uint4 w = philox_ctr(seed, e >> 2, 0u, 2u);
   uint32_t word = (e & 3) == 0 ? w.x : (e & 3) == 1 ? w.y : (e & 3) == 2 ? w.z : w.w;
   float u = (float)(word >> 8) * 0x1p-24f;
-  float amp = __fsqrt_rn(__fdiv_rn(6.0f, (float)(t.fi[l] + t.fo[l])));
+  float amp = __fsqrt_rn(__fdiv_rn(6.0f, (float)(t.sine ? t.fi[l] : t.fi[l] + t.fo[l])));
   theta[i] = __fmul_rn(amp, __fsub_rn(__fmul_rn(2.0f, u), 1.0f));
 }
 
@@ -122,6 +123,7 @@ cudaError_t launch_init_params(const ArchInfo& a, uint64_t seed, float* theta, c
       e += (int64_t)t.fi[k] * t.fo[k];
     }
   t.n = k;
+  t.sine = a.act == NBM_ACT_SINE ? 1 : 0;
   k_init<<<(unsigned)((off + 255) / 256), 256, 0, s>>>(t, off, seed, theta);
   return cudaGetLastError();
 }

@@ -203,7 +203,7 @@ def test_errors_and_capacity(orc):
     assert s.status() == 0                                    # sticky word cleared
     s.close()
     with pytest.raises(nbm.NbmError) as e:
-        nbm.Solver(dict(cfg, sizes=[3, 48, 48, 1]), 0, max_points=16)
+        nbm.Solver(dict(cfg, sizes=[3, 100, 100, 1]), 0, max_points=16)   # fp32 W in (64, 128)
     assert e.value.code == 1
 
 
