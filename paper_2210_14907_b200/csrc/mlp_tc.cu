@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
              W / 16, false);
         tc::mma_commit(bar);
       }
-      if (l == 2) nxt = fetch(t + 1);   // the next tile's loads overlap this tile
+      if (!TRAIN && l == 2) nxt = fetch(t + 1);   // the next tile's loads overlap this tile
       wait_mma();
       if (tid == 0 && l < NH) wload(curNet, l + 1);   // prefetch the next layer's weights
       TR(2 + 2 * (l - 2));
@@ -525,8 +525,10 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     }
     __syncthreads();
     TR(8);
-    cur = nxt;
-    if (!TRAIN) continue;
+    if (!TRAIN) {
+      cur = nxt;
+      continue;
+    }
     // ---- residual epilogue -> cotangents (S4) ----
     if (kind == kSegStencil) {
       if (tid < kTPT) {
@@ -616,6 +618,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
         gemm((uint32_t)(W * (l - 1)), gbuf, 256, 128, LBO_ACT, hbuf, 256, 128, LBO_ACT, ID_DW, kTB / 16, !dwFresh);
         tc::mma_commit(dwbar);
       }
+      if (l == NH) nxt = fetch(t + 1);   // the next tile's loads, under the longest MMA phase
       wait_mma();
       if (tid == 0) wload(curNet, l > 2 ? l - 1 : 2);   // next GEMM's weights (W_2 for the next tile)
       TR(11 + 2 * (NH - l));
@@ -669,6 +672,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       tc::mma_commit(bar);
     }
     tailPending = true;   // collected under the next tile's gather and layer 1
+    cur = nxt;
     TR(20);
     TR(21);
     dwFresh = false;
