@@ -20,10 +20,17 @@
 
 namespace nbm {
 
-constexpr int kB = 128;        // rows per tile
-constexpr int kPT = 18;        // points per stencil tile (126 rows)
-constexpr int kThreads = 512;   // 16 warps: 4 per scheduler hide the LDS latency
-constexpr int kRT = kB / 32;     // GEMM rows per thread
+#ifndef NBM_F32_TILE
+#define NBM_F32_TILE 64
+#endif
+// 64-row tiles with 256 threads run two CTAs per SM, so one CTA's barriers and load latencies
+// overlap the other's FFMA work; 128-row tiles with 512 threads run one.
+constexpr int kB = NBM_F32_TILE;     // rows per tile
+constexpr int kPT = (kB - 1) / 7;    // points per stencil tile (9 -> 63 rows; 18 -> 126 rows)
+constexpr int kThreads = 4 * kB;     // 8 or 16 warps
+constexpr int kCtasPerSm = kB == 64 ? 2 : 1;
+constexpr int kRT = kB / 32;         // GEMM rows per thread
+constexpr int kHalves = kThreads / 256;   // dW row groups (summed at the flush)
 
 
 
@@ -40,6 +47,14 @@ __device__ __forceinline__ void ldv(const float* p, float (&v)[2]) {
   v[0] = t.x; v[1] = t.y;
 }
 __device__ __forceinline__ void ldv(const float* p, float (&v)[1]) { v[0] = *p; }
+__device__ __forceinline__ void ldv(const float* p, float (&v)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void stv(float* p, const float (&v)[8]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
 __device__ __forceinline__ void stv(float* p, const float (&v)[1]) { *p = v[0]; }
 __device__ __forceinline__ void stv(float* p, const float (&v)[4]) {
   *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
@@ -52,7 +67,7 @@ template <int W, int NH, bool SINE = false>
 struct Layout {
   static constexpr int LDA = W + 4;              // padded row stride of activations
   static constexpr int LDW = W + 4;              // padded row stride of hidden weights
-  static constexpr int TC = W / 16;              // GEMM columns per thread (rows: kRT)
+  static constexpr int TC = W / (kThreads / 32);   // GEMM columns per thread (rows: kRT)
   static constexpr int DB = W / 16;              // dW block per thread: DB x DB (16 x 16 blocks)
   static constexpr int NHH = NH - 1;             // hidden x hidden layers
   // shared-memory carve (floats)
@@ -175,7 +190,7 @@ __device__ __forceinline__ void dw_gemm(const float* __restrict__ G, const float
   const int t = tid & 255, half = tid >> 8;
   const int to = t >> 4, ti = t & 15;
 #pragma unroll 4
-  for (int b = half * (kB / 2); b < (half + 1) * (kB / 2); ++b) {
+  for (int b = half * (kB / kHalves); b < (half + 1) * (kB / kHalves); ++b) {
     float g[DB], hv[DB];
     ldv(G + b * L::LDA + to * DB, g);
     ldv(H + b * L::LDA + ti * DB, hv);
@@ -209,7 +224,7 @@ __device__ __forceinline__ void colsum(const float* __restrict__ X, float* __res
 // embedded with zero weights and biases in the padded units (their activations are 0 for tanh
 // and sine, their deltas 0), and only real parameters are read and written.
 template <int W, int NH, int ACT, bool TRAIN>
-__global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpParams prm) {
   static_assert(kB % 32 == 0, "tile rows");
   constexpr bool SINE = ACT == NBM_ACT_SINE;
   using L = Layout<W, NH, SINE>;
@@ -291,7 +306,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
             const int i = ti * DB + c;
             if (o < wr && i < wr)
               out[tWl(l + 2) + (int64_t)o * wr + i] =
-                  dWh[l][a * DB + c] + scr[(t * (NHH > 0 ? NHH : 1) + l) * DB * DB + a * DB + c];
+                  dWh[l][a * DB + c] +
+                  (kHalves == 2 ? scr[(t * (NHH > 0 ? NHH : 1) + l) * DB * DB + a * DB + c] : 0.0f);
           }
         }
     }
@@ -449,7 +465,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_mlp_fp32(const MlpParams prm) {
       for (int r = part * per; r < (part + 1) * per; ++r) s = fmaf(sUb[r], hTop[r * L::LDA + col], s);
       sRed[part * W + col] = s;
       if (tid < 32) {
-        float b = sUb[tid] + sUb[tid + 32] + sUb[tid + 64] + sUb[tid + 96];
+        float b = 0.0f;
+        for (int r = tid; r < kB; r += 32) b += sUb[r];
         for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
         if (tid == 0) sAWo[W] += b;
       }
@@ -534,9 +551,11 @@ static cudaError_t launch_t(const MlpParams& p, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<grid, kThreads, L::bytes, s>>>(p);
+  kern<<<grid * kCtasPerSm, kThreads, L::bytes, s>>>(p);
   return cudaGetLastError();
 }
+
+int mlp_fp32_ctas_per_sm() { return kCtasPerSm; }
 
 // kernel width for a real hidden width (the smallest of 16 / 32 / 64 that holds it)
 static int kernel_width(int width) { return width <= 16 ? 16 : width <= 32 ? 32 : 64; }

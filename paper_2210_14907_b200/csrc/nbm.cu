@@ -312,7 +312,8 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   int64_t items = 2 * max_points;
   w.nblk_cls = (int)((items + 1023) / 1024);
   w.grid_base = sms;
-  w.grid_mlp = sms * ((ai.prec == NBM_PREC_BF16) ? mlp_tc_ctas_per_sm(ai.width, ai.n_hidden) : 1);
+  w.grid_mlp = sms * ((ai.prec == NBM_PREC_BF16) ? mlp_tc_ctas_per_sm(ai.width, ai.n_hidden)
+                                                 : (ai.width <= 64 ? mlp_fp32_ctas_per_sm() : 1));
   std::vector<void**> ptrs;
   size_t sizes[32];
   int k = 0;

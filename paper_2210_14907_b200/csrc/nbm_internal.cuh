@@ -173,6 +173,7 @@ struct MlpParams {
 cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
                             cudaStream_t s);
 int mlp_fp32_supported(int width, int n_hidden, int act);
+int mlp_fp32_ctas_per_sm();
 // mlp_tc.cu (tcgen05 bf16)
 cudaError_t launch_mlp_tc(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
                           cudaStream_t s);
