@@ -445,3 +445,38 @@ def test_grid_levelset_parity(orc, name, nc):
         cfg["h"] = cfg["H"] / inputs.LATTICE
     lt = _parity(orc, cfg, 1 << 13, 1 << 10, seed=4)
     assert lt[2] > 0
+
+
+def test_large_batch_2e24_points(orc):
+    """A 2^24-point batch (64x config 2) in one call: the crossed term (0.5 % of the points)
+    against the oracle on exactly those points with the global normalisation, and the total
+    against the sum of four shard calls."""
+    cfg = _cfg("c2")
+    N, Nb = 1 << 24, 1 << 21
+    s = nbm.Solver(cfg, 0, max_points=N)
+    pb, ar = orc.from_config(cfg)
+    s.init_params(0)
+    pts = torch.empty(N, 3, device="cuda")
+    bpts = torch.empty(Nb, 3, device="cuda")
+    s.sample(0, 3, 0, 0, N, pts)
+    s.sample(1, 3, 0, 0, Nb, bpts)
+    lx, gx = _gpu_loss_grad(s, s.theta, pts, bpts, terms=nbm.TERM_CROSSED)
+    P = pts.cpu().numpy()
+    _, cls = orc.classify(pb, P, cfg["h"])
+    X = P[cls == 2]
+    th = orc.init_params(ar, 0)
+    L, _, g, _ = orc.loss_grad(pb, ar, th, X, np.zeros((0, 3), np.float32), cfg["h"], n_glob=N, nb_glob=Nb)
+    assert abs(lx - L) <= LOSS_TOL * L and np.linalg.norm(gx - g) <= GRAD_TOL * np.linalg.norm(g)
+    lt, gt = _gpu_loss_grad(s, s.theta, pts, bpts)
+    acc_l, acc_g = 0.0, np.zeros_like(gt)
+    for r in range(4):
+        lo, hi, blo, bhi = r * N // 4, (r + 1) * N // 4, r * Nb // 4, (r + 1) * Nb // 4
+        l, g_ = _gpu_loss_grad(s, s.theta, pts[lo:hi], bpts[blo:bhi], n_glob=N, nb_glob=Nb)
+        acc_l += l
+        acc_g += g_
+    # each CTA accumulates 64x more tiles in fp32 than at config size, and the full and the
+    # sharded calls assign tiles to CTAs differently: compare at the fp32 gradient bar
+    assert abs(acc_l - lt) <= LOSS_TOL * lt
+    assert np.linalg.norm(acc_g - gt) <= GRAD_TOL * np.linalg.norm(gt)
+    assert s.status() == 0
+    s.close()

@@ -185,3 +185,34 @@ def test_tc_eval_w256(orc):
     assert np.abs(u - want).max() <= TOL * np.abs(want).max()
     assert s.status() == 0
     s.close()
+
+
+@pytest.mark.parametrize("name,w,nh", [("c5", 64, 4), ("c5", 128, 4), ("c3", 128, 4), ("c4", 256, 4)])
+def test_tc_ragged_and_empty(orc, name, w, nh):
+    """Edge cases on the tensor-core paths: a single crossed point, single points with one
+    boundary point, partial stencil / row tiles (19, 37 points; 129 boundary points: a pair
+    tile's odd half at W = 256), boundary-only, interior-only and empty calls.  Totals at the
+    bf16 bar against the fp64 oracle (the per-term floor is not stable on a few residuals)."""
+    cfg = inputs.config(name, width=w) if name in ("c4", "c5") else inputs.config(name)
+    cfg["sizes"] = [3] + [w] * nh + [1]
+    pb, ar = orc.from_config(cfg)
+    s = nbm.Solver(cfg, 0, max_points=4096)
+    th = orc.init_params(ar, 1)
+    allp = orc.sample(0, 12, 0, 0, 4096, cfg["H"])
+    allb = orc.sample(1, 12, 0, 0, 512, cfg["H"])
+    _, cls = orc.classify(pb, allp, cfg["h"])
+    crossed = allp[cls == 2]
+    cases = [(crossed[:1], allb[:0]), (allp[:1], allb[:1]), (allp[:19], allb[:3]), (allp[:37], allb[:129]),
+             (allp[:0], allb[:200]), (allp[:300], allb[:0])]
+    for p_, b_ in cases:
+        gl, gg = _run(s, _dev(th), _dev(p_) if len(p_) else None, _dev(b_) if len(b_) else None)
+        L, _, g, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"])
+        Le, _, ge, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"], mode=orc.MODE_BF16)
+        ltol = max(TOL, 4 * abs(Le - L) / L)
+        gtol = max(TOL, 4 * np.linalg.norm(ge - g) / np.linalg.norm(g))
+        assert abs(gl - L) <= ltol * L, (len(p_), len(b_), gl, L)
+        assert np.linalg.norm(gg - g) <= gtol * np.linalg.norm(g), (len(p_), len(b_))
+    gl, gg = _run(s, _dev(th), None, None)
+    assert gl == 0.0 and np.all(gg == 0.0)
+    assert s.status() == 0
+    s.close()
