@@ -109,6 +109,22 @@ __device__ __forceinline__ int d_side_exact(const DevProblem& P, const double x[
 // filter decides whenever its margin exceeds its error bound, else the fp64 formula runs.
 //  spheres: |x-c|^2 vs r^2 in fp32 (relative error < 4e-7) with a 1e-5 relative margin;
 //  star:    the fp32 formula with a margin above its error bound (>= 1e-5 (2 + r)).
+// sphere filter over fp32 sphere data [n][4] = (cx, cy, cz, r) (shared-memory copy in K2a)
+__device__ __forceinline__ int d_side_spheres(const DevProblem& P, const float4* __restrict__ sph, const double x[3]) {
+  const float x0 = (float)x[0], x1 = (float)x[1], x2 = (float)x[2];
+  bool unsure = false;
+  for (int k = 0; k < P.n_spheres; ++k) {
+    const float4 c = sph[k];
+    const float dx = x0 - c.x, dy = x1 - c.y, dz = x2 - c.z;
+    const float d2 = (dx * dx + dy * dy) + dz * dz;
+    const float r2 = c.w * c.w;
+    if (d2 < r2 * (1.0f - 1e-5f)) return 0;          // certainly inside sphere k
+    if (d2 <= r2 * (1.0f + 1e-5f)) unsure = true;
+  }
+  if (!unsure) return 1;                              // certainly outside all spheres
+  return d_side_exact(P, x);
+}
+
 __device__ __forceinline__ int d_side(const DevProblem& P, const double x[3]) {
   if (P.ls_kind == NBM_LS_SPHERES) {
     const float x0 = (float)x[0], x1 = (float)x[1], x2 = (float)x[2];
@@ -336,8 +352,15 @@ __global__ void __launch_bounds__(kClsBlock) k_classify(
     float* __restrict__ pcoef) {
   const DevProblem& P = *Pp;
   __shared__ int cnt[kNumCls];
+  __shared__ float4 sph[kMaxSpheres];   // the sphere union's fp32 data, read by every side test
   if (threadIdx.x < kNumCls) cnt[threadIdx.x] = 0;
+  if (P.ls_kind == NBM_LS_SPHERES && threadIdx.x < P.n_spheres)
+    sph[threadIdx.x] = make_float4(P.centers_f[threadIdx.x][0], P.centers_f[threadIdx.x][1],
+                                   P.centers_f[threadIdx.x][2], P.radii_f[threadIdx.x]);
   __syncthreads();
+  auto side = [&](const double x[3]) {
+    return P.ls_kind == NBM_LS_SPHERES ? d_side_spheres(P, sph, x) : d_side(P, x);
+  };
   int64_t base = (int64_t)blockIdx.x * kClsItems;
   int64_t total = n + nb;
   for (int k = 0; k < kClsPerThread; ++k) {
@@ -348,7 +371,7 @@ __global__ void __launch_bounds__(kClsBlock) k_classify(
     if (it < n && !eval_only) {
       const float* p = pts + 3 * it;
       double pd[3] = {p[0], p[1], p[2]};
-      int s = d_side(P, pd);
+      int s = side(pd);
       int mask = s;
       bool ood = false;
 #pragma unroll 1
@@ -358,7 +381,7 @@ __global__ void __launch_bounds__(kClsBlock) k_classify(
         q[dd] = (j & 1) ? __fadd_rn(p[dd], hf) : __fsub_rn(p[dd], hf);
         if (q[dd] < -1.0f || q[dd] > 1.0f) ood = true;
         double qd[3] = {q[0], q[1], q[2]};
-        mask |= d_side(P, qd) << j;
+        mask |= side(qd) << j;
       }
       if (mask_out) mask_out[it] = (uint8_t)mask;
       if (ood) {
@@ -391,7 +414,7 @@ __global__ void __launch_bounds__(kClsBlock) k_classify(
     } else {
       const float* p = eval_only ? pts + 3 * it : bpts + 3 * (it - n);
       double pd[3] = {p[0], p[1], p[2]};
-      int s = d_side(P, pd);
+      int s = side(pd);
       c = s ? kClsBndPlus : kClsBndMinus;
       if (!eval_only) {
         if (!(terms & NBM_TERM_BOUNDARY)) c = kClsSkip;
