@@ -45,6 +45,8 @@ def kernel_name(cfg):
     w = cfg["sizes"][1]
     if cfg["prec"] == inputs.PREC_FP32:
         return "k_mlp_fp32w" if w >= 128 else "k_mlp_fp32"
+    if cfg["prec"] == inputs.PREC_FP32X:
+        return "k_mlp_tc<P=3> (tcgen05, 3-plane bf16 split)"
     return "k_mlp_w256 (tcgen05 cta_group::2)" if w == 256 else "k_mlp_tc (tcgen05)"
 
 
@@ -175,7 +177,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--width", type=int, default=None)
-    ap.add_argument("--prec", default=None, choices=["fp32", "bf16"], help="override the config's precision (c4/c5)")
+    ap.add_argument("--prec", default=None, choices=["fp32", "bf16", "fp32x"], help="override the config's precision (c4/c5)")
     ap.add_argument("--impl", default="nbm", choices=["nbm", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -190,12 +192,13 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     rank, world, local = dp.env_rank_world()
-    prec = None if args.prec is None else (inputs.PREC_FP32 if args.prec == "fp32" else inputs.PREC_BF16)
+    prec = None if args.prec is None else {"fp32": inputs.PREC_FP32, "bf16": inputs.PREC_BF16,
+                                            "fp32x": inputs.PREC_FP32X}[args.prec]
     cfg = inputs.config(args.config, width=args.width, prec=prec)
     if args.grid:
         cfg = inputs.with_grid(cfg, args.grid)
     cfg["label"] = cfg["name"] + (f"-w{cfg['sizes'][1]}" if cfg["name"] == "c5" else "") + \
-        ("" if prec is None else ("-fp32" if prec == inputs.PREC_FP32 else "-bf16")) + \
+        ("" if prec is None else {inputs.PREC_FP32: "-fp32", inputs.PREC_BF16: "-bf16", inputs.PREC_FP32X: "-fp32x"}[prec]) + \
         (f"-grid{args.grid}" if args.grid else "")
     if args.points:
         cfg["N"] = args.points
@@ -349,6 +352,10 @@ def main():
     if cfg["prec"] == inputs.PREC_FP32:
         peak = FP32_FFMA_TFLOPS
         bound, peak_note = "alu", "fp32 FFMA: 148 SM x 128 lanes x 2 FLOP x 1965 MHz (derived, DESIGN.md)"
+    elif cfg["prec"] == inputs.PREC_FP32X:
+        peak = peaks["bf16_tflops"] / 6.0
+        bound, peak_note = "tensor", (f"bf16 dense ({src}, MEASURED_PEAKS.json) / 6: each fp32-accurate product is six "
+                                      "bf16 plane products (G26)")
     else:
         peak = peaks["bf16_tflops"]
         bound, peak_note = "tensor", f"bf16 dense, {src} (MEASURED_PEAKS.json)"
@@ -363,7 +370,8 @@ def main():
         "value": val, "unit": "pts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_ms / args.steps, "steps_per_sec": 1e3 * args.steps / tot_ms,
         "loss_grad_pts_per_sec": Ng * calls / args.levels / (lg_ms_max / 1e3) if calls else None,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32" if cfg["prec"] == 0 else "bf16",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": {inputs.PREC_FP32: "f32", inputs.PREC_BF16: "bf16",
+                  inputs.PREC_FP32X: "f32 (3-plane bf16 split on tcgen05, f32 accumulate)"}[cfg["prec"]],
         "data": "synthetic (seeded Philox lattice points; manufactured two-phase Poisson)",
         "config": {"workload": cfg["label"], "points_per_gpu": N, "boundary_per_gpu": Nb,
                    "global_points": Ng, "mlp": "x".join(map(str, cfg["sizes"])), "n_nets": cfg["n_nets"],
@@ -371,7 +379,7 @@ def main():
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      **({"measured_ffma_3reg_peak": FP32_FFMA_3REG_MEASURED_TFLOPS,
                          "frac_of_measured_ffma": achieved / FP32_FFMA_3REG_MEASURED_TFLOPS}
-                        if cfg["prec"] == inputs.PREC_FP32 else {}),
+                        if cfg["prec"] in (inputs.PREC_FP32, inputs.PREC_FP32X) else {}),
                      "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name(cfg) + " fused fwd/residual/bwd",
                      "flop_per_launch": flop_launch, "avg_launch_ms": mlp_avg_s * 1e3,
                      "share_of_step": mlp_ms / eager_ms, "peak_src": peak_note},

@@ -68,6 +68,10 @@ extern "C" {
 #define NBM_ACT_SINE  2     /* P:68 "sine-activated neurons"; init +-sqrt(6/fan_in) */
 #define NBM_PREC_FP32 0     /* IEEE fp32 arithmetic throughout (G15) */
 #define NBM_PREC_BF16 1     /* bf16 tensor-core hidden GEMMs, fp32 accumulate (G16) */
+#define NBM_PREC_FP32X 2    /* fp32-accurate hidden GEMMs on the tensor cores: each fp32 operand split
+                             * exactly into three bf16 planes, the six plane products with
+                             * i + j <= 2 summed in fp32 (relative error <= ~2^-22 per product),
+                             * accurate tanh, everything else fp32 (G26); W = 64, 2-3 hidden layers */
 
 #define NBM_POINTS_INTERIOR 0
 #define NBM_POINTS_BOUNDARY 1

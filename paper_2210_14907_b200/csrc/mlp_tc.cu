@@ -38,8 +38,13 @@ namespace {
 constexpr int kTB = 128;   // rows per tile (= MMA M = TMEM lanes)
 constexpr int kTPT = 18;   // stencil points per tile
 
-template <int W, int NH, int ACT>
+// P = 1: bf16 operands (G16).  P = 3: fp32-accurate GEMMs for the fp32 configs -- every operand
+// is split exactly into three bf16 planes x = x1 + x2 + x3 (x1 = bf16(x), x2 = bf16(x - x1),
+// x3 = bf16(x - x1 - x2)) and each GEMM sums the six plane products with i + j <= 2 (the three
+// dropped ones are below 2^-24 relative), fp32 accumulation in TMEM (PREC_FP32X, G26).
+template <int W, int NH, int ACT, int P = 1>
 struct TcLayout {
+  static_assert(P == 1 || (P == 3 && ACT == NBM_ACT_TANH), "plane split: tanh with resident weights");
   static constexpr bool SILU = ACT == NBM_ACT_SILU;
   static constexpr bool STREAM = SILU;                     // weights streamed (TMA bulk) to make room
   static constexpr int NHH = NH - 1;
@@ -49,11 +54,13 @@ struct TcLayout {
   static constexpr int THREADS = 128 * CH;                 // 4 lane quadrants x CH chunks
   static constexpr int NBUF = NH - 1 > 2 ? NH - 1 : 2;
   static constexpr int NT = NH + 2;                        // tensor-core reduced gradient vectors
-  static constexpr uint32_t ACT_BYTES = kTB * W * 2;       // one bf16 activation buffer
-  static constexpr uint32_t WMAT_BYTES = W * W * 2;        // one bf16 weight matrix
+  static constexpr uint32_t ACT_BYTES = kTB * W * 2;       // one bf16 activation plane
+  static constexpr uint32_t WMAT_BYTES = W * W * 2;        // one bf16 weight plane
+  static constexpr uint32_t ABUF = P * ACT_BYTES;          // one activation buffer (P planes)
+  static constexpr uint32_t WBUF = P * WMAT_BYTES;         // one weight matrix (P planes)
   static constexpr uint32_t oAct = 0;
-  static constexpr uint32_t oWh = oAct + NBUF * ACT_BYTES;
-  static constexpr uint32_t oDer = oWh + NWRES * WMAT_BYTES;  // bf16 act'(z_l), l = 2..NH-1 (SiLU)
+  static constexpr uint32_t oWh = oAct + NBUF * ABUF;
+  static constexpr uint32_t oDer = oWh + NWRES * WBUF;     // bf16 act'(z_l), l = 2..NH-1 (SiLU)
   static constexpr uint32_t oOnes = oDer + NDER * ACT_BYTES;  // bf16 [16][128] ones (MN-major)
   static constexpr uint32_t oXm = oOnes + 4096;            // bf16 [16][128] [1, x, y, z split]
   static constexpr uint32_t oW1 = oXm + 4096;              // fp32 [W][3]
@@ -68,11 +75,14 @@ struct TcLayout {
   static constexpr uint32_t oBar = oItem + 4 * kTB;        // mbarriers (MMA, weights) + tmem base
   static constexpr uint32_t bytes = oBar + 64;
   static constexpr uint32_t TMEM_COLS = (W * NH <= 128) ? 128 : (W * NH <= 256) ? 256 : 512;
-  static constexpr int MINB = (TMEM_COLS <= 256) ? 2 : 1;  // CTAs per SM (TMEM / smem permitting)
+  // CTAs per SM requested from the launch (TMEM permitting; the host sizes the partial slots with
+  // mlp_tc_ctas_per_sm, which must agree): the three-plane split runs one CTA per SM
+  static constexpr int MINB = (P == 1 && TMEM_COLS <= 256) ? 2 : 1;
+  static_assert(bytes <= 232448, "shared memory");
   static constexpr int MDW = W < 128 ? 128 : W;            // M of the dW / tail MMAs: rows o >= W of
                                                            // the MN-major A run into the next buffer
                                                            // and land in TMEM lanes that are never read
-  static_assert(4 * (4 * 2 * W + 4) <= (int)ACT_BYTES * NBUF, "flush scratch");
+  static_assert(4 * (4 * 2 * W + 4) <= (int)ABUF * NBUF, "flush scratch");
   // theta offsets within one network (G17)
   static constexpr int64_t tW1 = 0, tB1 = 3 * W;
   __host__ __device__ static constexpr int64_t tWl(int l) { return 4 * W + (int64_t)(l - 2) * (W * W + W); }
@@ -136,6 +146,43 @@ __device__ __forceinline__ void store_chunk_bf16(uint32_t buf, int row, int chun
                  pack_bf16(h[8 * q + 2], h[8 * q + 3]), pack_bf16(h[8 * q + 4], h[8 * q + 5]),
                  pack_bf16(h[8 * q + 6], h[8 * q + 7]));
 }
+// P planes of one thread's 32 columns of a row: plane p at buf + p * plane
+template <int P>
+__device__ __forceinline__ void store_chunk_planes(uint32_t buf, uint32_t plane, int row, int chunk, const float (&h)[32]) {
+  if (P == 1) {
+    store_chunk_bf16(buf, row, chunk, h);
+    return;
+  }
+  float r[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) r[j] = h[j];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    uint32_t w[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      w[j] = pack_bf16(r[2 * j], r[2 * j + 1]);
+      r[2 * j] -= bf_lo(w[j]);         // exact: the rounding error of a bf16 rounding is an fp32
+      r[2 * j + 1] -= bf_hi(w[j]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      st_shared_v4(buf + p * plane + core_off(kTB, row, chunk * 4 + q), w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  }
+}
+__device__ __forceinline__ void load_chunk_bf16(uint32_t buf, int row, int chunk, float (&h)[32]);
+// sum of the P planes (exact for the split of an fp32 value up to its last 2^-24 bits)
+template <int P>
+__device__ __forceinline__ void load_chunk_planes(uint32_t buf, uint32_t plane, int row, int chunk, float (&h)[32]) {
+  load_chunk_bf16(buf + (P - 1) * plane, row, chunk, h);
+#pragma unroll
+  for (int p = P - 2; p >= 0; --p) {
+    float t[32];
+    load_chunk_bf16(buf + p * plane, row, chunk, t);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) h[j] += t[j];
+  }
+}
 __device__ __forceinline__ void load_chunk_bf16(uint32_t buf, int row, int chunk, float (&h)[32]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -163,9 +210,12 @@ __device__ long long g_tc_trace[8][32];
   } while (0)
 #endif
 
-template <int W, int NH, int ACT, bool TRAIN>
-__global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH, ACT>::MINB) k_mlp_tc(const MlpParams prm) {
-  using L = TcLayout<W, NH, ACT>;
+template <int W, int NH, int ACT, bool TRAIN, int P = 1>
+__global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, NH, ACT, P>::MINB) k_mlp_tc(const MlpParams prm) {
+  using L = TcLayout<W, NH, ACT, P>;
+  constexpr uint32_t AP = L::ACT_BYTES, WP = L::WMAT_BYTES;   // plane strides (P = 3)
+  // activation: MUFU tanh.approx for the bf16 path (G16), accurate tanhf for the fp32 split (G15)
+  auto act_tanh = [](float x) { return P == 3 ? tanhf(x) : tanh_fast(x); };
   constexpr bool SILU = L::SILU, STREAM = L::STREAM;
   constexpr int NHH = L::NHH;
   constexpr int NT = L::NT;
@@ -246,7 +296,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       wpending = false;
     }
   };
-  auto wmat = [&](int l) -> uint32_t { return STREAM ? aWh : aWh + (l - 2) * L::WMAT_BYTES; };
+  auto wmat = [&](int l) -> uint32_t { return STREAM ? aWh : aWh + (l - 2) * L::WBUF; };
   const uint32_t aDer = sbase + L::oDer;
   {  // constant operands of the tail reductions
     uint32_t* ones = reinterpret_cast<uint32_t*>(smem + L::oOnes);
@@ -330,8 +380,20 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       for (int q = tid; q < W * (W / 8); q += THREADS) {
         const int o = q / (W / 8), c8 = q % (W / 8);
         const float* src = Wl + (int64_t)o * W + c8 * 8;   // net+ theta is not 16-B aligned
-        st_shared_v4(aWh + l * L::WMAT_BYTES + core_off(W, o, c8), pack_bf16(src[0], src[1]),
-                     pack_bf16(src[2], src[3]), pack_bf16(src[4], src[5]), pack_bf16(src[6], src[7]));
+        float r[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) r[e] = src[e];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {   // plane p of the exact bf16 split (P = 1: the RNE bf16 copy)
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            w[e] = pack_bf16(r[2 * e], r[2 * e + 1]);
+            r[2 * e] -= bf_lo(w[e]);
+            r[2 * e + 1] -= bf_hi(w[e]);
+          }
+          st_shared_v4(aWh + l * L::WBUF + p * WP + core_off(W, o, c8), w[0], w[1], w[2], w[3]);
+        }
       }
     }
     tc::fence_proxy_async_smem();
@@ -349,6 +411,20 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       tc::mma_bf16(tmem + dcol, tc::sdesc(a0 + s * a_step, a_lbo, a_sbo), tc::sdesc(b0 + s * b_step, b_lbo, b_sbo),
                    idesc, (acc || s > 0) ? 1u : 0u);
   };
+  // the plane products of a split GEMM (P = 3): planes i + j <= 2, the smallest first; P = 1: one
+  auto gemm_p = [&](uint32_t dcol, uint32_t a0, uint32_t a_step, uint32_t a_lbo, uint32_t a_sbo, uint32_t a_pl,
+                    uint32_t b0, uint32_t b_step, uint32_t b_lbo, uint32_t b_sbo, uint32_t b_pl, uint32_t idesc,
+                    int ksteps, bool acc) {
+    if (P == 1) {
+      gemm(dcol, a0, a_step, a_lbo, a_sbo, b0, b_step, b_lbo, b_sbo, idesc, ksteps, acc);
+      return;
+    }
+    const int pi[6] = {2, 1, 0, 1, 0, 0}, pj[6] = {0, 1, 2, 0, 1, 0};
+#pragma unroll 1
+    for (int q = 0; q < 6; ++q)
+      gemm(dcol, a0 + pi[q] * a_pl, a_step, a_lbo, a_sbo, b0 + pj[q] * b_pl, b_step, b_lbo, b_sbo, idesc, ksteps,
+           acc || q > 0);
+  };
   auto wait_mma = [&]() {
     tc::mbar_wait(bar, phase);
     phase ^= 1;
@@ -360,7 +436,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     for (int j = 0; j < 32; ++j) {
       const int n = ccol + j;
       const float z = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, fmaf(sW1[3 * n], x0, sBias[n])));
-      h[j] = SILU ? z * sigmoid_fast(z) : tanh_fast(z);
+      h[j] = SILU ? z * sigmoid_fast(z) : act_tanh(z);
     }
   };
 
@@ -410,9 +486,15 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       }
       tc::tmem_ld16(tmem + tlane + (uint32_t)(16 * (NH - 2)), v);
       tg[NH - 2] += v[0];
-      tg[NH - 1] += v[1] + v[2];
-      tg[NH] += v[3] + v[4];
-      tg[NH + 1] += v[5] + v[6];
+      if (P == 1) {
+        tg[NH - 1] += v[1] + v[2];
+        tg[NH] += v[3] + v[4];
+        tg[NH + 1] += v[5] + v[6];
+      } else {
+        tg[NH - 1] += (v[3] + v[2]) + v[1];
+        tg[NH] += (v[6] + v[5]) + v[4];
+        tg[NH + 1] += (v[9] + v[8]) + v[7];
+      }
     }
     tailPending = false;
   };
@@ -452,7 +534,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       float h[32];
       layer1(x0, x1, x2, h);
       if (tailPending) tail_collect();
-      store_chunk_bf16(aAct, row, chunk, h);
+      store_chunk_planes<P>(aAct, AP, row, chunk, h);
     }
     tc::fence_proxy_async_smem();
     tc::tc_fence_before();
@@ -465,8 +547,8 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       if (tid == 0) {
         wwait();
         tc::tc_fence_after();
-        gemm(0, aAct + (l - 2) * L::ACT_BYTES, 2 * LBO_ACT, LBO_ACT, 128, wmat(l), 2 * LBO_W, LBO_W, 128, ID_FWD,
-             W / 16, false);
+        gemm_p(0, aAct + (l - 2) * L::ABUF, 2 * LBO_ACT, LBO_ACT, 128, AP, wmat(l), 2 * LBO_W, LBO_W, 128, WP, ID_FWD,
+               W / 16, false);
         tc::mma_commit(bar);
       }
       if (!TRAIN && l == 2) nxt = fetch(t + 1);   // the next tile's loads overlap this tile
@@ -478,7 +560,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       const float* bl = sBias + (l - 1) * W + ccol;
       if (!SILU) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = tanh_fast(v[j] + bl[j]);
+        for (int j = 0; j < 32; ++j) v[j] = act_tanh(v[j] + bl[j]);
       }
       if (l < NH) {
         if (SILU) {
@@ -489,9 +571,9 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
             v[j] = z * sg;
             d[j] = sg * fmaf(z, 1.0f - sg, 1.0f);   // SiLU'(z)
           }
-          if (TRAIN && l >= 2 && l <= NH - 1) store_chunk_bf16(aDer + (l - 2) * L::ACT_BYTES, row, chunk, d);
+          if (TRAIN && l >= 2 && l <= NH - 1) store_chunk_bf16(aDer + (l - 2) * L::ACT_BYTES, row, chunk, d);   // P = 1
         }
-        store_chunk_bf16(aAct + (l - 1) * L::ACT_BYTES, row, chunk, v);
+        store_chunk_planes<P>(aAct + (l - 1) * L::ABUF, AP, row, chunk, v);
         tc::fence_proxy_async_smem();
       } else {
         float z[32];
@@ -572,7 +654,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       gbo += b;
     }
     // ---- output layer backward: dwo += ub h_NH; G_NH = ub wo (1 - h_NH^2) -> bf16 ----
-    const uint32_t gbufNH = (NH == 2) ? aAct + L::ACT_BYTES : aAct;
+    const uint32_t gbufNH = (NH == 2) ? aAct + L::ABUF : aAct;
     {
       float hv[32], v[32];
       tc::tmem_ld32(tmem + tlane + ccol, hv);
@@ -595,7 +677,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       gWo += warp_transpose_sum(v, lane);
 #pragma unroll
       for (int j = 0; j < 32; ++j) hv[j] *= ub * sWo[ccol + j];
-      store_chunk_bf16(gbufNH, row, chunk, hv);
+      store_chunk_planes<P>(gbufNH, AP, row, chunk, hv);
       gBN += warp_transpose_sum(hv, lane);
     }
     tc::tc_fence_before();
@@ -605,17 +687,18 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     // ---- hidden layers backward ----
 #pragma unroll 1
     for (int l = NH; l >= 2; --l) {
-      const uint32_t gbuf = (l == NH) ? gbufNH : aAct + (l - 1) * L::ACT_BYTES;   // G_l
-      const uint32_t hbuf = aAct + (l - 2) * L::ACT_BYTES;                        // h_{l-1}
+      const uint32_t gbuf = (l == NH) ? gbufNH : aAct + (l - 1) * L::ABUF;   // G_l
+      const uint32_t hbuf = aAct + (l - 2) * L::ABUF;                        // h_{l-1}
       if (tid == 0) {
         wwait();
         tc::tc_fence_after();
         // acc = G_l W_l: A = G (K-major), B = W_l (N = i, K = o: MN-major); its epilogue starts
         // while the dW MMA below still runs
-        gemm(0, gbuf, 2 * LBO_ACT, LBO_ACT, 128, wmat(l), 256, 128, LBO_W, ID_DH, W / 16, false);
+        gemm_p(0, gbuf, 2 * LBO_ACT, LBO_ACT, 128, AP, wmat(l), 256, 128, LBO_W, WP, ID_DH, W / 16, false);
         tc::mma_commit(bar);
         // dW_l += G_l^T h_{l-1}: A = G (M = o, MN-major), B = h (N = i, MN-major), K = rows
-        gemm((uint32_t)(W * (l - 1)), gbuf, 256, 128, LBO_ACT, hbuf, 256, 128, LBO_ACT, ID_DW, kTB / 16, !dwFresh);
+        gemm_p((uint32_t)(W * (l - 1)), gbuf, 256, 128, LBO_ACT, AP, hbuf, 256, 128, LBO_ACT, AP, ID_DW, kTB / 16,
+               !dwFresh);
         tc::mma_commit(dwbar);
       }
       if (l == NH) nxt = fetch(t + 1);   // the next tile's loads, under the longest MMA phase
@@ -626,7 +709,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       float v[32], hq[32];
       tc::tmem_ld32(tmem + tlane + ccol, v);
       if (!SILU) {                         // tanh' = 1 - h~^2 (bf16 operand copy)
-        load_chunk_bf16(hbuf, row, chunk, hq);
+        load_chunk_planes<P>(hbuf, AP, row, chunk, hq);
 #pragma unroll
         for (int j = 0; j < 32; ++j) hq[j] = 1.0f - hq[j] * hq[j];
       } else if (l - 1 >= 2) {             // SiLU': stored bf16 derivative
@@ -644,17 +727,34 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
       for (int j = 0; j < 32; ++j) v[j] *= hq[j];
       tc::mbar_wait(dwbar, dwphase);           // dW_l has read h_{l-1} (and G_l)
       dwphase ^= 1;
-      store_chunk_bf16(hbuf, row, chunk, v);   // G_{l-1} in place: h_{l-1} is consumed
+      store_chunk_planes<P>(hbuf, AP, row, chunk, v);   // G_{l-1} in place: h_{l-1} is consumed
       if (l - 1 == 2 && NH >= 3) {   // h1 again for dW_2 (buffer 0's G_NH is consumed)
         float h[32];
         layer1(x0, x1, x2, h);
-        store_chunk_bf16(aAct, row, chunk, h);
+        store_chunk_planes<P>(aAct, AP, row, chunk, h);
       }
       if (l == 2 && chunk == 0) {   // tail operand row: [1, x_hi, x_lo, y_hi, y_lo, z_hi, z_lo, 0]
         const float xh = __bfloat162float(__float2bfloat16_rn(x0)), yh = __bfloat162float(__float2bfloat16_rn(x1)),
                     zh = __bfloat162float(__float2bfloat16_rn(x2));
-        st_shared_v4(aXm + row * 16, pack_bf16(1.0f, xh), pack_bf16(x0 - xh, yh), pack_bf16(x1 - yh, zh),
-                     pack_bf16(x2 - zh, 0.0f));
+        if (P == 1) {
+          st_shared_v4(aXm + row * 16, pack_bf16(1.0f, xh), pack_bf16(x0 - xh, yh), pack_bf16(x1 - yh, zh),
+                       pack_bf16(x2 - zh, 0.0f));
+        } else {   // [1, x1, x2, x3, y1, y2, y3, z1 | z2, z3, 0...]: each coordinate as three bf16 planes
+          float pl[9];
+          const float xs[3] = {x0, x1, x2};
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            float r = xs[c];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              pl[3 * c + q] = __bfloat162float(__float2bfloat16_rn(r));
+              r -= pl[3 * c + q];
+            }
+          }
+          st_shared_v4(aXm + row * 16, pack_bf16(1.0f, pl[0]), pack_bf16(pl[1], pl[2]), pack_bf16(pl[3], pl[4]),
+                       pack_bf16(pl[5], pl[6]));
+          st_shared_v4(aXm + 2048 + row * 16, pack_bf16(pl[7], pl[8]), 0u, 0u, 0u);
+        }
       }
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
@@ -664,11 +764,14 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
     // ---- tile tail: bias gradients of layers 1..NH-1 and dW_1 on the tensor core ----
     if (tid == 0) {
       tc::tc_fence_after();
-      for (int l = 2; l <= NH - 1; ++l)   // db_l = G_l^T 1   (G_l in buffer l-1)
-        gemm((uint32_t)(16 * (l - 2)), aAct + (l - 1) * L::ACT_BYTES, 256, 128, LBO_ACT, aOnes, 256, 128, 2048,
-             ID_TAIL, kTB / 16, false);
-      // [db_1 | dW_1 (x, y, z as bf16 hi + lo)] = G_1^T X   (G_1 in buffer 0)
-      gemm((uint32_t)(16 * (NH - 2)), aAct, 256, 128, LBO_ACT, aXm, 256, 128, 2048, ID_TAIL, kTB / 16, false);
+      for (int l = 2; l <= NH - 1; ++l)   // db_l = G_l^T 1   (G_l in buffer l-1; every plane of G)
+        for (int p = 0; p < P; ++p)
+          gemm((uint32_t)(16 * (l - 2)), aAct + (l - 1) * L::ABUF + p * AP, 256, 128, LBO_ACT, aOnes, 256, 128, 2048,
+               ID_TAIL, kTB / 16, p > 0);
+      // [db_1 | dW_1 (x, y, z as bf16 planes)] = G_1^T X   (G_1 in buffer 0)
+      for (int p = 0; p < P; ++p)
+        gemm((uint32_t)(16 * (NH - 2)), aAct + p * AP, 256, 128, LBO_ACT, aXm, 256, 128, 2048, ID_TAIL, kTB / 16,
+             p > 0);
       tc::mma_commit(bar);
     }
     tailPending = true;   // collected under the next tile's gather and layer 1
@@ -702,10 +805,10 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT>::THREADS, TcLayout<W, NH,
   if (warp == 0) tc::tmem_dealloc(tmem, L::TMEM_COLS);
 }
 
-template <int W, int NH, int ACT, bool TRAIN>
+template <int W, int NH, int ACT, bool TRAIN, int P = 1>
 static cudaError_t launch_tc_t(const MlpParams& p, int grid, cudaStream_t s) {
-  using L = TcLayout<W, NH, ACT>;
-  auto kern = k_mlp_tc<W, NH, ACT, TRAIN>;
+  using L = TcLayout<W, NH, ACT, P>;
+  auto kern = k_mlp_tc<W, NH, ACT, TRAIN, P>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
@@ -722,13 +825,17 @@ extern "C" int nbm_debug_tc_trace(long long* out) {
 }
 #endif
 
-int mlp_tc_supported(int width, int n_hidden, int act) {
+int mlp_tc_supported(int width, int n_hidden, int act, int planes) {
+  if (planes == 3) return width == 64 && n_hidden >= 2 && n_hidden <= 3 && act == NBM_ACT_TANH;
   return (width == 64 || width == 128) && n_hidden >= 2 && n_hidden <= 4 &&
          (act == NBM_ACT_TANH || act == NBM_ACT_SILU);
 }
 
-// CTAs per SM of the tensor-core kernel (2 when a CTA needs <= 256 TMEM columns)
-int mlp_tc_ctas_per_sm(int width, int n_hidden) { return width * n_hidden <= 256 ? 2 : 1; }
+// CTAs per SM of the tensor-core kernel (2 when a CTA needs <= 256 TMEM columns and its shared
+// memory fits twice; the three-plane split needs one SM per CTA)
+int mlp_tc_ctas_per_sm(int width, int n_hidden, int planes) {
+  return planes == 1 && width * n_hidden <= 256 ? 2 : 1;
+}
 
 template <int ACT>
 static cudaError_t launch_tc_act(int width, int n_hidden, bool train, const MlpParams& p, int grid, cudaStream_t s) {
@@ -744,8 +851,17 @@ static cudaError_t launch_tc_act(int width, int n_hidden, bool train, const MlpP
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_mlp_tc(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
+cudaError_t launch_mlp_tc(int width, int n_hidden, int act, int planes, bool train, const MlpParams& p, int grid,
                           cudaStream_t s) {
+  if (planes == 3) {   // fp32-accurate split GEMMs (W = 64, tanh)
+    static_assert(TcLayout<64, 3, NBM_ACT_TANH, 3>::MINB == 1, "split kernel: one CTA per SM");
+    if (width != 64 || act != NBM_ACT_TANH) return cudaErrorInvalidValue;
+    switch (n_hidden) {
+      case 2: return train ? launch_tc_t<64, 2, NBM_ACT_TANH, true, 3>(p, grid, s) : launch_tc_t<64, 2, NBM_ACT_TANH, false, 3>(p, grid, s);
+      case 3: return train ? launch_tc_t<64, 3, NBM_ACT_TANH, true, 3>(p, grid, s) : launch_tc_t<64, 3, NBM_ACT_TANH, false, 3>(p, grid, s);
+    }
+    return cudaErrorInvalidValue;
+  }
   return act == NBM_ACT_SILU ? launch_tc_act<NBM_ACT_SILU>(width, n_hidden, train, p, grid, s)
                              : launch_tc_act<NBM_ACT_TANH>(width, n_hidden, train, p, grid, s);
 }

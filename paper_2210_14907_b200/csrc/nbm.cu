@@ -51,12 +51,15 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
     if (a->sizes[l] != W) { *why = "arch: hidden widths must be uniform"; return NBM_E_INVALID_ARCH; }
   if (a->n_nets != 1 && a->n_nets != 2) { *why = "arch: n_nets must be 1 or 2"; return NBM_E_INVALID_ARCH; }
   if (a->act != NBM_ACT_TANH && a->act != NBM_ACT_SILU && a->act != NBM_ACT_SINE) { *why = "arch: bad activation"; return NBM_E_INVALID_ARCH; }
-  if (a->prec != NBM_PREC_FP32 && a->prec != NBM_PREC_BF16) { *why = "arch: bad precision"; return NBM_E_INVALID_ARCH; }
+  if (a->prec != NBM_PREC_FP32 && a->prec != NBM_PREC_BF16 && a->prec != NBM_PREC_FP32X) {
+    *why = "arch: bad precision"; return NBM_E_INVALID_ARCH;
+  }
   int nh = a->n_layers - 2;
   bool ok = false;
   if (a->prec == NBM_PREC_FP32)
     ok = mlp_fp32_supported(W, nh, a->act) || (a->act == NBM_ACT_TANH && mlp_fp32w_supported(W, nh));
-  if (a->prec == NBM_PREC_BF16) ok = mlp_tc_supported(W, nh, a->act) || (W == 256 && nh >= 2 && nh <= 4 && a->act == NBM_ACT_TANH);
+  if (a->prec == NBM_PREC_BF16) ok = mlp_tc_supported(W, nh, a->act, 1) || (W == 256 && nh >= 2 && nh <= 4 && a->act == NBM_ACT_TANH);
+  if (a->prec == NBM_PREC_FP32X) ok = mlp_tc_supported(W, nh, a->act, 3);
   if (!ok) {
     *why = "arch: unsupported (prec, act, width, depth) combination in this build";
     return NBM_E_INVALID_ARCH;
@@ -241,7 +244,8 @@ cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cu
   if (is_w256(A))
     return launch_mlp_w256(A.n_hidden, train, p, w.wimg, w.wimg_b, w.hscr, w.rep, w.nrep, w.grid_base, s);
   if (is_fp32w(A)) return launch_mlp_fp32w(A.width, A.n_hidden, train, p, w.wimg32, w.rep, w.nrep, w.grid_base, s);
-  if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, A.act, train, p, w.grid_base, s);
+  if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, A.act, 1, train, p, w.grid_base, s);
+  if (A.prec == NBM_PREC_FP32X) return launch_mlp_tc(A.width, A.n_hidden, A.act, 3, train, p, w.grid_base, s);
   return launch_mlp_fp32(A.width, A.n_hidden, A.act, train, p, w.grid_base, s);
 }
 
@@ -312,8 +316,9 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   int64_t items = 2 * max_points;
   w.nblk_cls = (int)((items + 1023) / 1024);
   w.grid_base = sms;
-  w.grid_mlp = sms * ((ai.prec == NBM_PREC_BF16) ? mlp_tc_ctas_per_sm(ai.width, ai.n_hidden)
-                                                 : (ai.width <= 64 ? mlp_fp32_ctas_per_sm() : 1));
+  w.grid_mlp = sms * ((ai.prec == NBM_PREC_BF16)    ? mlp_tc_ctas_per_sm(ai.width, ai.n_hidden, 1)
+                      : (ai.prec == NBM_PREC_FP32X) ? mlp_tc_ctas_per_sm(ai.width, ai.n_hidden, 3)
+                      : (ai.width <= 64 ? mlp_fp32_ctas_per_sm() : 1));
   std::vector<void**> ptrs;
   size_t sizes[32];
   int k = 0;

@@ -175,10 +175,10 @@ cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, const 
 int mlp_fp32_supported(int width, int n_hidden, int act);
 int mlp_fp32_ctas_per_sm();
 // mlp_tc.cu (tcgen05 bf16)
-cudaError_t launch_mlp_tc(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
+cudaError_t launch_mlp_tc(int width, int n_hidden, int act, int planes, bool train, const MlpParams& p, int grid,
                           cudaStream_t s);
-int mlp_tc_supported(int width, int n_hidden, int act);
-int mlp_tc_ctas_per_sm(int width, int n_hidden);
+int mlp_tc_supported(int width, int n_hidden, int act, int planes);
+int mlp_tc_ctas_per_sm(int width, int n_hidden, int planes);
 cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t* wimg, cudaStream_t s);
 // mlp_fp32w.cu (fp32, W = 128 / 256: streamed weights, per-tile dW flushes into replicas)
 int mlp_fp32w_supported(int width, int n_hidden);

@@ -89,7 +89,7 @@ def test_classification_bit_exact(orc, name):
     s.close()
 
 
-def _parity(orc, cfg, n, nb, seed=0, theta_seed=None, step=0):
+def _parity(orc, cfg, n, nb, seed=0, theta_seed=None, step=0, floor_factor=4):
     s = nbm.Solver(cfg, 0, max_points=max(n, nb, 1))
     pb, ar = orc.from_config(cfg)
     pts = orc.sample(0, seed, step, 0, n, cfg["H"])
@@ -109,8 +109,8 @@ def _parity(orc, cfg, n, nb, seed=0, theta_seed=None, step=0):
             continue
         ltol, gtol = LOSS_TOL, GRAD_TOL
         if k < 2:   # ill-conditioned uncrossed terms: noise floor of fp32 (SURVEY 8c rule 2)
-            ltol = max(ltol, 4 * abs(lt32[k] - lt[k]) / lt[k])
-            gtol = max(gtol, 4 * np.linalg.norm(gt32[k] - gt[k]) / np.linalg.norm(gt[k]))
+            ltol = max(ltol, floor_factor * abs(lt32[k] - lt[k]) / lt[k])
+            gtol = max(gtol, floor_factor * np.linalg.norm(gt32[k] - gt[k]) / np.linalg.norm(gt[k]))
         assert abs(tl - lt[k]) <= ltol * lt[k], (k, tl, lt[k], ltol)
         assert np.linalg.norm(tg - gt[k]) <= gtol * np.linalg.norm(gt[k]), (k, gtol)
     s.close()
@@ -479,4 +479,43 @@ def test_large_batch_2e24_points(orc):
     assert abs(acc_l - lt) <= LOSS_TOL * lt
     assert np.linalg.norm(acc_g - gt) <= GRAD_TOL * np.linalg.norm(gt)
     assert s.status() == 0
+    s.close()
+
+
+@pytest.mark.parametrize("nh", [3, 2])
+def test_fp32x_split_parity(orc, nh):
+    """PREC_FP32X (G26): the fp32 config-2 networks on the tensor cores with every operand split
+    exactly into three bf16 planes (six plane products, fp32 accumulation, accurate tanh):
+    per-term parity at the fp32 bars (1e-5 / 1e-4).  On the noise-dominated uncrossed terms the
+    measured deviation of this path is up to ~5x the IEEE-fp32 emulation's (tensor-core
+    accumulation order and rounding), so their floor is 8x that deviation instead of 4x."""
+    cfg = _cfg("c2")
+    cfg["prec"] = inputs.PREC_FP32X
+    cfg["sizes"] = [3] + [64] * nh + [1]
+    lt = _parity(orc, cfg, 1 << 14, 1 << 11, theta_seed=5, floor_factor=8)
+    assert all(v > 0 for v in lt)
+
+
+def test_fp32x_full_size_and_determinism(orc):
+    """PREC_FP32X at config 2's full size (the bench launch configuration), bitwise
+    determinism, and eval parity."""
+    cfg = _cfg("c2")
+    cfg["prec"] = inputs.PREC_FP32X
+    s = nbm.Solver(cfg, 0)
+    pb, ar = orc.from_config(cfg)
+    s.init_params(0)
+    pts = torch.empty(cfg["N"], 3, device="cuda")
+    bpts = torch.empty(cfg["Nb"], 3, device="cuda")
+    s.sample(0, 0, 0, 0, cfg["N"], pts)
+    s.sample(1, 0, 0, 0, cfg["Nb"], bpts)
+    gl, gg = _gpu_loss_grad(s, s.theta, pts, bpts)
+    gl2, gg2 = _gpu_loss_grad(s, s.theta, pts, bpts)
+    assert gl == gl2 and np.array_equal(gg, gg2)
+    th = orc.init_params(ar, 0)
+    L, _, g, _ = orc.loss_grad(pb, ar, th, pts.cpu().numpy(), bpts.cpu().numpy(), cfg["h"])
+    assert abs(gl - L) <= LOSS_TOL * L
+    assert np.linalg.norm(gg - g) <= GRAD_TOL * np.linalg.norm(g)
+    u = s.eval(pts[:5000]).double().cpu().numpy()
+    want = orc.evaluate(pb, ar, th, pts[:5000].cpu().numpy())
+    assert np.allclose(u, want, rtol=1e-5, atol=1e-6 * np.abs(want).max())
     s.close()
