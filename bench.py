@@ -47,6 +47,8 @@ def kernel_name(cfg):
         return "k_mlp_fp32w" if w >= 128 else "k_mlp_fp32"
     if cfg["prec"] == inputs.PREC_FP32X:
         return "k_mlp_tc<P=3> (tcgen05, 3-plane bf16 split)"
+    if cfg.get("stencil", 0) == inputs.STENCIL_STABLE:
+        return "k_mlp_tc<STAB> (tcgen05, difference propagation)"
     return "k_mlp_w256 (tcgen05 cta_group::2)" if w == 256 else "k_mlp_tc (tcgen05)"
 
 
@@ -188,6 +190,8 @@ def main():
     ap.add_argument("--levels", type=int, default=1,
                     help="multi-resolution levels h0/2^l of the loss (S:348; the paper's scaling runs use 3)")
     ap.add_argument("--points", type=int, default=None, help="override interior points per GPU")
+    ap.add_argument("--stencil", default="direct", choices=["direct", "stable"],
+                    help="uncrossed stencil evaluation: 7 network values or difference propagation (G27; bf16 tanh)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -197,9 +201,10 @@ def main():
     cfg = inputs.config(args.config, width=args.width, prec=prec)
     if args.grid:
         cfg = inputs.with_grid(cfg, args.grid)
+    cfg["stencil"] = inputs.STENCIL_STABLE if args.stencil == "stable" else inputs.STENCIL_DIRECT
     cfg["label"] = cfg["name"] + (f"-w{cfg['sizes'][1]}" if cfg["name"] == "c5" else "") + \
         ("" if prec is None else {inputs.PREC_FP32: "-fp32", inputs.PREC_BF16: "-bf16", inputs.PREC_FP32X: "-fp32x"}[prec]) + \
-        (f"-grid{args.grid}" if args.grid else "")
+        (f"-grid{args.grid}" if args.grid else "") + ("-stable" if args.stencil == "stable" else "")
     if args.points:
         cfg["N"] = args.points
         cfg["Nb"] = max(1, args.points // 8)
@@ -375,7 +380,7 @@ def main():
         "data": "synthetic (seeded Philox lattice points; manufactured two-phase Poisson)",
         "config": {"workload": cfg["label"], "points_per_gpu": N, "boundary_per_gpu": Nb,
                    "global_points": Ng, "mlp": "x".join(map(str, cfg["sizes"])), "n_nets": cfg["n_nets"],
-                   "h": cfg["h"], "levels": args.levels, "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
+                   "h": cfg["h"], "levels": args.levels, "stencil": args.stencil, "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      **({"measured_ffma_3reg_peak": FP32_FFMA_3REG_MEASURED_TFLOPS,
                          "frac_of_measured_ffma": achieved / FP32_FFMA_3REG_MEASURED_TFLOPS}

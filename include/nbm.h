@@ -73,6 +73,15 @@ extern "C" {
                              * i + j <= 2 summed in fp32 (relative error <= ~2^-22 per product),
                              * accurate tanh, everything else fp32 (G26); W = 64, 2-3 hidden layers */
 
+/* evaluation of the uncrossed 7-point stencil (G27) */
+#define NBM_STENCIL_DIRECT 0  /* the 7 network values, r = u + c_hat sum_j u_j - b/d */
+#define NBM_STENCIL_STABLE 1  /* the same r through difference propagation: every hidden layer carries
+                               * the centre activation, the first differences a(x + h e_d) - a(x) and
+                               * the second differences a(x + h e_d) + a(x - h e_d) - 2 a(x) (tanh
+                               * addition theorem, no cancellation), r = (k/d) u + c_hat sum_d D_d u
+                               * - b/d; resolves r in bf16 at small h.  BF16 tanh, W in {64, 128};
+                               * crossed and boundary rows are evaluated directly */
+
 #define NBM_POINTS_INTERIOR 0
 #define NBM_POINTS_BOUNDARY 1
 
@@ -128,6 +137,7 @@ typedef struct nbm_arch {
   int act;                       /* NBM_ACT_* */
   int prec;                      /* NBM_PREC_* */
   int n_nets;                    /* 1 (shared) or 2 (net-, net+) */
+  int stencil;                   /* NBM_STENCIL_* (0 = direct) */
 } nbm_arch;
 
 typedef struct nbm_handle nbm_handle;

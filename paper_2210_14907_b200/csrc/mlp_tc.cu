@@ -37,6 +37,7 @@ namespace {
 
 constexpr int kTB = 128;   // rows per tile (= MMA M = TMEM lanes)
 constexpr int kTPT = 18;   // stencil points per tile
+constexpr int kTPTS = 16;  // stencil points per tile of the stable form (G27): 8 rows per point
 
 // P = 1: bf16 operands (G16).  P = 3: fp32-accurate GEMMs for the fp32 configs -- every operand
 // is split exactly into three bf16 planes x = x1 + x2 + x3 (x1 = bf16(x), x2 = bf16(x - x1),
@@ -131,6 +132,92 @@ __device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
   return v[0];
 }
 
+// ---- stable stencil evaluation (G27): difference propagation ----
+// Row roles on a stencil tile (point k at rows 8k..8k+7, one lane octet of a warp): 0 the
+// centre activation a, 1..3 the first differences P_d = a(x + h e_d) - a(x), 4..6 the second
+// differences Q_d = a(x + h e_d) + a(x - h e_d) - 2 a(x), 7 padding (zero).
+// tanh(d) - d: odd Taylor series to d^7 below 1/4 (truncation < 2e-5 relative, under the bf16
+// rounding of the rows), MUFU tanh above (rare: |d| is O(h) on the difference rows).  Both are
+// computed and selected: a branch per element would serialise the unrolled column loop
+__device__ __forceinline__ float tanh_minus_id(float d) {
+  const float d2 = d * d;
+  const float s = fmaf(d2, fmaf(d2, -17.0f / 315.0f, 2.0f / 15.0f), -1.0f / 3.0f) * (d * d2);
+  return fabsf(d) < 0.25f ? s : tanh_fast(d) - d;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// g(d) = tanh(z + d) - tanh(z) - (1 - t^2) d = s2 [(tanh d - d) - t tanh(d) d] / (1 + t tanh d)
+// with s2 = 1 - t^2 (tanh addition theorem)
+__device__ __forceinline__ float stab_g(float t, float s2, float d) {
+  const float s = tanh_minus_id(d), x = t * (d + s);
+  return s2 * fmaf(-x, d, s) * rcp_approx(1.0f + x);
+}
+// Role masks of a lane (0/1): the maps below are written branch-free (a select chain per element
+// compiles to branches, which serialise the unrolled column loop and guard every shuffle)
+struct StabRole {
+  int base, pl, partner;
+  float cC, cP, cQ, cPQ;
+  __device__ __forceinline__ explicit StabRole(int lane) {
+    const int jr = lane & 7;
+    const bool isP = jr >= 1 && jr < 4, isQ = jr >= 4 && jr < 7;
+    base = lane & ~7;
+    pl = base + (isQ ? jr - 3 : jr);                         // the P_d lane of this row's axis
+    partner = base + (isP ? jr + 3 : isQ ? jr - 3 : jr);     // P_d <-> Q_d
+    cC = jr == 0 ? 1.0f : 0.0f;
+    cP = isP ? 1.0f : 0.0f;
+    cQ = isQ ? 1.0f : 0.0f;
+    cPQ = cP + cQ;
+  }
+};
+// forward map of one 32-column chunk: v = the row's pre-activation without bias (z - b for the
+// centre, p_d, D_d); bl = the layer's bias.  a = tanh z, P = (1 - t^2) p + g(p),
+// Q = (1 - t^2) D + g(p) + g(D - p).  t from MUFU tanh.approx as on the direct path: its
+// 2^-11 error moves 1 - t^2 of saturated units by ~2^-10 absolute, below the bf16 rounding
+// of the rows (the GPU results agree with the exact-tanh emulation, test_gpu_stable)
+__device__ __forceinline__ void stab_fwd(float (&v)[32], const float* bl, int lane) {
+  const StabRole R(lane);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float t = tanh_fast(__shfl_sync(0xffffffffu, v[j] + bl[j], R.base));
+    const float s2 = fmaf(-t, t, 1.0f);
+    const float pv = __shfl_sync(0xffffffffu, v[j], R.pl);
+    const float g = stab_g(t, s2, fmaf(-R.cQ, pv, R.cPQ * v[j]));   // p, D - p; 0 on centre / pad
+    const float gp = __shfl_sync(0xffffffffu, g, R.pl);
+    v[j] = fmaf(R.cC, t, fmaf(R.cQ, gp, R.cPQ * fmaf(s2, v[j], g)));
+  }
+}
+// backward map: v = upstream gradients of the row (g_a, g_P or g_Q), hq = the row's activation
+// copy (t, P or Q).  With M = Q - P:  g_z = g_a (1 - t^2) - sum_d [g_P P (2t + P)
+// + g_Q (2tQ + P^2 + M^2)],  g_p = g_P (1 - (t + P)^2) + g_Q (M - P)(2t + M + P),
+// g_D = g_Q (1 - (t + M)^2)   (oracle/stable_stencil.py, pinned against the plain gradient)
+__device__ __forceinline__ void stab_bwd(float (&v)[32], const float (&hq)[32], int lane) {
+  const StabRole R(lane);
+  const uint32_t qm = R.cQ != 0.0f ? 0xffffffffu : 0u;   // bit select (LOP3), not a branch
+  auto sel = [qm](float a, float b) { return __uint_as_float((__float_as_uint(a) & qm) | (__float_as_uint(b) & ~qm)); };
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float t = __shfl_sync(0xffffffffu, hq[j], R.base);
+    const float ho = __shfl_sync(0xffffffffu, hq[j], R.partner);
+    const float go = __shfl_sync(0xffffffffu, v[j], R.partner);
+    const float pv = sel(ho, hq[j]), qv = sel(hq[j], ho);
+    const float gP = sel(go, v[j]), gQ = sel(v[j], go);
+    const float m = qv - pv, t2 = t + t;
+    const float cp = gP * pv * (t2 + pv), cq = gQ * fmaf(t2, qv, fmaf(pv, pv, m * m));
+    float c = fmaf(R.cP, cp, R.cQ * cq);
+    c += __shfl_xor_sync(0xffffffffu, c, 4);
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    const float tp = t + pv, tm = t + m;
+    const float oC = fmaf(v[j], fmaf(-t, t, 1.0f), -c);
+    const float oP = fmaf(gP, fmaf(-tp, tp, 1.0f), gQ * (m - pv) * (t2 + m + pv));
+    const float oQ = gQ * fmaf(-tm, tm, 1.0f);
+    v[j] = fmaf(R.cC, oC, fmaf(R.cP, oP, R.cQ * oQ));
+  }
+}
+
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -210,9 +297,12 @@ __device__ long long g_tc_trace[8][32];
   } while (0)
 #endif
 
-template <int W, int NH, int ACT, bool TRAIN, int P = 1>
+// STAB: stencil tiles in the stable difference form (G27; bf16, tanh, training pass only)
+template <int W, int NH, int ACT, bool TRAIN, int P = 1, bool STAB = false>
 __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, NH, ACT, P>::MINB) k_mlp_tc(const MlpParams prm) {
   using L = TcLayout<W, NH, ACT, P>;
+  static_assert(!STAB || (P == 1 && ACT == NBM_ACT_TANH && TRAIN), "stable form: bf16 tanh training pass");
+  constexpr int TPT = STAB ? kTPTS : kTPT;   // stencil points per tile
   constexpr uint32_t AP = L::ACT_BYTES, WP = L::WMAT_BYTES;   // plane strides (P = 3)
   // activation: MUFU tanh.approx for the bf16 path (G16), accurate tanhf for the fp32 split (G15)
   auto act_tanh = [](float x) { return P == 3 ? tanhf(x) : tanh_fast(x); };
@@ -246,7 +336,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
     int c = prm.counts[prm.cnt_slot[tid]];
     segCnt[tid] = c;
     segStart[tid] = prm.start_slot[tid] >= 0 ? prm.counts[prm.start_slot[tid]] : 0;
-    int per = prm.seg.kind[tid] == kSegStencil ? kTPT : kTB;
+    int per = prm.seg.kind[tid] == kSegStencil ? TPT : kTB;
     segTiles[tid] = (c + per - 1) / per;
   }
   if (tid == 0) {
@@ -430,8 +520,18 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
     phase ^= 1;
     tc::tc_fence_after();
   };
-  // layer 1 for this thread's 32 columns: h = tanh(W1 x + b1)
-  auto layer1 = [&](float x0, float x1, float x2, float (&h)[32]) {
+  // layer 1 for this thread's 32 columns: h = tanh(W1 x + b1); on a stable-form tile the row
+  // input is x (centre), h e_d (P_d rows) or 0 (Q_d rows, pad) and the bias enters the centre only
+  auto layer1 = [&](float x0, float x1, float x2, float (&h)[32], bool stab) {
+    if (STAB && stab) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = ccol + j;
+        h[j] = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, sW1[3 * n] * x0));
+      }
+      stab_fwd(h, sBias + ccol, lane);
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int n = ccol + j;
@@ -449,7 +549,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
     int sg = 0;
     while (tt >= firstTile[sg + 1]) ++sg;
     const int knd = prm.seg.kind[sg];
-    const int pr = knd == kSegStencil ? kTPT : kTB;
+    const int pr = knd == kSegStencil ? TPT : kTB;
     const int fst = (tt - firstTile[sg]) * pr;
     const int nv = min(pr, segCnt[sg] - fst);
     const int* its = prm.seg.items[sg] + segStart[sg];
@@ -457,7 +557,15 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       f.item = its[fst + tid];
       f.aux = prm.aux_by_item[sg] ? prm.seg.aux[sg][f.item] : prm.seg.aux[sg][segStart[sg] + fst + tid];
     }
-    if (knd == kSegStencil) {
+    if (STAB && knd == kSegStencil) {   // row 8k + jr: x, h e_1..3 (P_d), 0 (Q_d, pad)
+      const int k = tid >> 3, jr = tid & 7;
+      if (k < nv && jr == 0) {
+        const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + k];
+        f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
+      } else if (k < nv && jr < 4) {
+        if (jr == 1) f.x0 = prm.h; else if (jr == 2) f.x1 = prm.h; else f.x2 = prm.h;
+      }
+    } else if (knd == kSegStencil) {
       const int j = tid / kTPT, p = tid - j * kTPT;
       if (j < 7 && p < nv) {
         const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + p];
@@ -504,9 +612,11 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
     while (t >= firstTile[seg + 1]) ++seg;
     const int kind = prm.seg.kind[seg], net = prm.seg.net[seg];
     const int lt = t - firstTile[seg];
-    const int per = kind == kSegStencil ? kTPT : kTB;
+    const int per = kind == kSegStencil ? TPT : kTB;
     const int first = lt * per;
     const int nvalid = min(per, segCnt[seg] - first);
+    const bool stab = STAB && kind == kSegStencil;                 // warp-uniform
+    const bool centre = !stab || (row & 7) == 0;                   // rows that carry the biases
     if (net != curNet) {
       if (tailPending) {
         tail_collect();
@@ -532,7 +642,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
     const float x0 = sX[4 * row], x1 = sX[4 * row + 1], x2 = sX[4 * row + 2];
     {  // ---- layer 1 -> bf16 h1 (buffer 0; the previous tile's tail MMAs may still read it) ----
       float h[32];
-      layer1(x0, x1, x2, h);
+      layer1(x0, x1, x2, h, stab);
       if (tailPending) tail_collect();
       store_chunk_planes<P>(aAct, AP, row, chunk, h);
     }
@@ -558,7 +668,9 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       float v[32];
       tc::tmem_ld32(tmem + tlane + ccol, v);
       const float* bl = sBias + (l - 1) * W + ccol;
-      if (!SILU) {
+      if (STAB && stab) {
+        stab_fwd(v, bl, lane);
+      } else if (!SILU) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = act_tanh(v[j] + bl[j]);
       }
@@ -601,7 +713,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       float u = sUp[tid];
 #pragma unroll
       for (int c = 1; c < L::CH; ++c) u += sUp[c * kTB + tid];
-      u += sWo[W];
+      if (!stab || (tid & 7) == 0) u += sWo[W];   // differences carry no output bias
       if (!TRAIN && tid < nvalid) prm.u_out[sItem[tid]] = u;
       sU[tid] = u;
     }
@@ -612,7 +724,21 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       continue;
     }
     // ---- residual epilogue -> cotangents (S4) ----
-    if (kind == kSegStencil) {
+    if (stab) {   // r = c_c u + c_hat sum_d DU_d - b/d (G27); cotangents c_c 2r/N (centre), c_hat 2r/N (Q_d)
+      if (tid < kTB) {
+        const int k = tid >> 3, jr = tid & 7;
+        float ub = 0.0f;
+        if (k < nvalid) {
+          const float chat = prm.seg.chat[seg], cc = prm.seg.ccen[seg];
+          const float du = (sU[8 * k + 4] + sU[8 * k + 5]) + sU[8 * k + 6];
+          const float r = fmaf(cc, sU[8 * k], chat * du) - sAux[k];
+          if (jr == 0) lossAcc += 0.5 * (double)prm.two_over_n * (double)r * (double)r;
+          const float rc = prm.two_over_n * r;
+          ub = jr == 0 ? rc * cc : (jr >= 4 && jr < 7) ? rc * chat : 0.0f;
+        }
+        sUb[tid] = ub;
+      }
+    } else if (kind == kSegStencil) {
       if (tid < kTPT) {
         float r = 0.0f;
         if (tid < nvalid) {
@@ -648,7 +774,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
     TR(9);
     const float ub = sUb[row];
     if (chunk == 0) {   // output bias
-      float b = ub;
+      float b = centre ? ub : 0.0f;
 #pragma unroll
       for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
       gbo += b;
@@ -665,6 +791,14 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
           v[j] = z * sg;
           hv[j] = sg * fmaf(z, 1.0f - sg, 1.0f);
         }
+      } else if (STAB && stab) {   // G_NH = the backward map of (ub wo) through the last activation
+        float a[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          v[j] = a[j] = hv[j];
+          hv[j] = ub * sWo[ccol + j];
+        }
+        stab_bwd(hv, a, lane);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -675,9 +809,15 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] *= ub;
       gWo += warp_transpose_sum(v, lane);
+      if (!(STAB && stab)) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) hv[j] *= ub * sWo[ccol + j];
+        for (int j = 0; j < 32; ++j) hv[j] *= ub * sWo[ccol + j];
+      }
       store_chunk_planes<P>(gbufNH, AP, row, chunk, hv);
+      if (!centre) {   // b_NH: centre rows only
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hv[j] = 0.0f;
+      }
       gBN += warp_transpose_sum(hv, lane);
     }
     tc::tc_fence_before();
@@ -708,7 +848,12 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       // G_{l-1} = acc * (1 - h~^2), h~ = the bf16 operand copy of h_{l-1} (own row, chunk)
       float v[32], hq[32];
       tc::tmem_ld32(tmem + tlane + ccol, v);
-      if (!SILU) {                         // tanh' = 1 - h~^2 (bf16 operand copy)
+      if (STAB && stab) {                  // the backward map of the difference form (G27)
+        load_chunk_bf16(hbuf, row, chunk, hq);
+        stab_bwd(v, hq, lane);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hq[j] = 1.0f;
+      } else if (!SILU) {                  // tanh' = 1 - h~^2 (bf16 operand copy)
         load_chunk_planes<P>(hbuf, AP, row, chunk, hq);
 #pragma unroll
         for (int j = 0; j < 32; ++j) hq[j] = 1.0f - hq[j] * hq[j];
@@ -730,15 +875,20 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       store_chunk_planes<P>(hbuf, AP, row, chunk, v);   // G_{l-1} in place: h_{l-1} is consumed
       if (l - 1 == 2 && NH >= 3) {   // h1 again for dW_2 (buffer 0's G_NH is consumed)
         float h[32];
-        layer1(x0, x1, x2, h);
+        layer1(x0, x1, x2, h, stab);
         store_chunk_planes<P>(aAct, AP, row, chunk, h);
       }
       if (l == 2 && chunk == 0) {   // tail operand row: [1, x_hi, x_lo, y_hi, y_lo, z_hi, z_lo, 0]
         const float xh = __bfloat162float(__float2bfloat16_rn(x0)), yh = __bfloat162float(__float2bfloat16_rn(x1)),
                     zh = __bfloat162float(__float2bfloat16_rn(x2));
-        if (P == 1) {
-          st_shared_v4(aXm + row * 16, pack_bf16(1.0f, xh), pack_bf16(x0 - xh, yh), pack_bf16(x1 - yh, zh),
+        if (P == 1) {   // the bias column is 1 on the rows that carry biases (centre rows, G27)
+          const float cm = centre ? 1.0f : 0.0f;
+          st_shared_v4(aXm + row * 16, pack_bf16(cm, xh), pack_bf16(x0 - xh, yh), pack_bf16(x1 - yh, zh),
                        pack_bf16(x2 - zh, 0.0f));
+          if (STAB) {   // ones operand of db_2..db_{NH-1}: the same row mask
+            const uint32_t m2 = pack_bf16(cm, cm);
+            st_shared_v4(aOnes + row * 16, m2, m2, m2, m2);
+          }
         } else {   // [1, x1, x2, x3, y1, y2, y3, z1 | z2, z3, 0...]: each coordinate as three bf16 planes
           float pl[9];
           const float xs[3] = {x0, x1, x2};
@@ -805,10 +955,10 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
   if (warp == 0) tc::tmem_dealloc(tmem, L::TMEM_COLS);
 }
 
-template <int W, int NH, int ACT, bool TRAIN, int P = 1>
+template <int W, int NH, int ACT, bool TRAIN, int P = 1, bool STAB = false>
 static cudaError_t launch_tc_t(const MlpParams& p, int grid, cudaStream_t s) {
   using L = TcLayout<W, NH, ACT, P>;
-  auto kern = k_mlp_tc<W, NH, ACT, TRAIN, P>;
+  auto kern = k_mlp_tc<W, NH, ACT, TRAIN, P, STAB>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
@@ -851,8 +1001,28 @@ static cudaError_t launch_tc_act(int width, int n_hidden, bool train, const MlpP
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_mlp_tc(int width, int n_hidden, int act, int planes, bool train, const MlpParams& p, int grid,
-                          cudaStream_t s) {
+// training pass with the stencil tiles in the stable difference form (G27): bf16, tanh
+static cudaError_t launch_tc_stab(int width, int n_hidden, const MlpParams& p, int grid, cudaStream_t s) {
+  constexpr int T = NBM_ACT_TANH;
+#define NBM_TC_SCASES(WW)                                                  \
+  switch (n_hidden) {                                                      \
+    case 2: return launch_tc_t<WW, 2, T, true, 1, true>(p, grid, s);       \
+    case 3: return launch_tc_t<WW, 3, T, true, 1, true>(p, grid, s);       \
+    case 4: return launch_tc_t<WW, 4, T, true, 1, true>(p, grid, s);       \
+  }
+  if (width == 128) { NBM_TC_SCASES(128) }
+  if (width == 64) { NBM_TC_SCASES(64) }
+#undef NBM_TC_SCASES
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_mlp_tc(int width, int n_hidden, int act, int planes, bool train, bool stable,
+                          const MlpParams& p, int grid, cudaStream_t s) {
+  if (stable) {
+    if (!train) return launch_mlp_tc(width, n_hidden, act, planes, false, false, p, grid, s);   // no stencil rows
+    if (planes != 1 || act != NBM_ACT_TANH) return cudaErrorInvalidValue;
+    return launch_tc_stab(width, n_hidden, p, grid, s);
+  }
   if (planes == 3) {   // fp32-accurate split GEMMs (W = 64, tanh)
     static_assert(TcLayout<64, 3, NBM_ACT_TANH, 3>::MINB == 1, "split kernel: one CTA per SM");
     if (width != 64 || act != NBM_ACT_TANH) return cudaErrorInvalidValue;

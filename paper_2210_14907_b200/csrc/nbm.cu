@@ -64,6 +64,15 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
     *why = "arch: unsupported (prec, act, width, depth) combination in this build";
     return NBM_E_INVALID_ARCH;
   }
+  if (a->stencil != NBM_STENCIL_DIRECT && a->stencil != NBM_STENCIL_STABLE) {
+    *why = "arch: bad stencil evaluation";
+    return NBM_E_INVALID_ARCH;
+  }
+  if (a->stencil == NBM_STENCIL_STABLE &&
+      !(a->prec == NBM_PREC_BF16 && a->act == NBM_ACT_TANH && mlp_tc_supported(W, nh, a->act, 1))) {
+    *why = "arch: the stable stencil form needs BF16 tanh with W in {64, 128} (G27)";
+    return NBM_E_INVALID_ARCH;
+  }
   if (out) {
     memset(out, 0, sizeof(*out));
     out->n_layers = a->n_layers;
@@ -72,6 +81,7 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
     out->act = a->act;
     out->prec = a->prec;
     out->n_nets = a->n_nets;
+    out->stencil = a->stencil;
     int64_t p = 0;
     for (int l = 0; l < a->n_layers; ++l) out->sizes[l] = a->sizes[l];
     for (int l = 1; l < a->n_layers; ++l) p += (int64_t)a->sizes[l] * a->sizes[l - 1] + a->sizes[l];
@@ -244,8 +254,9 @@ cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cu
   if (is_w256(A))
     return launch_mlp_w256(A.n_hidden, train, p, w.wimg, w.wimg_b, w.hscr, w.rep, w.nrep, w.grid_base, s);
   if (is_fp32w(A)) return launch_mlp_fp32w(A.width, A.n_hidden, train, p, w.wimg32, w.rep, w.nrep, w.grid_base, s);
-  if (A.prec == NBM_PREC_BF16) return launch_mlp_tc(A.width, A.n_hidden, A.act, 1, train, p, w.grid_base, s);
-  if (A.prec == NBM_PREC_FP32X) return launch_mlp_tc(A.width, A.n_hidden, A.act, 3, train, p, w.grid_base, s);
+  if (A.prec == NBM_PREC_BF16)
+    return launch_mlp_tc(A.width, A.n_hidden, A.act, 1, train, A.stencil == NBM_STENCIL_STABLE, p, w.grid_base, s);
+  if (A.prec == NBM_PREC_FP32X) return launch_mlp_tc(A.width, A.n_hidden, A.act, 3, train, false, p, w.grid_base, s);
   return launch_mlp_fp32(A.width, A.n_hidden, A.act, train, p, w.grid_base, s);
 }
 
@@ -523,6 +534,7 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
     pm.seg.aux[s0] = w.list_aux;
     double bs = P.beta[side], d = side ? dpl : dm;
     pm.seg.chat[s0] = (float)((-bs / (hd * hd)) / d);
+    pm.seg.ccen[s0] = (float)(P.k[side] / d);
     pm.seg.kind[s0 + 1] = kSegXRows;
     pm.seg.net[s0 + 1] = net;
     pm.cnt_slot[s0 + 1] = 12 + k;

@@ -68,6 +68,7 @@ struct SegTable {
   const float* aux[kNumSeg];   // per-list-position scalar (rhs_hat / g / cotangent)
   float a[kNumSeg];            // boundary: 2 lambda_b / N_b,global
   float chat[kNumSeg];         // stencil: arm coefficient / diagonal (uncrossed row)
+  float ccen[kNumSeg];         // stencil, stable form (G27): k / diagonal = 1 + 6 chat, in fp64
 };
 
 struct Workspace {
@@ -110,6 +111,7 @@ struct Workspace {
 
 struct ArchInfo {
   int n_layers, width, n_hidden, act, prec, n_nets;
+  int stencil;          // NBM_STENCIL_*
   int sizes[kMaxLayers];
   int64_t p_net;        // parameters per network
 };
@@ -175,8 +177,8 @@ cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, const 
 int mlp_fp32_supported(int width, int n_hidden, int act);
 int mlp_fp32_ctas_per_sm();
 // mlp_tc.cu (tcgen05 bf16)
-cudaError_t launch_mlp_tc(int width, int n_hidden, int act, int planes, bool train, const MlpParams& p, int grid,
-                          cudaStream_t s);
+cudaError_t launch_mlp_tc(int width, int n_hidden, int act, int planes, bool train, bool stable,
+                          const MlpParams& p, int grid, cudaStream_t s);
 int mlp_tc_supported(int width, int n_hidden, int act, int planes);
 int mlp_tc_ctas_per_sm(int width, int n_hidden, int planes);
 cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t* wimg, cudaStream_t s);

@@ -18,6 +18,7 @@ SRC_SINE3PI, SRC_PAIR, SRC_GAUSS, SRC_PAPER41 = 0, 1, 2, 4
 MU_CONST, MU_PAPER41, MU_LINEAR = 0, 1, 2
 ACT_TANH, ACT_SILU, ACT_SINE = 0, 1, 2
 PREC_FP32, PREC_BF16, PREC_FP32X = 0, 1, 2
+STENCIL_DIRECT, STENCIL_STABLE = 0, 1
 
 
 def h_lattice(h: float) -> int:

@@ -23,6 +23,7 @@ LS_NONE, LS_SPHERES, LS_STAR, LS_PLANE = 0, 1, 2, 3
 SRC_SINE3PI, SRC_PAIR, SRC_GAUSS = 0, 1, 2
 ACT_TANH, ACT_SILU = 0, 1
 PREC_FP32, PREC_BF16 = 0, 1
+STENCIL_DIRECT, STENCIL_STABLE = 0, 1   # NBM_STENCIL_* (G27)
 POINTS_INTERIOR, POINTS_BOUNDARY = 0, 1
 TERM_UNX_MINUS, TERM_UNX_PLUS, TERM_CROSSED, TERM_BOUNDARY, TERM_ALL = 1, 2, 4, 8, 15
 
@@ -51,7 +52,7 @@ class nbm_problem(C.Structure):
 
 class nbm_arch(C.Structure):
     _fields_ = [("n_layers", C.c_int), ("sizes", C.POINTER(C.c_int)), ("act", C.c_int),
-                ("prec", C.c_int), ("n_nets", C.c_int)]
+                ("prec", C.c_int), ("n_nets", C.c_int), ("stencil", C.c_int)]
 
 
 _lib = None
@@ -146,6 +147,7 @@ class Descriptors:
         a.act = cfg["act"]
         a.prec = cfg["prec"]
         a.n_nets = cfg["n_nets"]
+        a.stencil = int(cfg.get("stencil", STENCIL_DIRECT))
         self.problem, self.arch = p, a
 
 
