@@ -843,6 +843,38 @@ void orc_eval(const orc_problem* pb, const orc_arch* a, const double* theta,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Error norms on the evaluation grid (Table 1): over all     */
+/* (M+1)^3 nodal points p of the box, e(p) = u_{side(p)}(p) - u*_{side(p)}(p),   */
+/* rmse = sqrt(mean e^2), linf = max |e|.  Nodal coordinates lo + (hi-lo) i/M    */
+/* in fp64, rounded to fp32 (the points the networks see), x fastest.    */
+/* Returns -1 when the problem has no closed-form solution.                      */
+/* ------------------------------------------------------------------------ */
+int orc_error_norms(const orc_problem* pb, const orc_arch* a, const double* theta, int M,
+                    int mode, double out[2]) {
+  const int64_t m1 = (int64_t)M + 1, total = m1 * m1 * m1;
+  double sum = 0.0, mx = 0.0;
+  int bad = 0;
+  for (int64_t g = 0; g < total; ++g) {
+    const int64_t idx[3] = {g % m1, (g / m1) % m1, g / (m1 * m1)};
+    double x[3];
+    for (int c = 0; c < 3; ++c) {
+      const double lo = -1.0, hi = 1.0;   /* the box (G23) */
+      x[c] = (double)(float)(lo + (hi - lo) * (double)idx[c] / (double)M);
+    }
+    const int s = orc_side(pb, x);
+    double ue, grad[3];
+    if (orc_exact(pb, s, x, &ue, grad) != 0) { bad = 1; break; }   /* 0 = defined */
+    const double e = orc_forward(a, theta, net_of(a, s), x, mode) - ue;
+    sum += e * e;
+    if (fabs(e) > mx) mx = fabs(e);
+  }
+  if (bad) return -1;
+  out[0] = sqrt(sum / (double)total);
+  out[1] = mx;
+  return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Adam: t <- t+1; m <- b1 m + (1-b1) g; v <- b2 v + (1-b2) g^2;      */
 /* theta <- theta - lr mhat / (sqrt(vhat) + eps)                             */
 /* ------------------------------------------------------------------------ */

@@ -155,6 +155,10 @@ int orc_residual_exact(const orc_problem* pb, const float* pts, int64_t n, float
 void orc_eval(const orc_problem* pb, const orc_arch* a, const double* theta,
               const float* pts, int64_t n, int mode, double* u);
 
+/* rmse, linf of u_{side} - u* over the (M+1)^3 nodal grid; -1: no exact solution */
+int orc_error_norms(const orc_problem* pb, const orc_arch* a, const double* theta, int M,
+                    int mode, double out[2]);
+
 /* ---- Adam ---- fp64 and an fp32 mirror with a fixed op order */
 void orc_adam(int64_t P, double* theta, double* m, double* v, const double* g,
               int64_t t, double lr, double b1, double b2, double eps);

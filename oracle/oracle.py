@@ -94,6 +94,7 @@ def lib():
         L.orc_classify.argtypes = [P(Problem), P(C.c_float), C.c_int64, C.c_float,
                                    P(C.c_uint8), P(C.c_uint8)]
         L.orc_param_count.restype = C.c_int64
+        L.orc_error_norms.argtypes = [P(Problem), P(Arch), P(C.c_double), C.c_int, C.c_int, P(C.c_double)]
         L.orc_param_count.argtypes = [P(Arch)]
         L.orc_init_params.argtypes = [P(Arch), C.c_uint64, P(C.c_float)]
         L.orc_forward.restype = C.c_double
@@ -408,6 +409,24 @@ def evaluate(pb, arch, theta, pts, mode=MODE_F64) -> np.ndarray:
     lib().orc_eval(pb.ref, arch.ref, _ptr(th, C.c_double), _ptr(pts, C.c_float), len(pts), mode,
                    _ptr(u, C.c_double))
     return u
+
+
+def error_norms(pb, arch, theta, M, mode=MODE_F64):
+    """(rmse, linf) of the pair against the exact solution over the (M+1)^3 nodal grid
+    (Table 1's columns)."""
+    th = _theta(theta)
+    out = np.zeros(2)
+    rc = lib().orc_error_norms(pb.ref, arch.ref, _ptr(th, C.c_double), int(M), mode, _ptr(out, C.c_double))
+    if rc:
+        raise ValueError("no closed-form solution for this problem")
+    return float(out[0]), float(out[1])
+
+
+def convergence_order(e_coarse: float, e_fine: float) -> float:
+    """log2(e_coarse / e_fine) for a resolution doubling (Table 1 "Order")."""
+    if not (e_coarse > 0 and e_fine > 0):
+        raise ValueError("NonPositiveError")
+    return float(np.log2(e_coarse / e_fine))
 
 
 def adam(theta, m, v, g_, t, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
