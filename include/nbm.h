@@ -227,6 +227,17 @@ int nbm_classify(nbm_handle* h, const float* pts_dev, int64_t n, float h_cell, u
 int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_t n,
              float* u_dev, void* stream);
 
+/* Error norms against the problem's closed-form solution (the RMSE and L-inf
+ * columns of Table 1).  Over the (M+1)^3 nodal points p of the
+ * box (coordinates -1 + 2 i / M in fp64 rounded to fp32, x fastest):
+ * e(p) = u_side(p)(p) - u*_side(p)(p) with the network evaluated as nbm_eval does and u* in
+ * fp64; out_dev (device, double[2]) receives rmse = sqrt(mean e^2) and linf = max |e|.
+ * Runs in chunks of max_points through the eval path (overwrites the workspace's crossed-row
+ * buffers; stream-ordered with nbm_loss_grad).  Deterministic (fixed-order reductions).
+ * Errors: NBM_E_ARG (M outside 1..4096, null pointers), NBM_E_INVALID_PROBLEM (a source
+ * without a closed-form solution: NBM_SRC_GAUSS). */
+int nbm_error_norms(nbm_handle* h, const float* theta_dev, int M, double* out_dev, void* stream);
+
 /* Adam (G19), in place on fp32 theta, m, v given grad, all [P]; t is the
  * 1-based step after increment.  Per element: m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
  * theta -= lr (m/bc1) / (sqrt(v/bc2) + eps) with bc_k = 1 - b_k^t computed in fp64. */

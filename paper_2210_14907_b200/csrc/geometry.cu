@@ -714,6 +714,85 @@ __global__ void __launch_bounds__(1024) k_crossed_residual(const int* __restrict
   }
 }
 
+// ---- evaluation-grid error norms (Table 1) ----
+// nodal points g = first .. first+n-1 of the (M+1)^3 grid over the box, x fastest:
+// lo + (hi - lo) i / M in fp64, rounded to fp32
+__global__ void k_nodal_points(int M, int64_t first, int64_t n, float* __restrict__ pts) {
+  const int64_t m1 = (int64_t)M + 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = first + i;
+    const int64_t idx[3] = {g % m1, (g / m1) % m1, g / (m1 * m1)};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) pts[3 * i + c] = (float)(-1.0 + 2.0 * (double)idx[c] / (double)M);
+  }
+}
+
+// e = u - u*_{side}: each block folds its points' sum e^2 and max |e| (fixed order: grid
+// stride, warp butterfly, warps in order) into its slot; chunks run in stream order, so the
+// result is deterministic
+__global__ void __launch_bounds__(kErrThreads) k_error_accum(const DevProblem* __restrict__ Pp,
+                                                             const float* __restrict__ pts,
+                                                             const float* __restrict__ u, int64_t n,
+                                                             double* __restrict__ slots, int init) {
+  const DevProblem& P = *Pp;
+  double sum = 0.0, mx = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double x[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    double ue, g[3];
+    d_exact(P, d_side_exact(P, x), x, &ue, g);
+    const double e = (double)u[i] - ue;
+    sum += e * e;
+    mx = fmax(mx, fabs(e));
+  }
+  for (int o = 16; o; o >>= 1) {
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  __shared__ double ws[2][kErrThreads / 32];
+  if ((threadIdx.x & 31) == 0) {
+    ws[0][threadIdx.x >> 5] = sum;
+    ws[1][threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0, m = 0.0;
+    for (int w = 0; w < kErrThreads / 32; ++w) {
+      t += ws[0][w];
+      m = fmax(m, ws[1][w]);
+    }
+    double* sl = slots + 2 * blockIdx.x;
+    sl[0] = init ? t : sl[0] + t;
+    sl[1] = init ? m : fmax(sl[1], m);
+  }
+}
+
+__global__ void k_error_final(const double* __restrict__ slots, int nslots, double inv_total, double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double t = 0.0, m = 0.0;
+  for (int b = 0; b < nslots; ++b) {
+    t += slots[2 * b];
+    m = fmax(m, slots[2 * b + 1]);
+  }
+  out[0] = sqrt(t * inv_total);
+  out[1] = m;
+}
+
+cudaError_t launch_nodal_points(int M, int64_t first, int64_t n, float* pts, cudaStream_t s) {
+  k_nodal_points<<<148 * 4, 256, 0, s>>>(M, first, n, pts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_error_accum(const nbm_handle* h, const float* pts, const float* u, int64_t n, bool init,
+                               cudaStream_t s) {
+  k_error_accum<<<kErrBlocks, kErrThreads, 0, s>>>(h->d_problem, pts, u, n, h->ws.epart, init ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_error_final(const nbm_handle* h, int64_t total, double* out, cudaStream_t s) {
+  k_error_final<<<1, 32, 0, s>>>(h->ws.epart, kErrBlocks, 1.0 / (double)total, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_crossed_residual(const nbm_handle* h, int64_t n_global, double weight, cudaStream_t s) {
   const Workspace& w = h->ws;   // weight: the resolution level's w_l, 1 for one level
   k_crossed_residual<<<1, 1024, 0, s>>>(w.counts, w.xrec, w.xrow_u, w.xrow_cot,

@@ -353,6 +353,7 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   ALLOC(w.touched, 2 * (size_t)w.grid_mlp * sizeof(int));
   ALLOC(w.lpart, ((size_t)w.grid_mlp + 1) * sizeof(double));
   ALLOC(w.err, sizeof(int));
+  ALLOC(w.epart, (size_t)2 * kErrBlocks * sizeof(double));
   ALLOC(w.bc, 2 * sizeof(float));
   const size_t nhh = ai.n_hidden > 1 ? ai.n_hidden - 1 : 1;
   ALLOC(w.wimg, (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t));
@@ -650,6 +651,28 @@ int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_
   p.u_out = u_dev;
   if (e == cudaSuccess) e = launch_mlp_h(h, false, p, s);
   return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_eval");
+}
+
+int nbm_error_norms(nbm_handle* h, const float* theta_dev, int M, double* out_dev, void* stream) {
+  if (!h || !theta_dev || !out_dev || M < 1 || M > 4096) return fail(h, NBM_E_ARG, "nbm_error_norms: bad arguments");
+  const int src = h->host_problem.source;
+  if (src != NBM_SRC_SINE3PI && src != NBM_SRC_PAIR && src != NBM_SRC_PAPER41)
+    return fail(h, NBM_E_INVALID_PROBLEM, "nbm_error_norms: the problem has no closed-form solution");
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const Workspace& w = h->ws;
+  const int64_t m1 = (int64_t)M + 1, total = m1 * m1 * m1;
+  cudaError_t e = cudaSuccess;
+  for (int64_t first = 0; first < total && e == cudaSuccess; first += w.cap) {
+    const int64_t n = std::min<int64_t>(w.cap, total - first);
+    e = launch_nodal_points(M, first, n, w.xrow_x, s);   // the crossed-row buffers are free here
+    if (e != cudaSuccess) break;
+    const int rc = nbm_eval(h, theta_dev, w.xrow_x, n, w.xrow_u, stream);
+    if (rc != NBM_OK) return rc;
+    e = launch_error_accum(h, w.xrow_x, w.xrow_u, n, first == 0, s);
+  }
+  if (e == cudaSuccess) e = launch_error_final(h, total, out_dev, s);
+  return e == cudaSuccess ? NBM_OK : cuda_fail(h, e, "nbm_error_norms");
 }
 
 int nbm_adam_step(nbm_handle* h, float* theta_dev, float* m_dev, float* v_dev, const float* grad_dev,

@@ -98,6 +98,7 @@ struct Workspace {
   int* touched;         // [2][grid_mlp]
   double* lpart;        // [grid_mlp + 1]  (+1: crossed rows' loss)
   int* err;             // sticky error word
+  double* epart;        // [kErrBlocks][2] error-norm slots (sum e^2, max |e|)
   float* bc;            // [2] Adam bias corrections of the device step counter
   uint16_t* wimg;       // [2][NH-1][W*W] bf16 weight image (tensor-core path)
   uint16_t* wimg_b;     // W = 256: backward-sliced image
@@ -152,6 +153,11 @@ cudaError_t launch_classify(const nbm_handle* h, const float* pts, int64_t n, co
 cudaError_t launch_assemble_crossed(const nbm_handle* h, const float* pts, int64_t n, int64_t H,
                                     cudaStream_t s);
 cudaError_t launch_crossed_residual(const nbm_handle* h, int64_t n_global, double weight, cudaStream_t s);
+constexpr int kErrBlocks = 296, kErrThreads = 256;   // error-norm reduction slots / block size
+cudaError_t launch_nodal_points(int M, int64_t first, int64_t n, float* pts, cudaStream_t s);
+cudaError_t launch_error_accum(const nbm_handle* h, const float* pts, const float* u, int64_t n, bool init,
+                               cudaStream_t s);
+cudaError_t launch_error_final(const nbm_handle* h, int64_t total, double* out, cudaStream_t s);
 // mlp_fp32.cu
 struct MlpParams {
   SegTable seg;

@@ -82,6 +82,7 @@ def lib():
         L.nbm_sample.argtypes = [v, u64, u64, C.c_int, i64, i64, f, v, v]
         L.nbm_loss_grad.argtypes = [v, v, v, i64, v, i64, f, i64, i64, C.c_uint, v, v, v]
         L.nbm_eval.argtypes = [v, v, v, i64, v, v]
+        L.nbm_error_norms.argtypes = [v, v, C.c_int, v, v]
         L.nbm_classify.argtypes = [v, v, i64, f, v, v, v]
         L.nbm_adam_step.argtypes = [v, v, v, v, v, i64, f, f, f, f, v]
         L.nbm_loss_grad_ml.argtypes = [v, v, v, i64, v, i64, f, C.c_int, v, i64, i64, C.c_uint, v, v, v]
@@ -227,6 +228,10 @@ def nbm_classify(h, pts, n: int, h_cell: float, mask, cls, stream=None) -> None:
 
 def nbm_eval(h, theta, pts, n: int, u, stream=None) -> None:
     _check(h, lib().nbm_eval(h, _ptr(theta), _ptr(pts), n, _ptr(u), _stream(stream)))
+
+
+def nbm_error_norms(h, theta, M: int, out, stream=None) -> None:
+    _check(h, lib().nbm_error_norms(h, _ptr(theta), int(M), _ptr(out), _stream(stream)))
 
 
 def nbm_adam_step(h, theta, m, v, grad, t: int, lr: float, b1: float, b2: float, eps: float,
@@ -384,6 +389,14 @@ class Solver:
             out = torch.empty(pts.shape[0], dtype=torch.float32, device=self.device)
         nbm_eval(self.h, self.theta, pts, pts.shape[0], out)
         return out
+
+    def error_norms(self, M: int, theta=None):
+        """(rmse, linf) against the closed-form solution on the (M+1)^3 nodal grid."""
+        import torch
+        out = torch.empty(2, dtype=torch.float64, device=self.device)
+        nbm_error_norms(self.h, self.theta if theta is None else theta, M, out)
+        r = out.cpu()
+        return float(r[0]), float(r[1])
 
     def status(self) -> int:
         return nbm_status(self.h)
