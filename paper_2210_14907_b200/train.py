@@ -26,9 +26,12 @@ def convergence_order(e_coarse: float, e_fine: float) -> float:
 
 
 def train(cfg: dict, N: int, epochs: int, batch: int = 16384, lr: float = 1e-3, seed: int = 0,
-          levels: int = 1, eval_M: int | None = None, log_every: int = 0, device: int = 0) -> dict:
+          levels: int = 1, eval_M: int | None = None, log_every: int = 0, device: int = 0,
+          lr_schedule=None) -> dict:
     """Train the configuration's network pair at base resolution N for `epochs` epochs and
-    report the RMSE / L-inf errors on the (M+1)^3 nodal grid (M = N unless eval_M)."""
+    report the RMSE / L-inf errors on the (M+1)^3 nodal grid (M = N unless eval_M).
+    lr_schedule: optional [(fraction of the epochs, lr), ...] phases (one captured graph per
+    phase; the Adam state and step counter run on), else a constant lr."""
     import torch
     if N < 4 or N & (N - 1):
         raise ValueError("N must be a power of two >= 4 (S:324)")
@@ -44,7 +47,13 @@ def train(cfg: dict, N: int, epochs: int, batch: int = 16384, lr: float = 1e-3, 
     dev = f"cuda:{device}"
     pts = torch.empty(n, 3, device=dev)
     bpts = torch.empty(nb, 3, device=dev)
-    step = s.capture_step(pts, bpts, n_global=n, nb_global=nb, lr=lr, seed=seed, levels=levels)
+    phases = lr_schedule or [(1.0, lr)]
+    bounds, acc = [], 0.0
+    for frac, plr in phases:
+        acc += frac
+        bounds.append((min(epochs, round(acc * epochs)), s.capture_step(pts, bpts, n_global=n, nb_global=nb, lr=plr,
+                                                                         seed=seed, levels=levels)))
+    bounds[-1] = (epochs, bounds[-1][1])
     rmse0, linf0 = s.error_norms(eval_M or N)
     history = []
     t_train = 0.0
@@ -56,8 +65,10 @@ def train(cfg: dict, N: int, epochs: int, batch: int = 16384, lr: float = 1e-3, 
         k = min(chunk, epochs - done)
         torch.cuda.synchronize(device)
         e0.record()
-        for _ in range(k * steps_per_epoch):
-            step()
+        for ep in range(done, done + k):
+            step = next(f for b, f in bounds if ep < b)
+            for _ in range(steps_per_epoch):
+                step()
         e1.record()
         e1.synchronize()
         t_train += e0.elapsed_time(e1) / 1e3
@@ -65,7 +76,7 @@ def train(cfg: dict, N: int, epochs: int, batch: int = 16384, lr: float = 1e-3, 
         history.append((done, float(s.loss.item())))
     rmse, linf = s.error_norms(eval_M or N)
     out = {"N": N, "h0": cfg["h"], "epochs": epochs, "batch": n, "boundary_batch": nb,
-           "steps_per_epoch": steps_per_epoch, "steps": epochs * steps_per_epoch, "levels": levels, "lr": lr,
+           "steps_per_epoch": steps_per_epoch, "steps": epochs * steps_per_epoch, "levels": levels, "lr": lr if lr_schedule is None else list(lr_schedule),
            "seconds": t_train, "sec_per_epoch": t_train / epochs, "rmse": rmse, "linf": linf,
            "rmse_init": rmse0, "linf_init": linf0, "eval_M": eval_M or N, "loss_history": history}
     s.close()
@@ -98,10 +109,13 @@ def _main():
     ap.add_argument("--levels", type=int, default=1)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--log-every", type=int, default=0)
+    ap.add_argument("--decay", action="store_true",
+                    help="lr phases 1e-3 (50%%), 3e-4 (25%%), 1e-4 (15%%), 3e-5 (10%%) instead of a constant lr")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    sched = [(0.5, 1e-3), (0.25, 3e-4), (0.15, 1e-4), (0.1, 3e-5)] if a.decay else None
     rows = convergence_sweep(inputs.config(a.config), a.N, a.epochs, batch=a.batch, lr=a.lr, levels=a.levels,
-                             seed=a.seed, log_every=a.log_every)
+                             seed=a.seed, log_every=a.log_every, lr_schedule=sched)
     for r in rows:
         print(json.dumps({k: v for k, v in r.items() if k != "loss_history"}))
     if a.out:
