@@ -27,7 +27,7 @@ SOURCES = {
     "mlp_fp32w.cu": [],
     "nbm.cu": [],
 }
-HEADERS = ["nbm_internal.cuh", "tc_ptx.cuh"]
+HEADERS = ["nbm_internal.cuh", "tc_ptx.cuh", "stab.cuh"]
 
 
 def _mtime(p):

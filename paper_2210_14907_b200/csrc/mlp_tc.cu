@@ -29,6 +29,7 @@
 #include <math.h>
 
 #include "nbm_internal.cuh"
+#include "stab.cuh"
 #include "tc_ptx.cuh"
 
 namespace nbm {
@@ -130,92 +131,6 @@ __device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
     }
   }
   return v[0];
-}
-
-// ---- stable stencil evaluation (G27): difference propagation ----
-// Row roles on a stencil tile (point k at rows 8k..8k+7, one lane octet of a warp): 0 the
-// centre activation a, 1..3 the first differences P_d = a(x + h e_d) - a(x), 4..6 the second
-// differences Q_d = a(x + h e_d) + a(x - h e_d) - 2 a(x), 7 padding (zero).
-// tanh(d) - d: odd Taylor series to d^7 below 1/4 (truncation < 2e-5 relative, under the bf16
-// rounding of the rows), MUFU tanh above (rare: |d| is O(h) on the difference rows).  Both are
-// computed and selected: a branch per element would serialise the unrolled column loop
-__device__ __forceinline__ float tanh_minus_id(float d) {
-  const float d2 = d * d;
-  const float s = fmaf(d2, fmaf(d2, -17.0f / 315.0f, 2.0f / 15.0f), -1.0f / 3.0f) * (d * d2);
-  return fabsf(d) < 0.25f ? s : tanh_fast(d) - d;
-}
-__device__ __forceinline__ float rcp_approx(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-// g(d) = tanh(z + d) - tanh(z) - (1 - t^2) d = s2 [(tanh d - d) - t tanh(d) d] / (1 + t tanh d)
-// with s2 = 1 - t^2 (tanh addition theorem)
-__device__ __forceinline__ float stab_g(float t, float s2, float d) {
-  const float s = tanh_minus_id(d), x = t * (d + s);
-  return s2 * fmaf(-x, d, s) * rcp_approx(1.0f + x);
-}
-// Role masks of a lane (0/1): the maps below are written branch-free (a select chain per element
-// compiles to branches, which serialise the unrolled column loop and guard every shuffle)
-struct StabRole {
-  int base, pl, partner;
-  float cC, cP, cQ, cPQ;
-  __device__ __forceinline__ explicit StabRole(int lane) {
-    const int jr = lane & 7;
-    const bool isP = jr >= 1 && jr < 4, isQ = jr >= 4 && jr < 7;
-    base = lane & ~7;
-    pl = base + (isQ ? jr - 3 : jr);                         // the P_d lane of this row's axis
-    partner = base + (isP ? jr + 3 : isQ ? jr - 3 : jr);     // P_d <-> Q_d
-    cC = jr == 0 ? 1.0f : 0.0f;
-    cP = isP ? 1.0f : 0.0f;
-    cQ = isQ ? 1.0f : 0.0f;
-    cPQ = cP + cQ;
-  }
-};
-// forward map of one 32-column chunk: v = the row's pre-activation without bias (z - b for the
-// centre, p_d, D_d); bl = the layer's bias.  a = tanh z, P = (1 - t^2) p + g(p),
-// Q = (1 - t^2) D + g(p) + g(D - p).  t from MUFU tanh.approx as on the direct path: its
-// 2^-11 error moves 1 - t^2 of saturated units by ~2^-10 absolute, below the bf16 rounding
-// of the rows (the GPU results agree with the exact-tanh emulation, test_gpu_stable)
-__device__ __forceinline__ void stab_fwd(float (&v)[32], const float* bl, int lane) {
-  const StabRole R(lane);
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float t = tanh_fast(__shfl_sync(0xffffffffu, v[j] + bl[j], R.base));
-    const float s2 = fmaf(-t, t, 1.0f);
-    const float pv = __shfl_sync(0xffffffffu, v[j], R.pl);
-    const float g = stab_g(t, s2, fmaf(-R.cQ, pv, R.cPQ * v[j]));   // p, D - p; 0 on centre / pad
-    const float gp = __shfl_sync(0xffffffffu, g, R.pl);
-    v[j] = fmaf(R.cC, t, fmaf(R.cQ, gp, R.cPQ * fmaf(s2, v[j], g)));
-  }
-}
-// backward map: v = upstream gradients of the row (g_a, g_P or g_Q), hq = the row's activation
-// copy (t, P or Q).  With M = Q - P:  g_z = g_a (1 - t^2) - sum_d [g_P P (2t + P)
-// + g_Q (2tQ + P^2 + M^2)],  g_p = g_P (1 - (t + P)^2) + g_Q (M - P)(2t + M + P),
-// g_D = g_Q (1 - (t + M)^2)   (oracle/stable_stencil.py, pinned against the plain gradient)
-__device__ __forceinline__ void stab_bwd(float (&v)[32], const float (&hq)[32], int lane) {
-  const StabRole R(lane);
-  const uint32_t qm = R.cQ != 0.0f ? 0xffffffffu : 0u;   // bit select (LOP3), not a branch
-  auto sel = [qm](float a, float b) { return __uint_as_float((__float_as_uint(a) & qm) | (__float_as_uint(b) & ~qm)); };
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float t = __shfl_sync(0xffffffffu, hq[j], R.base);
-    const float ho = __shfl_sync(0xffffffffu, hq[j], R.partner);
-    const float go = __shfl_sync(0xffffffffu, v[j], R.partner);
-    const float pv = sel(ho, hq[j]), qv = sel(hq[j], ho);
-    const float gP = sel(go, v[j]), gQ = sel(v[j], go);
-    const float m = qv - pv, t2 = t + t;
-    const float cp = gP * pv * (t2 + pv), cq = gQ * fmaf(t2, qv, fmaf(pv, pv, m * m));
-    float c = fmaf(R.cP, cp, R.cQ * cq);
-    c += __shfl_xor_sync(0xffffffffu, c, 4);
-    c += __shfl_xor_sync(0xffffffffu, c, 2);
-    c += __shfl_xor_sync(0xffffffffu, c, 1);
-    const float tp = t + pv, tm = t + m;
-    const float oC = fmaf(v[j], fmaf(-t, t, 1.0f), -c);
-    const float oP = fmaf(gP, fmaf(-tp, tp, 1.0f), gQ * (m - pv) * (t2 + m + pv));
-    const float oQ = gQ * fmaf(-tm, tm, 1.0f);
-    v[j] = fmaf(R.cC, oC, fmaf(R.cP, oP, R.cQ * oQ));
-  }
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -529,7 +444,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
         const int n = ccol + j;
         h[j] = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, sW1[3 * n] * x0));
       }
-      stab_fwd(h, sBias + ccol, lane);
+      stab::stab_fwd(h, sBias + ccol, lane);
       return;
     }
 #pragma unroll
@@ -669,7 +584,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       tc::tmem_ld32(tmem + tlane + ccol, v);
       const float* bl = sBias + (l - 1) * W + ccol;
       if (STAB && stab) {
-        stab_fwd(v, bl, lane);
+        stab::stab_fwd(v, bl, lane);
       } else if (!SILU) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = act_tanh(v[j] + bl[j]);
@@ -798,7 +713,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
           v[j] = a[j] = hv[j];
           hv[j] = ub * sWo[ccol + j];
         }
-        stab_bwd(hv, a, lane);
+        stab::stab_bwd(hv, a, lane);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -850,7 +765,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       tc::tmem_ld32(tmem + tlane + ccol, v);
       if (STAB && stab) {                  // the backward map of the difference form (G27)
         load_chunk_bf16(hbuf, row, chunk, hq);
-        stab_bwd(v, hq, lane);
+        stab::stab_bwd(v, hq, lane);
 #pragma unroll
         for (int j = 0; j < 32; ++j) hq[j] = 1.0f;
       } else if (!SILU) {                  // tanh' = 1 - h~^2 (bf16 operand copy)

@@ -23,6 +23,7 @@
 #include <math.h>
 
 #include "nbm_internal.cuh"
+#include "stab.cuh"
 #include "tc_ptx.cuh"
 
 namespace nbm {
@@ -32,6 +33,7 @@ namespace {
 constexpr int W = 256;
 constexpr int kB = 128;        // tile rows per CTA (256 per pair)
 constexpr int kPT = 18;        // stencil points per tile
+constexpr int kPTS = 16;       // stencil points per tile of the stable form (G27): 8 rows per point
 constexpr int kThreads = 512;
 constexpr int kStages = 4;     // weight ring: one whole GEMM's slices in flight
 constexpr uint32_t ACT = kB * W * 2;        // 64 KB bf16 activation tile
@@ -151,8 +153,11 @@ struct W256Params {
   int nrep;
 };
 
-template <int NH, bool TRAIN>
+// STAB: stencil tiles in the stable difference form (G27; training pass only)
+template <int NH, bool TRAIN, bool STAB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w256(const W256Params P) {
+  static_assert(!STAB || TRAIN, "stable form: training pass");
+  constexpr int TPT = STAB ? kPTS : kPT;
   using L = Lay<NH>;
   const MlpParams& prm = P.m;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -183,7 +188,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   const bool leader = rank == 0;
   if (tid < kNumSeg) {
     const int c = prm.counts[prm.cnt_slot[tid]];
-    const int per = prm.seg.kind[tid] == kSegStencil ? kPT : kB;
+    const int per = prm.seg.kind[tid] == kSegStencil ? TPT : kB;
     segCnt[tid] = c;
     segStart[tid] = prm.start_slot[tid] >= 0 ? prm.counts[prm.start_slot[tid]] : 0;
     segPairs[tid] = ((c + per - 1) / per + 1) / 2;
@@ -326,7 +331,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     for (int v = 0; v < NV; ++v) g[v][0] = g[v][1] = 0.0f;
     gbo = 0.0f;
   };
-  auto layer1 = [&](int c, float x0, float x1, float x2, float (&h)[32]) {
+  auto layer1 = [&](int c, float x0, float x1, float x2, float (&h)[32], bool stab) {
+    if (STAB && stab) {   // row inputs x / h e_d / 0; the bias enters the centre rows only
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int n = c * 32 + j;
+        h[j] = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, sW1[3 * n] * x0));
+      }
+      stab::stab_fwd(h, sBias + c * 32, lane);
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int n = c * 32 + j;
@@ -342,7 +356,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     if (uu >= u1 || tid >= kB) return f;
     const int sg = seg_of(uu);
     const int knd = prm.seg.kind[sg];
-    const int pr = knd == kSegStencil ? kPT : kB;
+    const int pr = knd == kSegStencil ? TPT : kB;
     const int fst = ((uu - firstPair[sg]) * 2 + (int)rank) * pr;
     const int nv = max(0, min(pr, segCnt[sg] - fst));
     const int* its = prm.seg.items[sg] + segStart[sg];
@@ -350,7 +364,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       f.item = its[fst + tid];
       f.aux = prm.aux_by_item[sg] ? prm.seg.aux[sg][f.item] : prm.seg.aux[sg][segStart[sg] + fst + tid];
     }
-    if (knd == kSegStencil) {
+    if (STAB && knd == kSegStencil) {   // row 8k + jr: x, h e_1..3 (P_d), 0 (Q_d, pad)
+      const int k = tid >> 3, jr = tid & 7;
+      if (k < nv && jr == 0) {
+        const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + k];
+        f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
+      } else if (k < nv && jr < 4) {
+        if (jr == 1) f.x0 = prm.h; else if (jr == 2) f.x1 = prm.h; else f.x2 = prm.h;
+      }
+    } else if (knd == kSegStencil) {
       const int j = tid / kPT, p = tid - j * kPT;
       if (j < 7 && p < nv) {
         const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + p];
@@ -372,9 +394,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   for (int u = u0; u < u1; ++u) {
     const int seg = seg_of(u);
     const int kind = prm.seg.kind[seg], net = prm.seg.net[seg];
-    const int per = kind == kSegStencil ? kPT : kB;
+    const int per = kind == kSegStencil ? TPT : kB;
     const int first = ((u - firstPair[seg]) * 2 + (int)rank) * per;
     const int nvalid = max(0, min(per, segCnt[seg] - first));   // 0: the pair's odd tail (all rows void)
+    const bool stab = STAB && kind == kSegStencil;              // block-uniform
+    const bool centre = !stab || (row & 7) == 0;                // rows that carry the biases
     const int nextNet = u + 1 < u1 ? prm.seg.net[seg_of(u + 1)] : -1;
     if (net != curNet) {
       __syncthreads();
@@ -397,7 +421,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     // ---- layer 1 -> h1 (tile 0, parked copy) ----
     for (int k = 0; k < 2; ++k) {
       float h[32];
-      layer1(2 * cg + k, x0, x1, x2, h);
+      layer1(2 * cg + k, x0, x1, x2, h, stab);
       put_chunk(aBuf[0], nullptr, row, 2 * cg + k, h);
     }
     tc::fence_proxy_async_smem();
@@ -430,8 +454,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
         const int c = 2 * cg + k;
         float v[32];
         tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
+        if (STAB && stab) {
+          stab::stab_fwd(v, sBias + (l - 1) * W + c * 32, lane);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = th(v[j] + sBias[(l - 1) * W + c * 32 + j]);
+          for (int j = 0; j < 32; ++j) v[j] = th(v[j] + sBias[(l - 1) * W + c * 32 + j]);
+        }
         if (l < NH) {
           put_chunk(aBuf[(l - 1) & 1], nullptr, row, c, v);
         } else {
@@ -453,7 +481,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       TRW(3 + 2 * (l - 2));
     }
     if (tid < kB) {
-      const float uu = ((sUp[tid] + sUp[kB + tid]) + sUp[2 * kB + tid]) + sUp[3 * kB + tid] + sWo[W];
+      const float uu = ((sUp[tid] + sUp[kB + tid]) + sUp[2 * kB + tid]) + sUp[3 * kB + tid] +
+                       ((!stab || (tid & 7) == 0) ? sWo[W] : 0.0f);   // differences carry no output bias
       if (!TRAIN && tid < nvalid) prm.u_out[sItem[tid]] = uu;
       sU[tid] = uu;
     }
@@ -461,7 +490,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     cur = nxt;
     if (!TRAIN) continue;
     // ---- residual epilogue ----
-    if (kind == kSegStencil) {
+    if (stab) {   // r = c_c u + c_hat sum_d DU_d - b/d (G27); cotangents c_c 2r/N (centre), c_hat 2r/N (Q_d)
+      if (tid < kB) {
+        const int k = tid >> 3, jr = tid & 7;
+        float ubv = 0.0f;
+        if (k < nvalid) {
+          const float chat = prm.seg.chat[seg], cc = prm.seg.ccen[seg];
+          const float du = (sU[8 * k + 4] + sU[8 * k + 5]) + sU[8 * k + 6];
+          const float r = fmaf(cc, sU[8 * k], chat * du) - sAux[k];
+          if (jr == 0) lossAcc += 0.5 * (double)prm.two_over_n * (double)r * (double)r;
+          const float rc = prm.two_over_n * r;
+          ubv = jr == 0 ? rc * cc : (jr >= 4 && jr < 7) ? rc * chat : 0.0f;
+        }
+        sUb[tid] = ubv;
+      }
+    } else if (kind == kSegStencil) {
       if (tid < kPT) {
         float r = 0.0f;
         if (tid < nvalid) {
@@ -496,7 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     __syncthreads();
     const float ub = sUb[row];
     if (cg == 0) {
-      float b = ub;
+      float b = centre ? ub : 0.0f;
 #pragma unroll
       for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
       gbo += b;
@@ -511,9 +554,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = ub * hv[j];
       g[NH + 3][k] += tsum(v, lane);
+      if (STAB && stab) {   // G_NH = the backward map of (ub wo) through the last activation
+        float a[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
+        for (int j = 0; j < 32; ++j) {
+          a[j] = hv[j];
+          hv[j] = ub * sWo[c * 32 + j];
+        }
+        stab::stab_bwd(hv, a, lane);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
+      }
       put_chunk(gb, nullptr, row, c, hv);
+      if (!centre) {   // b_NH: centre rows only
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hv[j] = 0.0f;
+      }
       g[NH - 1][k] += tsum(hv, lane);
     }
     tc::fence_proxy_async_smem();
@@ -567,13 +624,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
         float v[32], hq[32];
         tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
         get_chunk_g(hprev, row, c, hq);
+        if (STAB && stab) {
+          stab::stab_bwd(v, hq, lane);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] *= 1.0f - hq[j] * hq[j];
+          for (int j = 0; j < 32; ++j) v[j] *= 1.0f - hq[j] * hq[j];
+        }
         if (l - 1 >= 2) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) gk[k][j] = pk(v[2 * j], v[2 * j + 1]);
+          if (!centre) {   // b_{l-1}: centre rows only (v is consumed)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+          }
           g[l - 2][k] += tsum(v, lane);
-        } else {   // layer 1: dW1 += G1 x^T, db1 += G1
+        } else {   // layer 1: dW1 += G1 x^T (x = the row input), db1 += G1 (centre rows)
           float tv[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) tv[j] = v[j] * x0;
@@ -584,6 +649,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
 #pragma unroll
           for (int j = 0; j < 32; ++j) tv[j] = v[j] * x2;
           g[NH + 2][k] += tsum(tv, lane);
+          if (!centre) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+          }
           g[0][k] += tsum(v, lane);
         }
       }
@@ -691,9 +760,9 @@ extern "C" int nbm_debug_w256_ld(long long* out) {
 }
 #endif
 
-template <int NH, bool TRAIN>
+template <int NH, bool TRAIN, bool STAB = false>
 static cudaError_t launch_w256_t(const W256Params& p, int grid, cudaStream_t s) {
-  auto kern = k_mlp_w256<NH, TRAIN>;
+  auto kern = k_mlp_w256<NH, TRAIN, STAB>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay<NH>::bytes);
@@ -704,11 +773,19 @@ static cudaError_t launch_w256_t(const W256Params& p, int grid, cudaStream_t s) 
   return cudaGetLastError();
 }
 
-cudaError_t launch_mlp_w256(int n_hidden, bool train, const MlpParams& m, const uint16_t* wf,
+cudaError_t launch_mlp_w256(int n_hidden, bool train, bool stable, const MlpParams& m, const uint16_t* wf,
                             const uint16_t* wb, uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s) {
   W256Params p{m, wf, wb, hscr, rep, nrep};
   grid &= ~1;   // CTA pairs
   if (grid < 2 || nrep < 1) return cudaErrorInvalidValue;
+  if (stable && train) {
+    switch (n_hidden) {
+      case 2: return launch_w256_t<2, true, true>(p, grid, s);
+      case 3: return launch_w256_t<3, true, true>(p, grid, s);
+      case 4: return launch_w256_t<4, true, true>(p, grid, s);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (n_hidden) {
     case 2: return train ? launch_w256_t<2, true>(p, grid, s) : launch_w256_t<2, false>(p, grid, s);
     case 3: return train ? launch_w256_t<3, true>(p, grid, s) : launch_w256_t<3, false>(p, grid, s);

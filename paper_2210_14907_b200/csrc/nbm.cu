@@ -68,9 +68,8 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
     *why = "arch: bad stencil evaluation";
     return NBM_E_INVALID_ARCH;
   }
-  if (a->stencil == NBM_STENCIL_STABLE &&
-      !(a->prec == NBM_PREC_BF16 && a->act == NBM_ACT_TANH && mlp_tc_supported(W, nh, a->act, 1))) {
-    *why = "arch: the stable stencil form needs BF16 tanh with W in {64, 128} (G27)";
+  if (a->stencil == NBM_STENCIL_STABLE && !(a->prec == NBM_PREC_BF16 && a->act == NBM_ACT_TANH)) {
+    *why = "arch: the stable stencil form needs BF16 tanh (W in {64, 128, 256}, G27)";
     return NBM_E_INVALID_ARCH;
   }
   if (out) {
@@ -252,7 +251,8 @@ cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cu
   const ArchInfo& A = h->arch;
   const Workspace& w = h->ws;
   if (is_w256(A))
-    return launch_mlp_w256(A.n_hidden, train, p, w.wimg, w.wimg_b, w.hscr, w.rep, w.nrep, w.grid_base, s);
+    return launch_mlp_w256(A.n_hidden, train, A.stencil == NBM_STENCIL_STABLE, p, w.wimg, w.wimg_b, w.hscr, w.rep,
+                           w.nrep, w.grid_base, s);
   if (is_fp32w(A)) return launch_mlp_fp32w(A.width, A.n_hidden, train, p, w.wimg32, w.rep, w.nrep, w.grid_base, s);
   if (A.prec == NBM_PREC_BF16)
     return launch_mlp_tc(A.width, A.n_hidden, A.act, 1, train, A.stencil == NBM_STENCIL_STABLE, p, w.grid_base, s);

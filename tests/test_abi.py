@@ -55,13 +55,13 @@ def test_all_configs_are_valid_descriptors(lib):
 
 
 def test_stable_stencil_descriptor_rules(lib):
-    """NBM_STENCIL_STABLE (G27) needs the bf16 tanh tensor-core kernel (W in {64, 128})."""
+    """NBM_STENCIL_STABLE (G27) needs a bf16 tanh tensor-core kernel (W in {64, 128, 256})."""
     S = inputs.STENCIL_STABLE
     ok = dict(inputs.config("c5", width=128), stencil=S)
     assert nbm.nbm_check(nbm.Descriptors(ok)) == 0
     assert nbm.nbm_check(nbm.Descriptors(dict(inputs.config("c5", width=64), stencil=S))) == 0
-    for bad in (dict(inputs.config("c4"), stencil=S),                     # W = 256 (K3w)
-                dict(inputs.config("c2"), stencil=S),                     # fp32
+    assert nbm.nbm_check(nbm.Descriptors(dict(inputs.config("c4"), stencil=S))) == 0
+    for bad in (dict(inputs.config("c2"), stencil=S),                     # fp32
                 dict(inputs.config("c3"), stencil=S),                     # SiLU
                 dict(inputs.config("c5", width=128), stencil=2)):         # unknown mode
         assert nbm.nbm_check(nbm.Descriptors(bad)) == 1

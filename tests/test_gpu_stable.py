@@ -60,14 +60,15 @@ def _stable_emulation(orc, cfg, pb, ar, th, pts, side):
 
 
 @pytest.mark.parametrize("w,nh,k,n", [(128, 4, 0.0, 1 << 13), (128, 3, 0.0, (1 << 13) + 5), (128, 2, 0.0, 4099),
-                                      (64, 4, 0.0, 1 << 13), (64, 2, 0.0, 3001), (64, 3, 2.5, 1 << 13)])
+                                      (64, 4, 0.0, 1 << 13), (64, 2, 0.0, 3001), (64, 3, 2.5, 1 << 13),
+                                      (256, 4, 0.0, 1 << 13), (256, 2, 1.5, 5003), (256, 3, 0.0, 77)])
 def test_stable_parity(orc, w, nh, k, n):
     cfg = inputs.config("c5", width=w)
     cfg.update(sizes=[3] + [w] * nh + [1], k=(k, 2 * k), stencil=inputs.STENCIL_STABLE)
     direct = dict(cfg, stencil=inputs.STENCIL_DIRECT)
     nb = 1 << 10
-    s = nbm.Solver(cfg, 0, max_points=n)
-    sd = nbm.Solver(direct, 0, max_points=n)
+    s = nbm.Solver(cfg, 0, max_points=max(n, nb))
+    sd = nbm.Solver(direct, 0, max_points=max(n, nb))
     pb, ar = orc.from_config(cfg)
     pts = orc.sample(0, 5, 0, 0, n, cfg["H"])
     bpts = orc.sample(1, 5, 0, 0, nb, cfg["H"])
@@ -79,7 +80,10 @@ def test_stable_parity(orc, w, nh, k, n):
     assert abs(gl - L) <= TOL * L, (gl, L)
     assert _rel(gg, g) <= TOL
     gl2, gg2 = _run(s, dth, dp, db)
-    assert gl2 == gl and np.array_equal(gg2, gg)                     # deterministic
+    if w < 256:   # K3w flushes dW through L2 reductions: deterministic within tolerance only (G21)
+        assert gl2 == gl and np.array_equal(gg2, gg)
+    else:
+        assert abs(gl2 - gl) <= 1e-6 * gl and _rel(gg2, gg) <= 1e-5
     for kk, term in enumerate(TERMS):
         tl, tg = _run(s, dth, dp, db, terms=term)
         if lt[kk] == 0.0:
@@ -125,6 +129,6 @@ def test_stable_multiresolution(orc):
 
 
 def test_stable_unsupported_rejected():
-    cfg = dict(inputs.config("c4"), stencil=inputs.STENCIL_STABLE)
+    cfg = dict(inputs.config("c3"), stencil=inputs.STENCIL_STABLE)   # SiLU
     with pytest.raises(Exception):
         nbm.Solver(cfg, 0, max_points=16)
