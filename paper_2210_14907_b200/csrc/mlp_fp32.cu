@@ -20,6 +20,18 @@
 
 namespace nbm {
 
+// activation of the fp32 kernel: accurate tanhf (G15); NBM_F32_TANH_APPROX (timing experiments
+// only, not a supported build) swaps in MUFU tanh.approx
+#ifdef NBM_F32_TANH_APPROX
+__device__ __forceinline__ float f32_tanh(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+#else
+__device__ __forceinline__ float f32_tanh(float x) { return tanhf(x); }
+#endif
+
 #ifndef NBM_F32_TILE
 #define NBM_F32_TILE 64
 #endif
@@ -134,7 +146,7 @@ __device__ __forceinline__ void fwd_gemm(const float* __restrict__ Hin, float* _
 #pragma unroll
     for (int c = 0; c < TC; ++c) {
       if (SINE) sincosf(acc[i][c] + bv[c], &o[c], &oc[c]);   // P:68 sine units; cos kept for act'
-      else o[c] = tanhf(acc[i][c] + bv[c]);
+      else o[c] = f32_tanh(acc[i][c] + bv[c]);
     }
     stv(Hout + (tr + 32 * i) * L::LDA + tc * TC, o);
     if (SINE) stv(CosOut + (tr + 32 * i) * L::LDA + tc * TC, oc);
@@ -390,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
       for (int r = r0; r < kB; r += step) {
         float z = fmaf(w2, sX[4 * r + 2], fmaf(w1, sX[4 * r + 1], fmaf(w0, sX[4 * r], bb)));
         if (SINE) sincosf(z, &sAct[r * L::LDA + col], &sCos[r * L::LDA + col]);
-        else sAct[r * L::LDA + col] = tanhf(z);
+        else sAct[r * L::LDA + col] = f32_tanh(z);
       }
     }
     __syncthreads();

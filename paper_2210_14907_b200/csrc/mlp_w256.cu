@@ -555,13 +555,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       for (int j = 0; j < 32; ++j) v[j] = ub * hv[j];
       g[NH + 3][k] += tsum(v, lane);
       if (STAB && stab) {   // G_NH = the backward map of (ub wo) through the last activation
-        float a[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          a[j] = hv[j];
-          hv[j] = ub * sWo[c * 32 + j];
-        }
-        stab::stab_bwd(hv, a, lane);
+        for (int j = 0; j < 32; ++j) v[j] = ub * sWo[c * 32 + j];   // v is free after the sum
+        stab::stab_bwd(v, hv, lane);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hv[j] = v[j];
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
