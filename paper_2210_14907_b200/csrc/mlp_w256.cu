@@ -115,6 +115,44 @@ __device__ __forceinline__ void put_chunk(uint32_t buf, uint8_t* gbuf, int r, in
     if (gbuf) *reinterpret_cast<uint4*>(gbuf + off) = make_uint4(a, b, cc, d);
   }
 }
+// half hf (16 columns) of chunk c of row r (stable-form epilogues, G27: 16-column halves keep
+// the shuffled maps within the 128-register budget of the 512-thread CTA)
+__device__ __forceinline__ void put_half(uint32_t buf, int r, int c, int hf, const float (&h)[16]) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const uint32_t off = (uint32_t)((c * 4 + 2 * hf + q) * LBO_ACT + r * 16);
+    sts4(buf + off, pk(h[8 * q], h[8 * q + 1]), pk(h[8 * q + 2], h[8 * q + 3]), pk(h[8 * q + 4], h[8 * q + 5]),
+         pk(h[8 * q + 6], h[8 * q + 7]));
+  }
+}
+__device__ __forceinline__ void get_half_g(const uint8_t* gbuf, int r, int c, int hf, float (&h)[16]) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const uint4 w4 = ldcg4(gbuf + (c * 4 + 2 * hf + q) * LBO_ACT + r * 16);
+    const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      h[8 * q + 2 * e] = __uint_as_float(w[e] << 16);
+      h[8 * q + 2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+    }
+  }
+}
+// 16-column warp transpose-sum: lanes l and l + 16 receive the sum over the warp's 32 rows of
+// column l % 16
+__device__ __forceinline__ float tsum16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int s = 8; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const float send = up ? v[i] : v[i + s];
+      const float keep = up ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+}
+
 // chunk c of row r of a parked (global) bf16 tile -> fp32
 __device__ __forceinline__ void get_chunk_g(const uint8_t* gbuf, int r, int c, float (&h)[32]) {
 #pragma unroll
@@ -331,21 +369,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     for (int v = 0; v < NV; ++v) g[v][0] = g[v][1] = 0.0f;
     gbo = 0.0f;
   };
-  auto layer1 = [&](int c, float x0, float x1, float x2, float (&h)[32], bool stab) {
-    if (STAB && stab) {   // row inputs x / h e_d / 0; the bias enters the centre rows only
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = c * 32 + j;
-        h[j] = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, sW1[3 * n] * x0));
-      }
-      stab::stab_fwd(h, sBias + c * 32, lane);
-      return;
-    }
+  auto layer1 = [&](int c, float x0, float x1, float x2, float (&h)[32]) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int n = c * 32 + j;
       h[j] = th(fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, fmaf(sW1[3 * n], x0, sBias[n]))));
     }
+  };
+
+  // stable form (G27), 16 columns: row inputs x / h e_d / 0, the bias on the centre rows only
+  auto layer1_stab = [&](int c, int hf, float x0, float x1, float x2, float (&h)[16]) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int n = c * 32 + hf * 16 + j;
+      h[j] = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, sW1[3 * n] * x0));
+    }
+    stab::stab_fwd<16>(h, sBias + c * 32 + hf * 16, lane);
   };
 
   // global loads of pair-tile uu for thread tid < kB: item slot tid (index + aux) and the
@@ -420,9 +459,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     const float x0 = sX[4 * row], x1 = sX[4 * row + 1], x2 = sX[4 * row + 2];
     // ---- layer 1 -> h1 (tile 0, parked copy) ----
     for (int k = 0; k < 2; ++k) {
-      float h[32];
-      layer1(2 * cg + k, x0, x1, x2, h, stab);
-      put_chunk(aBuf[0], nullptr, row, 2 * cg + k, h);
+      if (STAB && stab) {
+        for (int hf = 0; hf < 2; ++hf) {
+          float h[16];
+          layer1_stab(2 * cg + k, hf, x0, x1, x2, h);
+          put_half(aBuf[0], row, 2 * cg + k, hf, h);
+        }
+      } else {
+        float h[32];
+        layer1(2 * cg + k, x0, x1, x2, h);
+        put_chunk(aBuf[0], nullptr, row, 2 * cg + k, h);
+      }
     }
     tc::fence_proxy_async_smem();
     tc::tc_fence_before();
@@ -450,16 +497,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       wait_bar(bmma, ph_mma);
       TRW(2 + 2 * (l - 2));
       float up = 0.0f;
-      for (int k = 0; k < 2; ++k) {
+      if (STAB && stab) for (int k = 0; k < 2; ++k) {   // stable form: 16-column halves
+        const int c = 2 * cg + k;
+        for (int hf = 0; hf < 2; ++hf) {
+          const uint32_t col = (uint32_t)(c * 32 + hf * 16);
+          float v[16];
+          tc::tmem_ld16(tmem + tlane + col, v);
+          stab::stab_fwd<16>(v, sBias + (l - 1) * W + col, lane);
+          if (l < NH) {
+            put_half(aBuf[(l - 1) & 1], row, c, hf, v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) up = fmaf(sWo[col + j], v[j], up);
+            tc::tmem_st16(tmem + tlane + col, v);
+          }
+        }
+      }
+      if (!(STAB && stab)) for (int k = 0; k < 2; ++k) {
         const int c = 2 * cg + k;
         float v[32];
         tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
-        if (STAB && stab) {
-          stab::stab_fwd(v, sBias + (l - 1) * W + c * 32, lane);
-        } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = th(v[j] + sBias[(l - 1) * W + c * 32 + j]);
-        }
+        for (int j = 0; j < 32; ++j) v[j] = th(v[j] + sBias[(l - 1) * W + c * 32 + j]);
         if (l < NH) {
           put_chunk(aBuf[(l - 1) & 1], nullptr, row, c, v);
         } else {
@@ -547,28 +606,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     const uint32_t gb = aBuf[(NH - 1) & 1];   // G_l (own rows, all outputs), then the dW operand G-halves
     const uint32_t hb = aBuf[NH & 1];         // the dW operand h-halves
     // ---- G_NH = ub wo (1 - h_NH^2) -> gb + parked copy ----
-    for (int k = 0; k < 2; ++k) {
+    if (STAB && stab) for (int k = 0; k < 2; ++k) {   // stable form: the backward map of ub wo, halves
+      const int c = 2 * cg + k;
+      for (int hf = 0; hf < 2; ++hf) {
+        const uint32_t col = (uint32_t)(c * 32 + hf * 16);
+        float hv[16], v[16];
+        tc::tmem_ld16(tmem + tlane + col, hv);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = ub * hv[j];
+        float sm = tsum16(v, lane);
+        if ((lane >> 4) == hf) g[NH + 3][k] += sm;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = ub * sWo[col + j];
+        stab::stab_bwd<16>(v, hv, lane);
+        put_half(gb, row, c, hf, v);
+        if (!centre) {   // b_NH: centre rows only
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+        }
+        sm = tsum16(v, lane);
+        if ((lane >> 4) == hf) g[NH - 1][k] += sm;
+      }
+    }
+    if (!(STAB && stab)) for (int k = 0; k < 2; ++k) {
       const int c = 2 * cg + k;
       float hv[32], v[32];
       tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), hv);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = ub * hv[j];
       g[NH + 3][k] += tsum(v, lane);
-      if (STAB && stab) {   // G_NH = the backward map of (ub wo) through the last activation
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = ub * sWo[c * 32 + j];   // v is free after the sum
-        stab::stab_bwd(v, hv, lane);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) hv[j] = v[j];
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
-      }
+      for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
       put_chunk(gb, nullptr, row, c, hv);
-      if (!centre) {   // b_NH: centre rows only
-#pragma unroll
-        for (int j = 0; j < 32; ++j) hv[j] = 0.0f;
-      }
       g[NH - 1][k] += tsum(hv, lane);
     }
     tc::fence_proxy_async_smem();
@@ -616,27 +685,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       TRW(11 + 4 * (NH - l));
       uint32_t gk[2][16];   // G_{l-1}, bf16, for the next dH GEMM's A tile
       const uint8_t* hprev = myScr + hslot(l - 1);
+      if (STAB && stab) for (int k = 0; k < 2; ++k) {   // stable form: 16-column halves
+        const int c = 2 * cg + k;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+        for (int hf = 0; hf < 2; ++hf) {
+          float v[16], hq[16];
+          tc::tmem_ld16(tmem + tlane + (uint32_t)(c * 32 + hf * 16), v);
+          get_half_g(hprev, row, c, hf, hq);
+          stab::stab_bwd<16>(v, hq, lane);
+          const bool mine = (lane >> 4) == hf;   // lane l accumulates column 32 k + l
+          if (l - 1 >= 2) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) gk[k][8 * hf + j] = pk(v[2 * j], v[2 * j + 1]);
+            if (!centre) {   // b_{l-1}: centre rows only (v is consumed)
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+            }
+            const float sm = tsum16(v, lane);
+            if (mine) g[l - 2][k] += sm;
+          } else {           // layer 1: dW1 += G1 x^T (x = the row input), db1 += G1 (centre rows)
+            const float xs[3] = {x0, x1, x2};
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              float tv[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) tv[j] = v[j] * xs[d];
+              const float sm = tsum16(tv, lane);
+              if (mine) g[NH + d][k] += sm;
+            }
+            if (!centre) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+            }
+            const float sm = tsum16(v, lane);
+            if (mine) g[0][k] += sm;
+          }
+        }
+      }
+      if (!(STAB && stab)) for (int k = 0; k < 2; ++k) {
         const int c = 2 * cg + k;
         float v[32], hq[32];
         tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
         get_chunk_g(hprev, row, c, hq);
-        if (STAB && stab) {
-          stab::stab_bwd(v, hq, lane);
-        } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] *= 1.0f - hq[j] * hq[j];
-        }
+        for (int j = 0; j < 32; ++j) v[j] *= 1.0f - hq[j] * hq[j];
         if (l - 1 >= 2) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) gk[k][j] = pk(v[2 * j], v[2 * j + 1]);
-          if (!centre) {   // b_{l-1}: centre rows only (v is consumed)
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.0f;
-          }
           g[l - 2][k] += tsum(v, lane);
-        } else {   // layer 1: dW1 += G1 x^T (x = the row input), db1 += G1 (centre rows)
+        } else {   // layer 1: dW1 += G1 x^T, db1 += G1
           float tv[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) tv[j] = v[j] * x0;
@@ -647,10 +744,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
 #pragma unroll
           for (int j = 0; j < 32; ++j) tv[j] = v[j] * x2;
           g[NH + 2][k] += tsum(tv, lane);
-          if (!centre) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.0f;
-          }
           g[0][k] += tsum(v, lane);
         }
       }

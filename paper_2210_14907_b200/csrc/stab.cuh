@@ -59,10 +59,12 @@ struct StabRole {
 // Q = (1 - t^2) D + g(p) + g(D - p).  t from MUFU tanh.approx as on the direct path: its
 // 2^-11 error moves 1 - t^2 of saturated units by ~2^-10 absolute, below the bf16 rounding
 // of the rows (the GPU results agree with the exact-tanh emulation, test_gpu_stable)
-__device__ __forceinline__ void stab_fwd(float (&v)[32], const float* bl, int lane) {
+// (N = 32 columns, or 16 where register pressure demands it)
+template <int N>
+__device__ __forceinline__ void stab_fwd(float (&v)[N], const float* bl, int lane) {
   const StabRole R(lane);
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < N; ++j) {
     const float t = stab_tanh(__shfl_sync(0xffffffffu, v[j] + bl[j], R.base));
     const float s2 = fmaf(-t, t, 1.0f);
     const float pv = __shfl_sync(0xffffffffu, v[j], R.pl);
@@ -75,12 +77,13 @@ __device__ __forceinline__ void stab_fwd(float (&v)[32], const float* bl, int la
 // copy (t, P or Q).  With M = Q - P:  g_z = g_a (1 - t^2) - sum_d [g_P P (2t + P)
 // + g_Q (2tQ + P^2 + M^2)],  g_p = g_P (1 - (t + P)^2) + g_Q (M - P)(2t + M + P),
 // g_D = g_Q (1 - (t + M)^2)   (oracle/stable_stencil.py, pinned against the plain gradient)
-__device__ __forceinline__ void stab_bwd(float (&v)[32], const float (&hq)[32], int lane) {
+template <int N>
+__device__ __forceinline__ void stab_bwd(float (&v)[N], const float (&hq)[N], int lane) {
   const StabRole R(lane);
   const uint32_t qm = R.cQ != 0.0f ? 0xffffffffu : 0u;   // bit select (LOP3), not a branch
   auto sel = [qm](float a, float b) { return __uint_as_float((__float_as_uint(a) & qm) | (__float_as_uint(b) & ~qm)); };
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < N; ++j) {
     const float t = __shfl_sync(0xffffffffu, hq[j], R.base);
     const float ho = __shfl_sync(0xffffffffu, hq[j], R.partner);
     const float go = __shfl_sync(0xffffffffu, v[j], R.partner);
