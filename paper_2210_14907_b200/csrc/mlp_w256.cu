@@ -335,9 +335,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   // this CTA's 128 outputs x 256 inputs of dW_pendL.  The replicas hold hidden-weight blocks
   // input-quad-major ([i/4][o][i%4], see k_reduce_rep), so one warp-wide red.v4 covers 32
   // consecutive outputs = 512 contiguous bytes.
-  auto flush_dw = [&]() {
+  // k0..k1-1: the thread's column chunks to flush (the forward spreads dW_2's flush over GEMMs)
+  auto flush_dw_part = [&](int k0, int k1) {
     float* out = rep + (int64_t)pendNet * prm.p_stride + L::tWl(pendL) + (int64_t)(kB * rank + row) * 4;
-    for (int k = 0; k < 2; ++k) {
+    for (int k = k0; k < k1; ++k) {
       const int c = 2 * cg + k;
       float v[32];
       tc::tmem_ld32(tmem + tlane + 256u + (uint32_t)(c * 32), v);
@@ -345,8 +346,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       for (int i = 0; i < 8; ++i)
         red4(out + (int64_t)(c * 8 + i) * (W * 4), v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     }
-    pend = false;
+    if (k1 == 2) pend = false;
   };
+  auto flush_dw = [&]() { flush_dw_part(0, 2); };
   auto flush_small = [&](int net) {
     float* out = rep + (int64_t)net * prm.p_stride;
     for (int k = 0; k < 2; ++k) {
@@ -486,7 +488,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       if (tid == 0) issue_gemm(aBuf[(l - 2) & 1], false, ID_FWD);
       if (l == 3) TRW(24);
       if (l == 2) nxt = fetch(u + 1);  // the next tile's loads overlap this tile
-      if (TRAIN && pend) flush_dw();   // the previous tile's dW_2, under this GEMM
+      // the previous tile's dW_2 under this tile's forward GEMMs: split over the last two (the first
+      // one's weight slices are still arriving, and the flush's writes hold up their reads)
+#ifndef NBM_W256_FLUSH_AT_L2
+      if (TRAIN && pend) {
+        if (NH >= 4 && l == NH - 1) flush_dw_part(0, 1);
+        else if (NH >= 4 && l == NH) flush_dw_part(1, 2);
+        else if (NH < 4 && l == NH) flush_dw();
+      }
+#else
+      if (TRAIN && pend) flush_dw();
+#endif
       if (tid == 0) {                  // the next GEMM's slices
         if (l < NH) queue_gemm(false, net, l + 1);
         else if (TRAIN) queue_gemm(true, net, NH);
