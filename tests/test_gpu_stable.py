@@ -132,3 +132,29 @@ def test_stable_unsupported_rejected():
     cfg = dict(inputs.config("c3"), stencil=inputs.STENCIL_STABLE)   # SiLU
     with pytest.raises(Exception):
         nbm.Solver(cfg, 0, max_points=16)
+
+
+def test_stable_graph_replay_matches_eager_steps():
+    """The stable form inside the captured CUDA-graph training step (device step counter):
+    bitwise equal to the host-counter calls for 3 steps (K3t is deterministic)."""
+    cfg = inputs.config("c5", width=64)
+    cfg.update(sizes=[3, 64, 64, 64, 1], stencil=inputs.STENCIL_STABLE, N=1 << 14, Nb=1 << 11)
+    N, Nb = cfg["N"], cfg["Nb"]
+    a = nbm.Solver(cfg, 0, max_points=N)
+    b = nbm.Solver(cfg, 0, max_points=N)
+    a.init_params(0)
+    b.init_params(0)
+    pa, ba = torch.empty(N, 3, device="cuda"), torch.empty(Nb, 3, device="cuda")
+    pb_, bb = torch.empty(N, 3, device="cuda"), torch.empty(Nb, 3, device="cuda")
+    step = b.capture_step(pb_, bb, lr=1e-3, levels=2)
+    for k in range(3):
+        a.sample(nbm.POINTS_INTERIOR, 0, k, 0, N, pa)
+        a.sample(nbm.POINTS_BOUNDARY, 0, k, 0, Nb, ba)
+        a.loss_grad(pa, ba, levels=2)
+        a.adam_step(lr=1e-3)
+        step()
+        torch.cuda.synchronize()
+        assert torch.equal(a.gbuf, b.gbuf)
+        assert torch.equal(a.theta, b.theta)
+    a.close()
+    b.close()
