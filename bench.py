@@ -395,7 +395,7 @@ def main():
     }
     if infer is not None:
         line["inference"] = infer
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:   # the oracle baseline: rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline(cfg, levels=args.levels)
     print(json.dumps(line), flush=True)
     if world > 1:
