@@ -158,3 +158,40 @@ def test_stable_graph_replay_matches_eager_steps():
         assert torch.equal(a.theta, b.theta)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("name,w", [("c5", 128), ("c4", 256)])
+def test_stable_full_size_shard_invariance(name, w):
+    """At the bench's full size (2^22 + 2^19 points, the timed launch configuration): the
+    stable-form total equals the sum of 4 shard calls with the global normalisation (fp32
+    reduction bars), and every term is finite.  Per-point parity is size-independent and is
+    checked above; this covers the tile indexing and reductions at full size."""
+    cfg = inputs.config(name, width=w)
+    cfg["stencil"] = inputs.STENCIL_STABLE
+    N, Nb = cfg["N"], cfg["Nb"]
+    s = nbm.Solver(cfg, 0)
+    s.init_params(0)
+    pts = torch.empty(N, 3, device="cuda")
+    bpts = torch.empty(Nb, 3, device="cuda")
+    s.sample(0, 0, 0, 0, N, pts)
+    s.sample(1, 0, 0, 0, Nb, bpts)
+    lt, gt = _run(s, s.theta, pts, bpts)
+    assert np.isfinite(lt) and np.all(np.isfinite(gt)) and lt > 0
+    for term in TERMS[:2]:
+        tl, _ = _run(s, s.theta, pts, bpts, terms=term)
+        assert np.isfinite(tl) and tl > 0
+    acc_l, acc_g = 0.0, np.zeros_like(gt)
+    for r in range(4):
+        lo, hi, blo, bhi = r * N // 4, (r + 1) * N // 4, r * Nb // 4, (r + 1) * Nb // 4
+        loss, grad = s.loss_grad(pts[lo:hi], bpts[blo:bhi], n_global=N, nb_global=Nb, theta=s.theta)
+        torch.cuda.synchronize()
+        acc_l += float(loss.item())
+        acc_g += grad.double().cpu().numpy()
+    assert abs(acc_l - lt) <= 1e-5 * lt
+    # the shards move tiles between CTAs; K3t sums each CTA's dW_l in TMEM (tensor-core fp32
+    # accumulation), where the difference rows' O(h^-1) / O(h^-2) gradients times O(h) / O(h^2)
+    # activations partly cancel: measured 5e-4 of the gradient norm at c5-w128 (K3w's L2
+    # reductions: < 1e-4), far inside the 2e-2 bf16 bar
+    assert np.linalg.norm(acc_g - gt) <= (2e-3 if w < 256 else 1e-4) * np.linalg.norm(gt)
+    assert s.status() == 0
+    s.close()
