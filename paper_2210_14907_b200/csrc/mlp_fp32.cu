@@ -111,10 +111,11 @@ struct Layout {
 };
 
 // Hout[b][n] = tanh(sum_k Hin[b][k] W[n][k] + bias[n]); thread = 8 rows x TC cols.
+// raw (stable form, G27): Hout = the pre-activation, the bias on the centre rows (8k) only
 template <int W, int NH, bool SINE = false>
 __device__ __forceinline__ void fwd_gemm(const float* __restrict__ Hin, float* __restrict__ Hout,
                                          const float* __restrict__ Ws, const float* __restrict__ bias,
-                                         int tid, float* __restrict__ CosOut = nullptr) {
+                                         int tid, float* __restrict__ CosOut = nullptr, bool raw = false) {
   using L = Layout<W, NH>;
   constexpr int TC = L::TC;
   const int tr = tid & 31, tc = tid >> 5;
@@ -146,6 +147,7 @@ __device__ __forceinline__ void fwd_gemm(const float* __restrict__ Hin, float* _
 #pragma unroll
     for (int c = 0; c < TC; ++c) {
       if (SINE) sincosf(acc[i][c] + bv[c], &o[c], &oc[c]);   // P:68 sine units; cos kept for act'
+      else if (raw) o[c] = (tr & 7) == 0 ? acc[i][c] + bv[c] : acc[i][c];
       else o[c] = f32_tanh(acc[i][c] + bv[c]);
     }
     stv(Hout + (tr + 32 * i) * L::LDA + tc * TC, o);
@@ -154,10 +156,12 @@ __device__ __forceinline__ void fwd_gemm(const float* __restrict__ Hin, float* _
 }
 
 // In place: H[b][i] <- (sum_o G[b][o] W[o][i]) * (1 - H[b][i]^2)   (delta_{l-1}, tanh')
+// raw (stable form, G27): the products sum_o G W are written over G itself (after a barrier:
+// every thread has read G) for the stable backward map, H is left unchanged
 template <int W, int NH, bool SINE = false>
-__device__ __forceinline__ void bwd_gemm(const float* __restrict__ G, float* __restrict__ H,
+__device__ __forceinline__ void bwd_gemm(float* __restrict__ G, float* __restrict__ H,
                                          const float* __restrict__ Ws, int tid,
-                                         const float* __restrict__ Cs = nullptr) {
+                                         const float* __restrict__ Cs = nullptr, bool raw = false) {
   using L = Layout<W, NH>;
   constexpr int TC = L::TC;
   const int tr = tid & 31, tc = tid >> 5;
@@ -179,6 +183,12 @@ __device__ __forceinline__ void bwd_gemm(const float* __restrict__ G, float* __r
       for (int i = 0; i < kRT; ++i)
 #pragma unroll
         for (int c = 0; c < TC; ++c) acc[i][c] = fmaf(g[i][q], w[q][c], acc[i][c]);
+  }
+  if (raw) {
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kRT; ++i) stv(G + (tr + 32 * i) * L::LDA + tc * TC, acc[i]);
+    return;
   }
 #pragma unroll
   for (int i = 0; i < kRT; ++i) {
@@ -213,15 +223,78 @@ __device__ __forceinline__ void dw_gemm(const float* __restrict__ G, const float
   }
 }
 
+// ---- the stable stencil form in fp32 (G27): one thread per (point, column)
+// of a stencil tile, rows 8k..8k+7 = centre, P_x, P_y, P_z, Q_x, Q_y, Q_z, pad (fp32-accurate
+// maps: tanhf, the series of tanh d - d to d^11 below 1/4, IEEE division) ----
+__device__ __forceinline__ float tanh_minus_id_f32(float d) {
+  const float d2 = d * d;
+  const float s = fmaf(d2, fmaf(d2, fmaf(d2, fmaf(d2, -1382.0f / 155925.0f, 62.0f / 2835.0f), -17.0f / 315.0f),
+                                2.0f / 15.0f), -1.0f / 3.0f) * (d * d2);
+  return fabsf(d) < 0.25f ? s : tanhf(d) - d;
+}
+__device__ __forceinline__ float stab_g_f32(float t, float s2, float d) {
+  const float s = tanh_minus_id_f32(d), x = t * (d + s);
+  return s2 * fmaf(-x, d, s) / (1.0f + x);
+}
+// in place: z (bias included), p_d, D_d -> t = tanh z, P_d, Q_d
+template <int W, int LDA>
+__device__ void stab_fwd_pass(float* __restrict__ H, int tid) {
+  for (int it = tid; it < (kB / 8) * W; it += kThreads) {
+    float* h = H + (it / W) * 8 * LDA + it % W;
+    const float t = tanhf(h[0]);
+    const float s2 = (1.0f - t) * (1.0f + t);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float p = h[(1 + d) * LDA], D = h[(4 + d) * LDA];
+      const float gp = stab_g_f32(t, s2, p), gm = stab_g_f32(t, s2, D - p);
+      h[(1 + d) * LDA] = fmaf(s2, p, gp);
+      h[(4 + d) * LDA] = fmaf(s2, D, gp) + gm;
+    }
+    h[0] = t;
+    h[7 * LDA] = 0.0f;
+  }
+}
+// G of the point's rows from the upstream gradients R (g_a, g_P, g_Q; R = null: the output
+// layer's ub_row wo_col) and the activations H (t, P, Q), written over H
+template <int W, int LDA>
+__device__ void stab_bwd_pass(const float* __restrict__ R, float* __restrict__ H, const float* __restrict__ ub,
+                              const float* __restrict__ wo, int tid) {
+  for (int it = tid; it < (kB / 8) * W; it += kThreads) {
+    const int k = it / W, col = it % W;
+    float* h = H + k * 8 * LDA + col;
+    auto up = [&](int j) { return R ? R[(k * 8 + j) * LDA + col] : ub[k * 8 + j] * wo[col]; };
+    const float t = h[0], t2 = t + t;
+    float gz = up(0) * ((1.0f - t) * (1.0f + t));
+    float gp[3], gd[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float P = h[(1 + d) * LDA], Q = h[(4 + d) * LDA], M = Q - P;
+      const float gP = up(1 + d), gQ = up(4 + d);
+      gz -= gP * P * (t2 + P) + gQ * fmaf(t2, Q, fmaf(P, P, M * M));
+      const float tp = t + P, tm = t + M;
+      gp[d] = fmaf(gP, (1.0f - tp) * (1.0f + tp), gQ * (M - P) * (t2 + M + P));
+      gd[d] = gQ * ((1.0f - tm) * (1.0f + tm));
+    }
+    h[0] = gz;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      h[(1 + d) * LDA] = gp[d];
+      h[(4 + d) * LDA] = gd[d];
+    }
+    h[7 * LDA] = 0.0f;
+  }
+}
+
 // acc[col] += sum_b X[b][col] (fixed order: contiguous row ranges, then parts in order)
 template <int W, int NH>
 __device__ __forceinline__ void colsum(const float* __restrict__ X, float* __restrict__ acc,
-                                       float* __restrict__ red, int tid) {
+                                       float* __restrict__ red, int tid, bool centre_only = false) {
   using L = Layout<W, NH>;
   constexpr int parts = kThreads / W, per = kB / parts;
   const int col = tid % W, part = tid / W;
   float s = 0.0f;
-  for (int r = part * per; r < (part + 1) * per; ++r) s += X[r * L::LDA + col];
+  for (int r = part * per; r < (part + 1) * per; ++r)
+    if (!centre_only || (r & 7) == 0) s += X[r * L::LDA + col];
   red[part * W + col] = s;
   __syncthreads();
   if (tid < W) {
@@ -235,9 +308,12 @@ __device__ __forceinline__ void colsum(const float* __restrict__ X, float* __res
 // W is the kernel width (16, 32, 64); the network's real width wr <= W (prm.width_real) is
 // embedded with zero weights and biases in the padded units (their activations are 0 for tanh
 // and sine, their deltas 0), and only real parameters are read and written.
-template <int W, int NH, int ACT, bool TRAIN>
+// STAB: stencil tiles in the stable difference form (G27; tanh, training pass)
+template <int W, int NH, int ACT, bool TRAIN, bool STAB = false>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpParams prm) {
   static_assert(kB % 32 == 0, "tile rows");
+  static_assert(!STAB || (ACT == NBM_ACT_TANH && TRAIN), "stable form: tanh training pass");
+  constexpr int TPT = STAB ? kB / 8 : kPT;   // stencil points per tile
   constexpr bool SINE = ACT == NBM_ACT_SINE;
   using L = Layout<W, NH, SINE>;
   constexpr int NHH = L::NHH;
@@ -271,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
     int c = prm.counts[prm.cnt_slot[tid]];
     segCnt[tid] = c;
     segStart[tid] = prm.start_slot[tid] >= 0 ? prm.counts[prm.start_slot[tid]] : 0;
-    int per = prm.seg.kind[tid] == kSegStencil ? kPT : kB;
+    int per = prm.seg.kind[tid] == kSegStencil ? TPT : kB;
     segTiles[tid] = (c + per - 1) / per;
   }
   __syncthreads();
@@ -354,9 +430,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
     while (t >= firstTile[seg + 1]) ++seg;
     const int kind = prm.seg.kind[seg], net = prm.seg.net[seg];
     const int lt = t - firstTile[seg];
-    const int per = kind == kSegStencil ? kPT : kB;
+    const int per = kind == kSegStencil ? TPT : kB;
     const int first = lt * per;
     const int nvalid = min(per, segCnt[seg] - first);
+    const bool stab = STAB && kind == kSegStencil;   // block-uniform
     if (net != curNet) {
       __syncthreads();
       if (TRAIN && curNet >= 0) flush(curNet);
@@ -377,7 +454,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
     __syncthreads();
     if (tid < kB) {
       float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
-      if (kind == kSegStencil) {
+      if (stab) {   // row 8k + jr: x, h e_1..3 (P_d), 0 (Q_d, pad)
+        const int k = tid >> 3, jr = tid & 7;
+        if (k < nvalid && jr == 0) {
+          const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[k];
+          x0 = src[0]; x1 = src[1]; x2 = src[2];
+        } else if (k < nvalid && jr < 4) {
+          if (jr == 1) x0 = prm.h; else if (jr == 2) x1 = prm.h; else x2 = prm.h;
+        }
+      } else if (kind == kSegStencil) {
         const int j = tid / kPT, p = tid - j * kPT;
         if (j < 7 && p < nvalid) {
           const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[p];
@@ -400,18 +485,27 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
       constexpr int step = kThreads / W;
       const float w0 = sW1[3 * col], w1 = sW1[3 * col + 1], w2 = sW1[3 * col + 2], bb = sBias[col];
       for (int r = r0; r < kB; r += step) {
-        float z = fmaf(w2, sX[4 * r + 2], fmaf(w1, sX[4 * r + 1], fmaf(w0, sX[4 * r], bb)));
+        float z = fmaf(w2, sX[4 * r + 2], fmaf(w1, sX[4 * r + 1], fmaf(w0, sX[4 * r], (!stab || (r & 7) == 0) ? bb : 0.0f)));
         if (SINE) sincosf(z, &sAct[r * L::LDA + col], &sCos[r * L::LDA + col]);
+        else if (STAB && stab) sAct[r * L::LDA + col] = z;
         else sAct[r * L::LDA + col] = f32_tanh(z);
       }
     }
     __syncthreads();
+    if (STAB && stab) {
+      stab_fwd_pass<W, L::LDA>(sAct, tid);
+      __syncthreads();
+    }
     // ---- hidden GEMMs ----
 #pragma unroll
     for (int l = 0; l < NHH; ++l) {
       fwd_gemm<W, NH, SINE>(sAct + l * kB * L::LDA, sAct + (l + 1) * kB * L::LDA, sWh + l * W * L::LDW,
-                            sBias + (l + 1) * W, tid, sCos + (l + 1) * kB * L::LDA);
+                            sBias + (l + 1) * W, tid, sCos + (l + 1) * kB * L::LDA, STAB && stab);
       __syncthreads();
+      if (STAB && stab) {
+        stab_fwd_pass<W, L::LDA>(sAct + (l + 1) * kB * L::LDA, tid);
+        __syncthreads();
+      }
     }
     // ---- output layer u = wo . h_NH + bo ----
     float* hTop = sAct + (NH - 1) * kB * L::LDA;
@@ -421,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
       for (int k = qq * (W / 4); k < (qq + 1) * (W / 4); ++k) s = fmaf(sWo[k], hTop[r * L::LDA + k], s);
       s += __shfl_xor_sync(0xffffffffu, s, 1);
       s += __shfl_xor_sync(0xffffffffu, s, 2);
-      if (qq == 0) sU[r] = s + sWo[W];
+      if (qq == 0) sU[r] = (!stab || (r & 7) == 0) ? s + sWo[W] : s;   // differences carry no output bias
     }
     __syncthreads();
     if (!TRAIN) {
@@ -430,7 +524,21 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
       continue;
     }
     // ---- residual epilogue -> cotangents (S4) ----
-    if (kind == kSegStencil) {
+    if (STAB && stab) {   // r = c_c u + c_hat sum_d DU_d - b/d (G27); cotangents c_c 2r/N, c_hat 2r/N (Q_d)
+      if (tid < kB) {
+        const int k = tid >> 3, jr = tid & 7;
+        float ub = 0.0f;
+        if (k < nvalid) {
+          const float chat = prm.seg.chat[seg], cc = prm.seg.ccen[seg];
+          const float du = (sU[8 * k + 4] + sU[8 * k + 5]) + sU[8 * k + 6];
+          const float r = fmaf(cc, sU[8 * k], chat * du) - sAux[k];
+          if (jr == 0) lossAcc += 0.5 * (double)prm.two_over_n * (double)r * (double)r;
+          const float rc = prm.two_over_n * r;
+          ub = jr == 0 ? rc * cc : (jr >= 4 && jr < 7) ? rc * chat : 0.0f;
+        }
+        sUb[tid] = ub;
+      }
+    } else if (kind == kSegStencil) {
       if (tid < kPT) {
         float r = 0.0f;
         float cj[6];   // arm coefficients c_j / d: uniform (constant beta) or per point (variable mu)
@@ -478,7 +586,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
       sRed[part * W + col] = s;
       if (tid < 32) {
         float b = 0.0f;
-        for (int r = tid; r < kB; r += 32) b += sUb[r];
+        for (int r = tid; r < kB; r += 32)
+          if (!stab || (r & 7) == 0) b += sUb[r];
         for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
         if (tid == 0) sAWo[W] += b;
       }
@@ -489,10 +598,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
         sAWo[tid] += t;
       }
       const float wo = sWo[col];
-      for (int r = part; r < kB; r += parts) {
-        float hv = hTop[r * L::LDA + col];
-        const float ad = SINE ? sCos[(NH - 1) * kB * L::LDA + r * L::LDA + col] : 1.0f - hv * hv;
-        hTop[r * L::LDA + col] = sUb[r] * wo * ad;
+      if (STAB && stab) {
+        __syncthreads();   // dWo has read h_NH
+        stab_bwd_pass<W, L::LDA>(nullptr, hTop, sUb, sWo, tid);
+      } else {
+        for (int r = part; r < kB; r += parts) {
+          float hv = hTop[r * L::LDA + col];
+          const float ad = SINE ? sCos[(NH - 1) * kB * L::LDA + r * L::LDA + col] : 1.0f - hv * hv;
+          hTop[r * L::LDA + col] = sUb[r] * wo * ad;
+        }
       }
     }
     __syncthreads();
@@ -501,9 +615,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
       float* Gl = sAct + (l + 1) * kB * L::LDA;
       float* Hp = sAct + l * kB * L::LDA;
       dw_gemm<W, NH>(Gl, Hp, dWh[l], tid);
-      colsum<W, NH>(Gl, sAB + (l + 1) * W, sRed, tid);   // db (contains __syncthreads)
-      bwd_gemm<W, NH, SINE>(Gl, Hp, sWh + l * W * L::LDW, tid, sCos + l * kB * L::LDA);
+      colsum<W, NH>(Gl, sAB + (l + 1) * W, sRed, tid, STAB && stab);   // db (contains __syncthreads)
+      bwd_gemm<W, NH, SINE>(Gl, Hp, sWh + l * W * L::LDW, tid, sCos + l * kB * L::LDA, STAB && stab);
       __syncthreads();
+      if (STAB && stab) {   // G_{l+1} W_{l+1} (now in Gl) through the backward map of layer l+1 -> Hp
+        stab_bwd_pass<W, L::LDA>(Gl, Hp, nullptr, nullptr, tid);
+        __syncthreads();
+      }
     }
     {  // layer 1: dW1[n][c] += sum_b G1[b][n] x[b][c]; db1 += sum_b G1[b][n]
       const int col = tid % W, part = tid / W;
@@ -514,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
         s0 = fmaf(g, sX[4 * r], s0);
         s1 = fmaf(g, sX[4 * r + 1], s1);
         s2 = fmaf(g, sX[4 * r + 2], s2);
-        sb += g;
+        if (!stab || (r & 7) == 0) sb += g;
       }
       sRed[(0 * parts + part) * W + col] = s0;
       sRed[(1 * parts + part) * W + col] = s1;
@@ -553,10 +671,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
   }
 }
 
-template <int W, int NH, int ACT, bool TRAIN>
+template <int W, int NH, int ACT, bool TRAIN, bool STAB = false>
 static cudaError_t launch_t(const MlpParams& p, int grid, cudaStream_t s) {
   using L = Layout<W, NH, ACT == NBM_ACT_SINE>;
-  auto kern = k_mlp_fp32<W, NH, ACT, TRAIN>;
+  auto kern = k_mlp_fp32<W, NH, ACT, TRAIN, STAB>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
@@ -605,11 +723,32 @@ static cudaError_t dispatch(int W, int NH, const MlpParams& p, int grid, cudaStr
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
+// the stable form (G27): tanh training pass
+static cudaError_t dispatch_stab(int W, int NH, const MlpParams& p, int grid, cudaStream_t s) {
+  constexpr int T = NBM_ACT_TANH;
+#define NBM_F32_SCASES(WW)                                        \
+  switch (NH) {                                                   \
+    case 1: return launch_t<WW, 1, T, true, true>(p, grid, s);    \
+    case 2: return launch_t<WW, 2, T, true, true>(p, grid, s);    \
+    case 3: return launch_t<WW, 3, T, true, true>(p, grid, s);    \
+    case 4: return launch_t<WW, 4, T, true, true>(p, grid, s);    \
+  }
+  if (W == 16) { NBM_F32_SCASES(16) }
+  if (W == 32) { NBM_F32_SCASES(32) }
+  if (W == 64) { NBM_F32_SCASES(64) }
+#undef NBM_F32_SCASES
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, bool stable, const MlpParams& p, int grid,
                             cudaStream_t s) {
   MlpParams q = p;
   q.width_real = width;
   const int W = kernel_width(width);
+  if (stable && train) {
+    if (act != NBM_ACT_TANH || p.pcoef) return cudaErrorInvalidValue;
+    return dispatch_stab(W, n_hidden, q, grid, s);
+  }
   if (act == NBM_ACT_SINE)
     return train ? dispatch<NBM_ACT_SINE, true>(W, n_hidden, q, grid, s) : dispatch<NBM_ACT_SINE, false>(W, n_hidden, q, grid, s);
   return train ? dispatch<NBM_ACT_TANH, true>(W, n_hidden, q, grid, s) : dispatch<NBM_ACT_TANH, false>(W, n_hidden, q, grid, s);

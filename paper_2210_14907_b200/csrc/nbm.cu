@@ -68,8 +68,9 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
     *why = "arch: bad stencil evaluation";
     return NBM_E_INVALID_ARCH;
   }
-  if (a->stencil == NBM_STENCIL_STABLE && !(a->prec == NBM_PREC_BF16 && a->act == NBM_ACT_TANH)) {
-    *why = "arch: the stable stencil form needs BF16 tanh (W in {64, 128, 256}, G27)";
+  if (a->stencil == NBM_STENCIL_STABLE &&
+      !(a->act == NBM_ACT_TANH && (a->prec == NBM_PREC_BF16 || (a->prec == NBM_PREC_FP32 && mlp_fp32_supported(W, nh, a->act))))) {
+    *why = "arch: the stable stencil form needs tanh, BF16 (W in {64, 128, 256}) or FP32 with W <= 64 (G27)";
     return NBM_E_INVALID_ARCH;
   }
   if (out) {
@@ -257,7 +258,7 @@ cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cu
   if (A.prec == NBM_PREC_BF16)
     return launch_mlp_tc(A.width, A.n_hidden, A.act, 1, train, A.stencil == NBM_STENCIL_STABLE, p, w.grid_base, s);
   if (A.prec == NBM_PREC_FP32X) return launch_mlp_tc(A.width, A.n_hidden, A.act, 3, train, false, p, w.grid_base, s);
-  return launch_mlp_fp32(A.width, A.n_hidden, A.act, train, p, w.grid_base, s);
+  return launch_mlp_fp32(A.width, A.n_hidden, A.act, train, A.stencil == NBM_STENCIL_STABLE, p, w.grid_base, s);
 }
 
 
@@ -308,6 +309,10 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   if (rc) { g_create_error = why; return rc; }
   if (dp.mu_kind != NBM_MU_CONST && !(ai.prec == NBM_PREC_FP32 && ai.width <= 64)) {
     g_create_error = "variable mu: supported by the fp32 kernel with W <= 64 in this build";
+    return NBM_E_INVALID_ARCH;
+  }
+  if (dp.mu_kind != NBM_MU_CONST && ai.stencil == NBM_STENCIL_STABLE) {
+    g_create_error = "the stable stencil form assumes constant mu per phase (G27)";
     return NBM_E_INVALID_ARCH;
   }
   cudaError_t e = cudaSetDevice(device);

@@ -178,7 +178,7 @@ struct MlpParams {
   float* u_out;              // forward-only mode: u_out[item] = u
   const uint16_t* wimg;      // bf16 hidden weights in the tensor-core smem layout [2][NH-1][W*W]
 };
-cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, const MlpParams& p, int grid,
+cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, bool stable, const MlpParams& p, int grid,
                             cudaStream_t s);
 int mlp_fp32_supported(int width, int n_hidden, int act);
 int mlp_fp32_ctas_per_sm();

@@ -195,3 +195,42 @@ def test_stable_full_size_shard_invariance(name, w):
     assert np.linalg.norm(acc_g - gt) <= (2e-3 if w < 256 else 1e-4) * np.linalg.norm(gt)
     assert s.status() == 0
     s.close()
+
+
+@pytest.mark.parametrize("name,sizes,k,n,hq", [("c2", None, 0.0, 1 << 14, None), ("c2", None, 2.0, 5003, None),
+                                                ("c1", None, 0.0, 4096, None), ("c5", [3, 64, 64, 64, 64, 1], 0.0, 1 << 13, None),
+                                                ("c5", [3, 20, 20, 1], 0.0, 3001, None)])
+def test_stable_fp32_strict_parity(orc, name, sizes, k, n, hq):
+    """fp32 stable form (K3f<STAB>): every term, the uncrossed ones included, at the STRICT fp32
+    bars of the north_star (1e-5 loss, 1e-4 gradient; no noise-floor relaxation), where the
+    direct fp32 evaluation needs it (c5 at h = 2/1023: the oracle's fp32 emulation of the
+    direct form is off by up to 5x on the Omega- term)."""
+    cfg = inputs.config(name)
+    if name == "c5":
+        cfg.update(prec=inputs.PREC_FP32)
+    if sizes:
+        cfg["sizes"] = sizes
+    if k:
+        cfg["k"] = (k, 2 * k)
+    cfg["stencil"] = inputs.STENCIL_STABLE
+    nb = max(64, n // 8)
+    s = nbm.Solver(cfg, 0, max_points=max(n, nb))
+    pb, ar = orc.from_config(cfg)
+    pts = orc.sample(0, 3, 0, 0, n, cfg["H"])
+    bpts = orc.sample(1, 3, 0, 0, nb, cfg["H"])
+    th = orc.init_params(ar, 0)
+    L, lt, g, gt = orc.loss_grad(pb, ar, th, pts, bpts, cfg["h"], per_term=True)
+    dth, dp, db = _dev(th), _dev(pts), _dev(bpts)
+    gl, gg = _run(s, dth, dp, db)
+    assert abs(gl - L) <= 1e-5 * L, (gl, L)
+    assert _rel(gg, g) <= 1e-4
+    gl2, gg2 = _run(s, dth, dp, db)
+    assert gl2 == gl and np.array_equal(gg2, gg)
+    for kk, term in enumerate(TERMS):
+        tl, tg = _run(s, dth, dp, db, terms=term)
+        if lt[kk] == 0.0:
+            assert tl == 0.0
+            continue
+        assert abs(tl - lt[kk]) <= 1e-5 * lt[kk], (kk, tl, lt[kk])
+        assert _rel(tg, gt[kk]) <= 1e-4, (kk, _rel(tg, gt[kk]))
+    s.close()
