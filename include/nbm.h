@@ -79,8 +79,9 @@ extern "C" {
                                * the centre activation, the first differences a(x + h e_d) - a(x) and
                                * the second differences a(x + h e_d) + a(x - h e_d) - 2 a(x) (tanh
                                * addition theorem, no cancellation), r = (k/d) u + c_hat sum_d D_d u
-                               * - b/d; resolves r in bf16 at small h.  BF16 tanh, W in {64, 128};
-                               * crossed and boundary rows are evaluated directly */
+                               * - b/d; resolves r at small h (bf16 to ~1e-2, fp32 to the fp32
+                               * bars).  Tanh networks, BF16 or FP32, constant mu; crossed and
+                               * boundary rows are evaluated directly */
 
 #define NBM_POINTS_INTERIOR 0
 #define NBM_POINTS_BOUNDARY 1

@@ -17,6 +17,7 @@
 #include <math.h>
 
 #include "nbm_internal.cuh"
+#include "stab.cuh"
 
 namespace nbm {
 
@@ -72,11 +73,14 @@ __device__ __forceinline__ void red4(float* p, float a, float b, float c, float 
 
 }  // namespace
 
-template <int W, int NH, bool TRAIN>
+// STAB: stencil tiles in the stable difference form (G27; training pass): R / 8 points per tile
+template <int W, int NH, bool TRAIN, bool STAB = false>
 __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, const float* __restrict__ wimg,
                                                         float* __restrict__ rep, int nrep) {
   using L = FW<W, NH>;
-  constexpr int R = L::R, PT = L::PT, NS = L::NS, NHH = L::NHH;
+  static_assert(!STAB || TRAIN, "stable form: training pass");
+  constexpr int R = L::R, NS = L::NS, NHH = L::NHH;
+  constexpr int PT = STAB ? R / 8 : L::PT;   // stencil points per tile
   extern __shared__ __align__(16) float sm[];
   float* sAct = sm + L::oAct;
   float* sSl = sm + L::oSl;
@@ -173,13 +177,13 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
     primed = next;
   };
   // column sums over the tile's rows (fixed order): acc[col] += sum_r X[r][col] * (wr ? wr[r] : 1)
-  auto colsum = [&](const float* X, const float* wr, float* accv) {
+  auto colsum = [&](const float* X, const float* wr, float* accv, bool centre_only = false) {
     constexpr int parts = kThr / W > 0 ? kThr / W : 1;
     const int col = tid % W, part = tid / W;
     if (part < parts) {
       float s = 0.0f;
       for (int r = part * (R / parts); r < (part + 1) * (R / parts); ++r)
-        s = wr ? fmaf(wr[r], X[r * W + col], s) : s + X[r * W + col];
+        if (!centre_only || (r & 7) == 0) s = wr ? fmaf(wr[r], X[r * W + col], s) : s + X[r * W + col];
       sRed[part * W + col] = s;
     }
     __syncthreads();
@@ -258,6 +262,7 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
     const int first = (t - firstTile[seg]) * per;
     const int nvalid = min(per, segCnt[seg] - first);
     const int nextNet = t + 1 < t1 ? net_of_tile(t + 1) : -1;
+    const bool stab = STAB && kind == kSegStencil;   // block-uniform
     if (net != curNet) {
       __syncthreads();
       if (TRAIN && curNet >= 0) flush_small(curNet);
@@ -278,7 +283,15 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
     __syncthreads();
     if (tid < R) {
       float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
-      if (kind == kSegStencil) {
+      if (stab) {   // row 8k + jr: x, h e_1..3 (P_d), 0 (Q_d, pad)
+        const int k = tid >> 3, jr = tid & 7;
+        if (k < nvalid && jr == 0) {
+          const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[k];
+          x0 = src[0]; x1 = src[1]; x2 = src[2];
+        } else if (k < nvalid && jr < 4) {
+          if (jr == 1) x0 = prm.h; else if (jr == 2) x1 = prm.h; else x2 = prm.h;
+        }
+      } else if (kind == kSegStencil) {
         const int j = tid / PT, p = tid - j * PT;
         if (j < 7 && p < nvalid) {
           const float* src = prm.seg.src[seg] + 3 * (int64_t)sItem[p];
@@ -298,10 +311,15 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
     // ---- layer 1 (K = 3) ----
     for (int e = tid; e < R * W; e += kThr) {
       const int r = e / W, n = e % W;
-      const float z = fmaf(sW1[3 * n + 2], sX[4 * r + 2], fmaf(sW1[3 * n + 1], sX[4 * r + 1], fmaf(sW1[3 * n], sX[4 * r], sBias[n])));
-      sAct[e] = tanhf(z);
+      const float b = (!stab || (r & 7) == 0) ? sBias[n] : 0.0f;   // stable form: bias on the centre rows
+      const float z = fmaf(sW1[3 * n + 2], sX[4 * r + 2], fmaf(sW1[3 * n + 1], sX[4 * r + 1], fmaf(sW1[3 * n], sX[4 * r], b)));
+      sAct[e] = (STAB && stab) ? z : tanhf(z);
     }
     __syncthreads();
+    if (STAB && stab) {
+      stab::fwd_pass_f32<W, W, R / 8, kThr>(sAct, tid);
+      __syncthreads();
+    }
     // ---- hidden layers: h_l = tanh(h_{l-1} W_l^T + b_l) ----
 #pragma unroll 1
     for (int l = 2; l <= NH; ++l) {
@@ -311,10 +329,21 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
       gemm(sAct + (l - 2) * R * W, img_of(net, l, 0), next, acc);
       const float4 bv = *reinterpret_cast<const float4*>(sBias + (l - 1) * W + c0);
       float* out = sAct + (l - 1) * R * W;
+      if (STAB && stab) {   // raw pre-activations (bias on the centre rows), then the stable map
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        *reinterpret_cast<float4*>(out + (r0 + i) * W + c0) =
-            make_float4(tanhf(acc[i][0] + bv.x), tanhf(acc[i][1] + bv.y), tanhf(acc[i][2] + bv.z), tanhf(acc[i][3] + bv.w));
+        for (int i = 0; i < 8; ++i) {
+          const float m = ((r0 + i) & 7) == 0 ? 1.0f : 0.0f;
+          *reinterpret_cast<float4*>(out + (r0 + i) * W + c0) =
+              make_float4(fmaf(m, bv.x, acc[i][0]), fmaf(m, bv.y, acc[i][1]), fmaf(m, bv.z, acc[i][2]), fmaf(m, bv.w, acc[i][3]));
+        }
+        __syncthreads();
+        stab::fwd_pass_f32<W, W, R / 8, kThr>(out, tid);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          *reinterpret_cast<float4*>(out + (r0 + i) * W + c0) =
+              make_float4(tanhf(acc[i][0] + bv.x), tanhf(acc[i][1] + bv.y), tanhf(acc[i][2] + bv.z), tanhf(acc[i][3] + bv.w));
+      }
       __syncthreads();
     }
     // ---- output layer u = wo . h_NH + bo ----
@@ -326,7 +355,7 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
       for (int k = q * span; k < (q + 1) * span; ++k) s = fmaf(sWo[k], hTop[r * W + k], s);
 #pragma unroll
       for (int o = 1; o < L::TPR; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (q == 0) sU[r] = s + sWo[W];
+      if (q == 0) sU[r] = (!stab || (r & 7) == 0) ? s + sWo[W] : s;   // differences carry no output bias
     }
     __syncthreads();
     if (!TRAIN) {
@@ -335,7 +364,21 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
       continue;
     }
     // ---- residual epilogue -> cotangents (S4) ----
-    if (kind == kSegStencil) {
+    if (STAB && stab) {   // r = c_c u + c_hat sum_d DU_d - b/d (G27); cotangents c_c 2r/N, c_hat 2r/N (Q_d)
+      if (tid < R) {
+        const int k = tid >> 3, jr = tid & 7;
+        float ub = 0.0f;
+        if (k < nvalid) {
+          const float chat = prm.seg.chat[seg], cc = prm.seg.ccen[seg];
+          const float du = (sU[8 * k + 4] + sU[8 * k + 5]) + sU[8 * k + 6];
+          const float r = fmaf(cc, sU[8 * k], chat * du) - sAux[k];
+          if (jr == 0) lossAcc += 0.5 * (double)prm.two_over_n * (double)r * (double)r;
+          const float rc = prm.two_over_n * r;
+          ub = jr == 0 ? rc * cc : (jr >= 4 && jr < 7) ? rc * chat : 0.0f;
+        }
+        sUb[tid] = ub;
+      }
+    } else if (kind == kSegStencil) {
       if (tid < PT) {
         float r = 0.0f;
         if (tid < nvalid) {
@@ -372,15 +415,21 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
     colsum(hTop, sUb, sAWo);   // dwo += sum_r ub h_NH
     if (tid < 32) {
       float b = 0.0f;
-      for (int r = tid; r < R; r += 32) b += sUb[r];
+      for (int r = tid; r < R; r += 32)
+        if (!stab || (r & 7) == 0) b += sUb[r];
 #pragma unroll
       for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
       if (tid == 0) sAWo[W] += b;
     }
-    for (int e = tid; e < R * W; e += kThr) {
-      const int r = e / W, n = e % W;
-      const float hv = hTop[e];
-      hTop[e] = sUb[r] * sWo[n] * (1.0f - hv * hv);
+    if (STAB && stab) {
+      __syncthreads();   // dwo has read h_NH
+      stab::bwd_pass_f32<W, W, R / 8, kThr>(nullptr, hTop, sUb, sWo, tid);
+    } else {
+      for (int e = tid; e < R * W; e += kThr) {
+        const int r = e / W, n = e % W;
+        const float hv = hTop[e];
+        hTop[e] = sUb[r] * sWo[n] * (1.0f - hv * hv);
+      }
     }
     __syncthreads();
 #pragma unroll 1
@@ -388,10 +437,20 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
       float* Gl = sAct + (l - 1) * R * W;
       float* Hp = sAct + (l - 2) * R * W;
       dw_flush(Gl, Hp, l, net);
-      colsum(Gl, nullptr, sAB + (l - 1) * W);   // db_l (contains __syncthreads)
+      colsum(Gl, nullptr, sAB + (l - 1) * W, STAB && stab);   // db_l (contains __syncthreads)
       const float* next = l > 2 ? img_of(net, l - 1, 1) : (nextNet >= 0 ? img_of(nextNet, 2, 0) : nullptr);
       float acc[8][4];
       gemm(Gl, img_of(net, l, 1), next, acc);   // (G_l W_l)[r][i]
+      if (STAB && stab) {   // the products over the consumed G_l, then the backward map -> Hp
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          *reinterpret_cast<float4*>(Gl + (r0 + i) * W + c0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        __syncthreads();
+        stab::bwd_pass_f32<W, W, R / 8, kThr>(Gl, Hp, nullptr, nullptr, tid);
+        __syncthreads();
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         float* p = Hp + (r0 + i) * W + c0;
@@ -409,7 +468,7 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
           s0 = fmaf(g, sX[4 * r], s0);
           s1 = fmaf(g, sX[4 * r + 1], s1);
           s2 = fmaf(g, sX[4 * r + 2], s2);
-          sb += g;
+          if (!stab || (r & 7) == 0) sb += g;
         }
         sAW1[3 * n] += s0;
         sAW1[3 * n + 1] += s1;
@@ -434,10 +493,10 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
   }
 }
 
-template <int W, int NH, bool TRAIN>
+template <int W, int NH, bool TRAIN, bool STAB = false>
 static cudaError_t launch_fw_t(const MlpParams& p, const float* wimg, float* rep, int nrep, int grid, cudaStream_t s) {
   using L = FW<W, NH>;
-  auto kern = k_mlp_fp32w<W, NH, TRAIN>;
+  auto kern = k_mlp_fp32w<W, NH, TRAIN, STAB>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
@@ -452,9 +511,21 @@ int mlp_fp32w_supported(int width, int n_hidden) {
   return (width == 128 || width == 256) && n_hidden >= 2 && n_hidden <= 4;
 }
 
-cudaError_t launch_mlp_fp32w(int width, int n_hidden, bool train, const MlpParams& p, const float* wimg, float* rep,
-                             int nrep, int grid, cudaStream_t s) {
+cudaError_t launch_mlp_fp32w(int width, int n_hidden, bool train, bool stable, const MlpParams& p, const float* wimg,
+                             float* rep, int nrep, int grid, cudaStream_t s) {
   if (nrep < 1) return cudaErrorInvalidValue;
+  if (stable && train) {
+#define NBM_FW_SCASES(WW)                                                          \
+  switch (n_hidden) {                                                              \
+    case 2: return launch_fw_t<WW, 2, true, true>(p, wimg, rep, nrep, grid, s);    \
+    case 3: return launch_fw_t<WW, 3, true, true>(p, wimg, rep, nrep, grid, s);    \
+    case 4: return launch_fw_t<WW, 4, true, true>(p, wimg, rep, nrep, grid, s);    \
+  }
+    if (width == 256) { NBM_FW_SCASES(256) }
+    if (width == 128) { NBM_FW_SCASES(128) }
+#undef NBM_FW_SCASES
+    return cudaErrorInvalidValue;
+  }
 #define NBM_FW_CASES(WW)                                                                              \
   switch (n_hidden) {                                                                                 \
     case 2: return train ? launch_fw_t<WW, 2, true>(p, wimg, rep, nrep, grid, s)                      \

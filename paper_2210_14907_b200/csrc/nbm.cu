@@ -69,8 +69,8 @@ int check_arch(const nbm_arch* a, ArchInfo* out, std::string* why) {
     return NBM_E_INVALID_ARCH;
   }
   if (a->stencil == NBM_STENCIL_STABLE &&
-      !(a->act == NBM_ACT_TANH && (a->prec == NBM_PREC_BF16 || (a->prec == NBM_PREC_FP32 && mlp_fp32_supported(W, nh, a->act))))) {
-    *why = "arch: the stable stencil form needs tanh, BF16 (W in {64, 128, 256}) or FP32 with W <= 64 (G27)";
+      !(a->act == NBM_ACT_TANH && (a->prec == NBM_PREC_BF16 || a->prec == NBM_PREC_FP32))) {
+    *why = "arch: the stable stencil form needs tanh with BF16 or FP32 (G27)";
     return NBM_E_INVALID_ARCH;
   }
   if (out) {
@@ -254,7 +254,9 @@ cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cu
   if (is_w256(A))
     return launch_mlp_w256(A.n_hidden, train, A.stencil == NBM_STENCIL_STABLE, p, w.wimg, w.wimg_b, w.hscr, w.rep,
                            w.nrep, w.grid_base, s);
-  if (is_fp32w(A)) return launch_mlp_fp32w(A.width, A.n_hidden, train, p, w.wimg32, w.rep, w.nrep, w.grid_base, s);
+  if (is_fp32w(A))
+    return launch_mlp_fp32w(A.width, A.n_hidden, train, A.stencil == NBM_STENCIL_STABLE, p, w.wimg32, w.rep, w.nrep,
+                            w.grid_base, s);
   if (A.prec == NBM_PREC_BF16)
     return launch_mlp_tc(A.width, A.n_hidden, A.act, 1, train, A.stencil == NBM_STENCIL_STABLE, p, w.grid_base, s);
   if (A.prec == NBM_PREC_FP32X) return launch_mlp_tc(A.width, A.n_hidden, A.act, 3, train, false, p, w.grid_base, s);

@@ -190,8 +190,8 @@ int mlp_tc_ctas_per_sm(int width, int n_hidden, int planes);
 cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t* wimg, cudaStream_t s);
 // mlp_fp32w.cu (fp32, W = 128 / 256: streamed weights, per-tile dW flushes into replicas)
 int mlp_fp32w_supported(int width, int n_hidden);
-cudaError_t launch_mlp_fp32w(int width, int n_hidden, bool train, const MlpParams& p, const float* wimg, float* rep,
-                             int nrep, int grid, cudaStream_t s);
+cudaError_t launch_mlp_fp32w(int width, int n_hidden, bool train, bool stable, const MlpParams& p, const float* wimg,
+                             float* rep, int nrep, int grid, cudaStream_t s);
 cudaError_t launch_pack_fp32w(const ArchInfo& a, const float* theta, float* img, cudaStream_t s);
 // mlp_w256.cu (tcgen05 bf16, W = 256: streamed weights, parked activations, dW replicas)
 cudaError_t launch_mlp_w256(int n_hidden, bool train, bool stable, const MlpParams& m, const uint16_t* wf, const uint16_t* wb,

@@ -103,5 +103,66 @@ __device__ __forceinline__ void stab_bwd(float (&v)[N], const float (&hq)[N], in
   }
 }
 
+// ---- fp32 kernels (K3f, K3fw): one thread per (point, column) of a stencil tile in shared memory, rows 8k..8k+7 = centre, P_x, P_y, P_z, Q_x, Q_y, Q_z, pad (fp32-accurate
+// maps: tanhf, the series of tanh d - d to d^11 below 1/4, IEEE division) ----
+__device__ __forceinline__ float tanh_minus_id_f32(float d) {
+  const float d2 = d * d;
+  const float s = fmaf(d2, fmaf(d2, fmaf(d2, fmaf(d2, -1382.0f / 155925.0f, 62.0f / 2835.0f), -17.0f / 315.0f),
+                                2.0f / 15.0f), -1.0f / 3.0f) * (d * d2);
+  return fabsf(d) < 0.25f ? s : tanhf(d) - d;
+}
+__device__ __forceinline__ float stab_g_f32(float t, float s2, float d) {
+  const float s = tanh_minus_id_f32(d), x = t * (d + s);
+  return s2 * fmaf(-x, d, s) / (1.0f + x);
+}
+// in place: z (bias included), p_d, D_d -> t = tanh z, P_d, Q_d
+template <int W, int LDA, int NPTS, int NTHR>
+__device__ void fwd_pass_f32(float* __restrict__ H, int tid) {
+  for (int it = tid; it < NPTS * W; it += NTHR) {
+    float* h = H + (it / W) * 8 * LDA + it % W;
+    const float t = tanhf(h[0]);
+    const float s2 = (1.0f - t) * (1.0f + t);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float p = h[(1 + d) * LDA], D = h[(4 + d) * LDA];
+      const float gp = stab_g_f32(t, s2, p), gm = stab_g_f32(t, s2, D - p);
+      h[(1 + d) * LDA] = fmaf(s2, p, gp);
+      h[(4 + d) * LDA] = fmaf(s2, D, gp) + gm;
+    }
+    h[0] = t;
+    h[7 * LDA] = 0.0f;
+  }
+}
+// G of the point's rows from the upstream gradients R (g_a, g_P, g_Q; R = null: the output
+// layer's ub_row wo_col) and the activations H (t, P, Q), written over H
+template <int W, int LDA, int NPTS, int NTHR>
+__device__ void bwd_pass_f32(const float* __restrict__ R, float* __restrict__ H, const float* __restrict__ ub,
+                             const float* __restrict__ wo, int tid) {
+  for (int it = tid; it < NPTS * W; it += NTHR) {
+    const int k = it / W, col = it % W;
+    float* h = H + k * 8 * LDA + col;
+    auto up = [&](int j) { return R ? R[(k * 8 + j) * LDA + col] : ub[k * 8 + j] * wo[col]; };
+    const float t = h[0], t2 = t + t;
+    float gz = up(0) * ((1.0f - t) * (1.0f + t));
+    float gp[3], gd[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float P = h[(1 + d) * LDA], Q = h[(4 + d) * LDA], M = Q - P;
+      const float gP = up(1 + d), gQ = up(4 + d);
+      gz -= gP * P * (t2 + P) + gQ * fmaf(t2, Q, fmaf(P, P, M * M));
+      const float tp = t + P, tm = t + M;
+      gp[d] = fmaf(gP, (1.0f - tp) * (1.0f + tp), gQ * (M - P) * (t2 + M + P));
+      gd[d] = gQ * ((1.0f - tm) * (1.0f + tm));
+    }
+    h[0] = gz;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      h[(1 + d) * LDA] = gp[d];
+      h[(4 + d) * LDA] = gd[d];
+    }
+    h[7 * LDA] = 0.0f;
+  }
+}
+
 }  // namespace stab
 }  // namespace nbm

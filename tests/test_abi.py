@@ -62,7 +62,8 @@ def test_stable_stencil_descriptor_rules(lib):
     assert nbm.nbm_check(nbm.Descriptors(dict(inputs.config("c5", width=64), stencil=S))) == 0
     assert nbm.nbm_check(nbm.Descriptors(dict(inputs.config("c4"), stencil=S))) == 0
     assert nbm.nbm_check(nbm.Descriptors(dict(inputs.config("c2"), stencil=S))) == 0   # fp32 W <= 64
-    for bad in (dict(inputs.config("c5", width=128, prec=inputs.PREC_FP32), stencil=S),   # fp32 W = 128
+    assert nbm.nbm_check(nbm.Descriptors(dict(inputs.config("c5", width=128, prec=inputs.PREC_FP32), stencil=S))) == 0
+    for bad in (dict(inputs.config("c2"), stencil=S, prec=inputs.PREC_FP32X),           # fp32x
                 dict(inputs.config("c3"), stencil=S),                     # SiLU
                 dict(inputs.config("c5", width=128), stencil=2)):         # unknown mode
         assert nbm.nbm_check(nbm.Descriptors(bad)) == 1

@@ -199,7 +199,9 @@ def test_stable_full_size_shard_invariance(name, w):
 
 @pytest.mark.parametrize("name,sizes,k,n,hq", [("c2", None, 0.0, 1 << 14, None), ("c2", None, 2.0, 5003, None),
                                                 ("c1", None, 0.0, 4096, None), ("c5", [3, 64, 64, 64, 64, 1], 0.0, 1 << 13, None),
-                                                ("c5", [3, 20, 20, 1], 0.0, 3001, None)])
+                                                ("c5", [3, 20, 20, 1], 0.0, 3001, None),
+                                                ("c5", [3, 128, 128, 128, 1], 0.0, 4099, None),
+                                                ("c5", [3, 256, 256, 1], 1.5, 2048, None)])
 def test_stable_fp32_strict_parity(orc, name, sizes, k, n, hq):
     """fp32 stable form (K3f<STAB>): every term, the uncrossed ones included, at the STRICT fp32
     bars of the north_star (1e-5 loss, 1e-4 gradient; no noise-floor relaxation), where the
@@ -225,7 +227,10 @@ def test_stable_fp32_strict_parity(orc, name, sizes, k, n, hq):
     assert abs(gl - L) <= 1e-5 * L, (gl, L)
     assert _rel(gg, g) <= 1e-4
     gl2, gg2 = _run(s, dth, dp, db)
-    assert gl2 == gl and np.array_equal(gg2, gg)
+    if cfg["sizes"][1] <= 64:
+        assert gl2 == gl and np.array_equal(gg2, gg)
+    else:   # K3fw: L2 reductions, deterministic within tolerance (G21)
+        assert abs(gl2 - gl) <= 1e-6 * gl and _rel(gg2, gg) <= 1e-6
     for kk, term in enumerate(TERMS):
         tl, tg = _run(s, dth, dp, db, terms=term)
         if lt[kk] == 0.0:
