@@ -53,3 +53,28 @@ def test_training_reduces_error_and_is_deterministic():
     assert np.median(losses[-k:]) < np.median(losses[:k])
     r2 = train.train(cfg, 8, 300, log_every=10)
     assert (r2["rmse"], r2["linf"]) == (r["rmse"], r["linf"])
+
+
+def test_error_norms_on_a_sampled_level_set(orc):
+    """The side of each nodal point comes from the sampled (grid) level set: the
+    error norms still match the oracle's, which evaluates the same trilinear phi."""
+    cfg = inputs.with_grid(inputs.config("c2"), 32)
+    s = nbm.Solver(cfg, 0, max_points=2048)
+    pb, ar = orc.from_config(cfg)
+    th = inputs.random_theta(cfg["sizes"], cfg["n_nets"], 6)
+    rmse, linf = s.error_norms(24, theta=_dev(th))
+    o_rmse, o_linf = orc.error_norms(pb, ar, th, 24)
+    assert rmse == pytest.approx(o_rmse, rel=1e-5)
+    assert linf == pytest.approx(o_linf, rel=1e-5)
+    s.close()
+
+
+def test_training_multilevel_and_lr_phases():
+    """train() with two implicit levels and an lr schedule of two captured graphs:
+    runs, stays finite, lowers the error, and is bitwise repeatable."""
+    cfg = inputs.config("p41")
+    kw = dict(levels=2, lr_schedule=[(0.5, 2e-3), (0.5, 5e-4)], log_every=50)
+    r = train.train(cfg, 8, 200, **kw)
+    assert np.isfinite(r["rmse"]) and r["rmse"] < 0.5 * r["rmse_init"]
+    r2 = train.train(cfg, 8, 200, **kw)
+    assert (r2["rmse"], r2["linf"]) == (r["rmse"], r["linf"])
