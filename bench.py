@@ -365,6 +365,10 @@ def main():
         peak = peaks["bf16_tflops"]
         bound, peak_note = "tensor", f"bf16 dense, {src} (MEASURED_PEAKS.json)"
     achieved = flop_launch / mlp_avg_s / 1e12
+    # secondary bound: the MUFU ceiling, one transcendental per hidden activation of
+    # the forward, 16 per clock per SM (B200 MUFU; accurate fp32 tanhf costs more than one)
+    acts_launch = sum(cfg["sizes"][1:-1]) * (args.levels * 7 * N + Nb) / args.levels
+    mufu_ms = acts_launch / (148 * 16 * 1.965e9) * 1e3
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{cfg['label']}.json")
     if os.path.exists(tp):
@@ -387,7 +391,10 @@ def main():
                         if cfg["prec"] in (inputs.PREC_FP32, inputs.PREC_FP32X) else {}),
                      "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name(cfg) + " fused fwd/residual/bwd",
                      "flop_per_launch": flop_launch, "avg_launch_ms": mlp_avg_s * 1e3,
-                     "share_of_step": mlp_ms / eager_ms, "peak_src": peak_note},
+                     "share_of_step": mlp_ms / eager_ms, "peak_src": peak_note,
+                     "secondary": {"bound": "mufu", "activations_per_launch": acts_launch,
+                                   "t_ms": mufu_ms, "frac": mufu_ms / (mlp_avg_s * 1e3),
+                                   "peak_src": "148 SM x 16 MUFU/clk x 1965 MHz (derived)"}},
         "gpu_launches": launches_per_step * args.steps,
         "launch_mode": mode, "ms_per_step_eager": eager_ms / args.steps,
         "clocks": clocks,
