@@ -672,8 +672,14 @@ static cudaError_t dispatch_stab(int W, int NH, const MlpParams& p, int grid, cu
     case 3: return launch_t<WW, 3, T, true, true>(p, grid, s);    \
     case 4: return launch_t<WW, 4, T, true, true>(p, grid, s);    \
   }
-  if (W == 16) { NBM_F32_SCASES(16) }
-  if (W == 32) { NBM_F32_SCASES(32) }
+  if (W == 16) {
+    if (NH == 5) return launch_t<16, 5, T, true, true>(p, grid, s);
+    NBM_F32_SCASES(16)
+  }
+  if (W == 32) {
+    if (NH == 5) return launch_t<32, 5, T, true, true>(p, grid, s);
+    NBM_F32_SCASES(32)
+  }
   if (W == 64) { NBM_F32_SCASES(64) }
 #undef NBM_F32_SCASES
   return cudaErrorInvalidValue;

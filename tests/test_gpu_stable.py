@@ -201,7 +201,9 @@ def test_stable_full_size_shard_invariance(name, w):
                                                 ("c1", None, 0.0, 4096, None), ("c5", [3, 64, 64, 64, 64, 1], 0.0, 1 << 13, None),
                                                 ("c5", [3, 20, 20, 1], 0.0, 3001, None),
                                                 ("c5", [3, 128, 128, 128, 1], 0.0, 4099, None),
-                                                ("c5", [3, 256, 256, 1], 1.5, 2048, None)])
+                                                ("c5", [3, 256, 256, 1], 1.5, 2048, None),
+                                                ("c2", [3, 16, 1], 0.0, 2000, None),
+                                                ("c2", [3, 24, 24, 24, 24, 24, 1], 0.0, 2000, None)])
 def test_stable_fp32_strict_parity(orc, name, sizes, k, n, hq):
     """fp32 stable form (K3f<STAB>): every term, the uncrossed ones included, at the STRICT fp32
     bars of the north_star (1e-5 loss, 1e-4 gradient; no noise-floor relaxation), where the
