@@ -44,7 +44,8 @@ constexpr int kTPTS = 16;  // stencil points per tile of the stable form (G27): 
 // is split exactly into three bf16 planes x = x1 + x2 + x3 (x1 = bf16(x), x2 = bf16(x - x1),
 // x3 = bf16(x - x1 - x2)) and each GEMM sums the six plane products with i + j <= 2 (the three
 // dropped ones are below 2^-24 relative), fp32 accumulation in TMEM (PREC_FP32X, G26).
-template <int W, int NH, int ACT, int P = 1>
+// STG: columns of the fp32 staging tile of the shared-memory stable maps (0: none)
+template <int W, int NH, int ACT, int P = 1, int STG = 0>
 struct TcLayout {
   static_assert(P == 1 || (P == 3 && ACT == NBM_ACT_TANH), "plane split: tanh with resident weights");
   static constexpr bool SILU = ACT == NBM_ACT_SILU;
@@ -75,7 +76,9 @@ struct TcLayout {
   static constexpr uint32_t oAux = oUb + 4 * kTB;          // fp32 [kTB]
   static constexpr uint32_t oItem = oAux + 4 * kTB;        // int  [kTB]
   static constexpr uint32_t oBar = oItem + 4 * kTB;        // mbarriers (MMA, weights) + tmem base
-  static constexpr uint32_t bytes = oBar + 64;
+  static constexpr int SLD = STG + 4;                       // staging row stride (floats)
+  static constexpr uint32_t oStg = oBar + 64;              // fp32 [kTB][SLD] (stable form, W = 64)
+  static constexpr uint32_t bytes = oStg + (STG > 0 ? 4 * kTB * SLD : 0);
   static constexpr uint32_t TMEM_COLS = (W * NH <= 128) ? 128 : (W * NH <= 256) ? 256 : 512;
   // CTAs per SM requested from the launch (TMEM permitting; the host sizes the partial slots with
   // mlp_tc_ctas_per_sm, which must agree): the three-plane split runs one CTA per SM
@@ -213,9 +216,16 @@ __device__ long long g_tc_trace[8][32];
 #endif
 
 // STAB: stencil tiles in the stable difference form (G27; bf16, tanh, training pass only)
+// stable maps staged through shared memory, one thread per (point, column) (W = 64, where the
+// staging tile fits next to two CTAs per SM); W = 128 uses the in-register octet maps
+template <int W, bool STAB>
+constexpr int tc_stage_cols() { return (STAB && W == 64) ? 32 : 0; }
+
 template <int W, int NH, int ACT, bool TRAIN, int P = 1, bool STAB = false>
-__global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, NH, ACT, P>::MINB) k_mlp_tc(const MlpParams prm) {
-  using L = TcLayout<W, NH, ACT, P>;
+__global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>()>::THREADS,
+                                  TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>()>::MINB) k_mlp_tc(const MlpParams prm) {
+  using L = TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>()>;
+  constexpr bool SST = tc_stage_cols<W, STAB>() > 0;
   static_assert(!STAB || (P == 1 && ACT == NBM_ACT_TANH && TRAIN), "stable form: bf16 tanh training pass");
   constexpr int TPT = STAB ? kTPTS : kTPT;   // stencil points per tile
   constexpr uint32_t AP = L::ACT_BYTES, WP = L::WMAT_BYTES;   // plane strides (P = 3)
@@ -435,6 +445,87 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
     phase ^= 1;
     tc::tc_fence_after();
   };
+  // ---- stable maps through shared memory (SST, W = 64): per 32-column round, the owners of the
+  // round's chunk stage their rows (fp32), one thread per (point, column) maps the point's 7 rows
+  // in place, the owners read them back ----
+  float* sStg = reinterpret_cast<float*>(smem + L::oStg);
+  constexpr int SLD = L::SLD;
+  auto stage_round = [&](float (&v)[32], int rc, auto&& item) {
+    if (chunk == rc) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(sStg + row * SLD + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    __syncthreads();
+    for (int it = tid; it < kTPTS * 32; it += THREADS) item(it >> 5, it & 31);
+    __syncthreads();
+    if (chunk == rc) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = *reinterpret_cast<const float4*>(sStg + row * SLD + 4 * q);
+        v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+      }
+    }
+    __syncthreads();
+  };
+  // forward: v = the row's raw pre-activation (no bias) -> a, P_d, Q_d; bl = the layer's biases
+  auto stage_fwd = [&](float (&v)[32], const float* bl) {
+    for (int rc = 0; rc < L::CH; ++rc)
+      stage_round(v, rc, [&](int k, int c) {
+        float* h = sStg + 8 * k * SLD + c;
+        const float t = tanh_fast(h[0] + bl[32 * rc + c]);
+        const float s2 = fmaf(-t, t, 1.0f);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const float p = h[(1 + d) * SLD], D = h[(4 + d) * SLD];
+          const float gp = stab::stab_g(t, s2, p), gm = stab::stab_g(t, s2, D - p);
+          h[(1 + d) * SLD] = fmaf(s2, p, gp);
+          h[(4 + d) * SLD] = fmaf(s2, D, gp) + gm;
+        }
+        h[0] = t;
+        h[7 * SLD] = 0.0f;
+      });
+  };
+  // backward: top (hbufA == 0): v = h_NH (fp32), upstream ub wo; else v = the upstream products
+  // and the activations are the bf16 copies in hbufA.  v <- (g_z, g_p, g_D)
+  auto stage_bwd = [&](float (&v)[32], uint32_t hbufA) {
+    const uint16_t* hb16 = reinterpret_cast<const uint16_t*>(smem + (hbufA - sbase));
+    for (int rc = 0; rc < L::CH; ++rc)
+      stage_round(v, rc, [&](int k, int c) {
+        float* g = sStg + 8 * k * SLD + c;
+        const int col = 32 * rc + c;
+        float H[7], R[7];
+#pragma unroll
+        for (int j = 0; j < 7; ++j) {
+          if (hbufA) {
+            H[j] = __uint_as_float((uint32_t)hb16[(core_off(kTB, 8 * k + j, col >> 3) + (col & 7) * 2) >> 1] << 16);
+            R[j] = g[j * SLD];
+          } else {
+            H[j] = g[j * SLD];
+            R[j] = sUb[8 * k + j] * sWo[col];
+          }
+        }
+        const float t = H[0], t2 = t + t;
+        float gz = R[0] * fmaf(-t, t, 1.0f);
+        float gp[3], gd[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const float P = H[1 + d], Q = H[4 + d], M = Q - P, gP = R[1 + d], gQ = R[4 + d];
+          gz -= gP * P * (t2 + P) + gQ * fmaf(t2, Q, fmaf(P, P, M * M));
+          const float tp = t + P, tm = t + M;
+          gp[d] = fmaf(gP, fmaf(-tp, tp, 1.0f), gQ * (M - P) * (t2 + M + P));
+          gd[d] = gQ * fmaf(-tm, tm, 1.0f);
+        }
+        g[0] = gz;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          g[(1 + d) * SLD] = gp[d];
+          g[(4 + d) * SLD] = gd[d];
+        }
+        g[7 * SLD] = 0.0f;
+      });
+  };
+
   // layer 1 for this thread's 32 columns: h = tanh(W1 x + b1); on a stable-form tile the row
   // input is x (centre), h e_d (P_d rows) or 0 (Q_d rows, pad) and the bias enters the centre only
   auto layer1 = [&](float x0, float x1, float x2, float (&h)[32], bool stab) {
@@ -444,7 +535,8 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
         const int n = ccol + j;
         h[j] = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, sW1[3 * n] * x0));
       }
-      stab::stab_fwd(h, sBias + ccol, lane);
+      if (SST) stage_fwd(h, sBias);
+      else stab::stab_fwd(h, sBias + ccol, lane);
       return;
     }
 #pragma unroll
@@ -584,7 +676,8 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       tc::tmem_ld32(tmem + tlane + ccol, v);
       const float* bl = sBias + (l - 1) * W + ccol;
       if (STAB && stab) {
-        stab::stab_fwd(v, bl, lane);
+        if (SST) stage_fwd(v, sBias + (l - 1) * W);
+        else stab::stab_fwd(v, bl, lane);
       } else if (!SILU) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = act_tanh(v[j] + bl[j]);
@@ -707,13 +800,19 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
           hv[j] = sg * fmaf(z, 1.0f - sg, 1.0f);
         }
       } else if (STAB && stab) {   // G_NH = the backward map of (ub wo) through the last activation
-        float a[32];
+        if (SST) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          v[j] = a[j] = hv[j];
-          hv[j] = ub * sWo[ccol + j];
+          for (int j = 0; j < 32; ++j) v[j] = hv[j];
+          stage_bwd(hv, 0u);
+        } else {
+          float a[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = a[j] = hv[j];
+            hv[j] = ub * sWo[ccol + j];
+          }
+          stab::stab_bwd(hv, a, lane);
         }
-        stab::stab_bwd(hv, a, lane);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -764,8 +863,12 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
       float v[32], hq[32];
       tc::tmem_ld32(tmem + tlane + ccol, v);
       if (STAB && stab) {                  // the backward map of the difference form (G27)
-        load_chunk_bf16(hbuf, row, chunk, hq);
-        stab::stab_bwd(v, hq, lane);
+        if (SST) {
+          stage_bwd(v, hbuf);
+        } else {
+          load_chunk_bf16(hbuf, row, chunk, hq);
+          stab::stab_bwd(v, hq, lane);
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) hq[j] = 1.0f;
       } else if (!SILU) {                  // tanh' = 1 - h~^2 (bf16 operand copy)
@@ -872,7 +975,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P>::THREADS, TcLayout<W, 
 
 template <int W, int NH, int ACT, bool TRAIN, int P = 1, bool STAB = false>
 static cudaError_t launch_tc_t(const MlpParams& p, int grid, cudaStream_t s) {
-  using L = TcLayout<W, NH, ACT, P>;
+  using L = TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>()>;
   auto kern = k_mlp_tc<W, NH, ACT, TRAIN, P, STAB>;
   static bool attr = false;
   if (!attr) {
