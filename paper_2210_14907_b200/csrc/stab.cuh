@@ -109,11 +109,14 @@ __device__ __forceinline__ float tanh_minus_id_f32(float d) {
   const float d2 = d * d;
   const float s = fmaf(d2, fmaf(d2, fmaf(d2, fmaf(d2, -1382.0f / 155925.0f, 62.0f / 2835.0f), -17.0f / 315.0f),
                                 2.0f / 15.0f), -1.0f / 3.0f) * (d * d2);
-  return fabsf(d) < 0.25f ? s : tanhf(d) - d;
+  if (fabsf(d) >= 0.25f) return tanhf(d) - d;   // rare (a branch: tanhf is long)
+  return s;
 }
+// 1 + x lies in [0.75, 1.25] (|x| <= |tanh d| < 1/4 below the cut): the approximate division
+// (reciprocal within 1 ulp) keeps g within 2 ulp
 __device__ __forceinline__ float stab_g_f32(float t, float s2, float d) {
   const float s = tanh_minus_id_f32(d), x = t * (d + s);
-  return s2 * fmaf(-x, d, s) / (1.0f + x);
+  return __fdividef(s2 * fmaf(-x, d, s), 1.0f + x);
 }
 // in place: z (bias included), p_d, D_d -> t = tanh z, P_d, Q_d
 template <int W, int LDA, int NPTS, int NTHR>
