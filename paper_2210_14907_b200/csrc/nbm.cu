@@ -505,8 +505,11 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
   if (e == cudaSuccess && uses_rep(A)) {
     e = cudaMemsetAsync(w.rep, 0, (size_t)w.nrep * 2 * ((A.p_net + 3) & ~3ll) * sizeof(float), s);
   }
-  if (e == cudaSuccess) e = launch_assemble_crossed(h, pts_dev, n, H, s);
-  launches += 2;
+  // no interface (NBM_LS_NONE): no crossed rows, whose count slots and loss partial stay at
+  // the zeros written at create, so the crossed-row kernels are not launched
+  const bool crossing = P.ls_kind != NBM_LS_NONE;
+  if (crossing && e == cudaSuccess) e = launch_assemble_crossed(h, pts_dev, n, H, s);
+  if (crossing) launches += 2;
   // pass A: forward-only over the crossed rows (u per row)
   MlpParams pa;
   fill_common(h, pa, theta_dev, h_cell);
@@ -521,10 +524,9 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
     pa.aux_by_item[k] = 1;
   }
   pa.u_out = w.xrow_u;
-  if (e == cudaSuccess) e = launch_mlp_h(h, false, pa, s);
-  launches += 1;
-  if (e == cudaSuccess) e = launch_crossed_residual(h, n_global > 0 ? n_global : 1, weight, s);
-  launches += 1;
+  if (crossing && e == cudaSuccess) e = launch_mlp_h(h, false, pa, s);
+  if (crossing && e == cudaSuccess) e = launch_crossed_residual(h, n_global > 0 ? n_global : 1, weight, s);
+  if (crossing) launches += 2;
   // main fused pass over all segments (net- first, then net+)
   MlpParams pm;
   fill_common(h, pm, theta_dev, h_cell);
