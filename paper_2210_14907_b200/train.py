@@ -25,6 +25,16 @@ def convergence_order(e_coarse: float, e_fine: float) -> float:
     return math.log2(e_coarse / e_fine)
 
 
+def epoch_plan(N: int, batch: int):
+    """(steps per epoch, interior points per step, boundary points per step) of an epoch of N^3
+    interior and 6 (N+1)^2 boundary points in steps of at most `batch` interior points."""
+    if N < 4 or N & (N - 1):
+        raise ValueError("N must be a power of two >= 4 (S:324)")
+    n_int, n_bnd = N ** 3, 6 * (N + 1) ** 2
+    steps = max(1, math.ceil(n_int / batch))
+    return steps, math.ceil(n_int / steps), math.ceil(n_bnd / steps)
+
+
 def train(cfg: dict, N: int, epochs: int, batch: int = 16384, lr: float = 1e-3, seed: int = 0,
           levels: int = 1, eval_M: int | None = None, log_every: int = 0, device: int = 0,
           lr_schedule=None) -> dict:
@@ -33,15 +43,10 @@ def train(cfg: dict, N: int, epochs: int, batch: int = 16384, lr: float = 1e-3, 
     lr_schedule: optional [(fraction of the epochs, lr), ...] phases (one captured graph per
     phase; the Adam state and step counter run on), else a constant lr."""
     import torch
-    if N < 4 or N & (N - 1):
-        raise ValueError("N must be a power of two >= 4 (S:324)")
+    steps_per_epoch, n, nb = epoch_plan(N, batch)
     cfg = dict(cfg)
     cfg["H"] = inputs.h_lattice(2.0 / N)
     cfg["h"] = cfg["H"] / inputs.LATTICE
-    n_int, n_bnd = N ** 3, 6 * (N + 1) ** 2
-    steps_per_epoch = max(1, math.ceil(n_int / batch))
-    n = math.ceil(n_int / steps_per_epoch)
-    nb = math.ceil(n_bnd / steps_per_epoch)
     s = nbm.Solver(cfg, device, max_points=max(n, nb, 1 << 16))
     s.init_params(seed)
     dev = f"cuda:{device}"
