@@ -292,28 +292,52 @@ def main():
     # points from pinned memory, D2H of the loss) ----
     e2e = None
     if not args.no_e2e:
+        # double-buffered inputs: step k+1's host->device copy runs on a copy stream while step k
+        # computes; every step's copy and its loss read-back stay inside the timed region
         hp = torch.empty(N, 3, pin_memory=True)
         hb = torch.empty(Nb, 3, pin_memory=True)
         s.sample(nbm.POINTS_INTERIOR, 1, 0, rank * N, N, pts)
         s.sample(nbm.POINTS_BOUNDARY, 1, 0, rank * Nb, Nb, bpts)
         hp.copy_(pts)
         hb.copy_(bpts)
-        hl = torch.empty(1, pin_memory=True)
+        hl = torch.empty(args.steps, pin_memory=True)
+        dpts = [pts, torch.empty_like(pts)]
+        dbps = [bpts, torch.empty_like(bpts)]
+        cstream = torch.cuda.Stream()
+        copied = [torch.cuda.Event() for _ in range(2)]
+        used = [torch.cuda.Event() for _ in range(2)]
         ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(args.steps)]
+
+        def issue_copy(k):   # inside the timed interval of step k - 1 (of step 0 for k = 0)
+            b = k & 1
+            cstream.wait_stream(stream)
+            with torch.cuda.stream(cstream):
+                if k >= 2:
+                    cstream.wait_event(used[b])      # step k - 2 has consumed this buffer
+                dpts[b].copy_(hp, non_blocking=True)
+                dbps[b].copy_(hb, non_blocking=True)
+                copied[b].record(cstream)
+
         barrier()
         for k in range(args.steps):
             flush.zero_()
             ee[k][0].record(stream)
-            pts.copy_(hp, non_blocking=True)
-            bpts.copy_(hb, non_blocking=True)
-            s.loss_grad(pts, bpts, n_global=Ng, nb_global=Nbg, levels=args.levels)
+            if k == 0:
+                issue_copy(0)
+            b = k & 1
+            stream.wait_event(copied[b])
+            if k + 1 < args.steps:
+                issue_copy(k + 1)
+            s.loss_grad(dpts[b], dbps[b], n_global=Ng, nb_global=Nbg, levels=args.levels)
+            used[b].record(stream)
             dp.allreduce_sum_(s.gbuf)
             s.adam_step(lr=cfg["lr"])
-            hl.copy_(s.loss, non_blocking=True)
+            hl[k:k + 1].copy_(s.loss, non_blocking=True)
             ee[k][1].record(stream)
+        torch.cuda.synchronize()
         barrier()
-        e_ms = sum(a.elapsed_time(b) for a, b in ee)
+        e_ms = sum(x.elapsed_time(y) for x, y in ee)
         if world > 1:
             t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
             tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
