@@ -4,11 +4,13 @@ loss+grad evaluations/s and steps/s at 1/2/4/8 B200, % roofline).
 
 One step = sample (interior + boundary, K1) -> nbm_loss_grad (K2 classify/assemble,
 K3 fused MLP fwd/residual/bwd, K4r reduce) -> all-reduce of [grad, loss] (N > 1) ->
-nbm_adam_step (K4a).  Default workload: BASELINE config 2 (configs[1]): sphere interface,
-two 3-64-64-64-1 tanh fp32 MLPs, 2^18 interior + 2^15 boundary points per GPU (weak
-scaling), h = 1/128.  Synthetic seeded data (the paper's dragon scan is not available).
+nbm_adam_step (K4a).  Default workload: BASELINE config 4 (configs[3], the north_star's
+2^22 points/step): union of 32 spheres, two 3-256^4-1 tanh bf16 MLPs, 2^22 interior + 2^19
+boundary points per GPU (weak scaling), h = 2/1023.  A `secondary` record times config 5 at
+width 256 in fp32 (the paper's own arithmetic) on the same points.  Synthetic seeded data (the
+paper's dragon scan is not available).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl reference]
 Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ... (NCCL all-reduce).
 """
 from __future__ import annotations
@@ -106,30 +108,47 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(cfg, seconds_hint=15.0, levels=1):
-    """The oracle as it stands (fp64, OpenMP over all host cores) on a bounded sample of
-    the same workload; returns pts/s (loss+grad evaluations per second)."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(cfg, levels=1):
+    """The oracle as it stands (fp64 C, OpenMP with a fixed-order reduction) on a seeded
+    subsample of the same workload: 2^12 interior + 2^9 boundary points on all
+    host cores, 2^10 + 2^7 on one core.  Loss+grad cost is exactly linear in the point count,
+    so pts/s carries over to the full N; the full-step time is extrapolated and marked so."""
     import oracle
     pb, ar = oracle.from_config(cfg)
     th = oracle.init_params(ar, 0)
-    n = 1 << 10
-    nb = max(1, n * cfg["Nb"] // cfg["N"])
-    while True:
+
+    def run(n, threads):
+        nb = max(1, n * cfg["Nb"] // cfg["N"])
         pts = oracle.sample(0, 0, 0, 0, n, cfg["H"])
         bpts = oracle.sample(1, 0, 0, 0, nb, cfg["H"])
         t0 = time.perf_counter()
         if levels == 1:
-            oracle.loss_grad(pb, ar, th, pts, bpts, cfg["h"], n_glob=cfg["N"], nb_glob=cfg["Nb"])
+            oracle.loss_grad(pb, ar, th, pts, bpts, cfg["h"], n_glob=cfg["N"], nb_glob=cfg["Nb"], nthreads=threads)
         else:
             oracle.loss_grad_ml(pb, ar, th, pts, bpts, cfg["h"], levels, n_glob=cfg["N"], nb_glob=cfg["Nb"])
-        dt = time.perf_counter() - t0
-        if dt > seconds_hint / 4 or n >= cfg["N"]:
-            break
-        n = min(cfg["N"], n * max(2, int(seconds_hint / 4 / max(dt, 1e-3))))
-        nb = max(1, n * cfg["Nb"] // cfg["N"])
-    return {"value": n / dt, "unit": "pts/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{n} interior + {nb} boundary points of {cfg['label']} (fp64 loss+grad, "
-                      f"{dt:.2f} s)"}
+        return n, nb, time.perf_counter() - t0
+
+    cores = oracle.num_threads()
+    n, nb, dt = run(min(cfg["N"], 1 << 12), cores)
+    n1, nb1, dt1 = run(min(cfg["N"], 1 << 10), 1)
+    return {"value": n / dt, "unit": "pts/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} interior + {nb} boundary points of {cfg['label']} (seeded subsample, fp64 loss+grad, "
+                      f"{dt:.2f} s on {cores} threads); pts/s carries over linearly to N = {cfg['N']}",
+            "extrapolated_step_s": dt * cfg["N"] / n, "extrapolated": True,
+            "one_core": {"value": n1 / dt1, "unit": "pts/s", "cores": 1,
+                         "sample": f"{n1} interior + {nb1} boundary points ({dt1:.2f} s)",
+                         "extrapolated_step_s": dt1 * cfg["N"] / n1},
+            "nproc": os.cpu_count(), "cpu_model": cpu_model()}
 
 
 def run_reference(args, cfg, rank, world):
@@ -172,12 +191,62 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_secondary(args):
+    """config 5 at width 256 in IEEE fp32 (K3fw; the paper's own arithmetic) on
+    2^22 + 2^19 points: graph-replayed steps timed with CUDA events, L2 flushed between steps,
+    the fused kernel timed by the library's event hook (roofline: the fp32 FFMA peak)."""
+    import torch
+    from paper_2210_14907_b200 import nbm
+    cfg = inputs.config("c5", width=256, prec=inputs.PREC_FP32)
+    N, Nb = cfg["N"], cfg["Nb"]
+    s = nbm.Solver(cfg, device=torch.cuda.current_device(), max_points=max(N, Nb))
+    s.init_params(0)
+    pts = torch.empty(N, 3, device="cuda")
+    bpts = torch.empty(Nb, 3, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    steps, warm = 3, 3
+
+    def step(it):
+        s.sample(nbm.POINTS_INTERIOR, 0, it, 0, N, pts)
+        s.sample(nbm.POINTS_BOUNDARY, 0, it, 0, Nb, bpts)
+        s.loss_grad(pts, bpts)
+        s.adam_step(lr=cfg["lr"])
+    for it in range(warm):
+        step(it)
+    nbm.nbm_timing_enable(s.h, True)
+    nbm.nbm_timing_read(s.h)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for k in range(steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        step(warm + k)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    mlp_ms, _, calls = nbm.nbm_timing_read(s.h)
+    tot = sum(a.elapsed_time(b) for a, b in ev)
+    st = s.status()
+    s.close()
+    _, fb = mlp_macs(cfg["sizes"])
+    flop = 2.0 * fb * (7 * N + Nb)
+    achieved = flop / (mlp_ms / max(calls, 1) / 1e3) / 1e12
+    return {"workload": "c5-w256-fp32", "metric": METRIC, "value": N * steps / (tot / 1e3), "unit": "pts/s",
+            "steps": steps, "warmup": warm, "ms_per_step": tot / steps, "dtype": "f32", "status": st,
+            "launch_mode": "eager", "points_per_gpu": N, "boundary_per_gpu": Nb, "mlp": "3x256x256x256x256x1",
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": FP32_FFMA_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP32_FFMA_TFLOPS, "kernel": "k_mlp_fp32w fused fwd/residual/bwd",
+                         "avg_launch_ms": mlp_ms / max(calls, 1),
+                         "peak_src": "fp32 FFMA: 148 SM x 128 lanes x 2 FLOP x 1965 MHz (derived, DESIGN.md)"}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the fp32 c5-w256 secondary record")
     ap.add_argument("--width", type=int, default=None)
     ap.add_argument("--prec", default=None, choices=["fp32", "bf16", "fp32x"], help="override the config's precision (c4/c5)")
     ap.add_argument("--impl", default="nbm", choices=["nbm", "reference"])
@@ -218,6 +287,7 @@ def main():
     from paper_2210_14907_b200 import nbm
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # NCCL logs its rank count / NVLS use to stderr
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     N, Nb = cfg["N"], cfg["Nb"]                 # per GPU (weak scaling)
     Ng, Nbg = N * world, Nb * world
@@ -288,6 +358,21 @@ def main():
     else:
         lg_ms_max = lg_ms
 
+    # ---- all-reduce time per step: the [grad, loss] collective alone,
+    # CUDA events on the launching stream, max over ranks ----
+    allreduce_us = None
+    if world > 1:
+        ar_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        for k in range(args.steps):
+            ar_ev[k][0].record(stream)
+            dp.allreduce_sum_(s.gbuf)
+            ar_ev[k][1].record(stream)
+        barrier()
+        t = torch.tensor([sum(a.elapsed_time(b) for a, b in ar_ev) / args.steps], device="cuda", dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        allreduce_us = t.item() * 1e3
+
     # ---- e2e: same step through the public API with host buffers (H2D of the step's
     # points from pinned memory, D2H of the loss) ----
     e2e = None
@@ -332,8 +417,10 @@ def main():
             s.loss_grad(dpts[b], dbps[b], n_global=Ng, nb_global=Nbg, levels=args.levels)
             used[b].record(stream)
             dp.allreduce_sum_(s.gbuf)
-            s.adam_step(lr=cfg["lr"])
+            s.adam_step_at(lr=cfg["lr"])       # the device step counter, as in the timed graph
             hl[k:k + 1].copy_(s.loss, non_blocking=True)
+            if k + 1 < args.steps:
+                stream.wait_event(copied[(k + 1) & 1])   # step k+1's upload is counted in step k
             ee[k][1].record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -410,6 +497,9 @@ def main():
                    "global_points": Ng, "mlp": "x".join(map(str, cfg["sizes"])), "n_nets": cfg["n_nets"],
                    "h": cfg["h"], "levels": args.levels, "stencil": args.stencil, "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     **({"peak_sustained": peaks["bf16_tflops_sustained"],
+                         "frac_sustained": achieved / peaks["bf16_tflops_sustained"]}
+                        if cfg["prec"] == inputs.PREC_BF16 else {}),
                      **({"measured_ffma_3reg_peak": FP32_FFMA_3REG_MEASURED_TFLOPS,
                          "frac_of_measured_ffma": achieved / FP32_FFMA_3REG_MEASURED_TFLOPS}
                         if cfg["prec"] in (inputs.PREC_FP32, inputs.PREC_FP32X) else {}),
@@ -423,11 +513,18 @@ def main():
         "launch_mode": mode, "ms_per_step_eager": eager_ms / args.steps,
         "clocks": clocks,
         "e2e": e2e,
+        "allreduce_us_per_step": allreduce_us,
+        **({"nccl": {"ranks": world, "backend": tdist.get_backend()}} if world > 1 else {}),
     }
     if infer is not None:
         line["inference"] = infer
     if not args.no_cpu_baseline and world == 1:   # the oracle baseline: rank 0 at N = 1 only
         line["cpu_baseline"] = cpu_baseline(cfg, levels=args.levels)
+    if cfg["name"] == "c4" and not args.no_secondary and world == 1 and args.points is None:
+        s.close()
+        del flush
+        torch.cuda.empty_cache()
+        line["secondary"] = run_secondary(args)
     print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()

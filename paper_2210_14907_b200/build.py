@@ -24,6 +24,7 @@ SOURCES = {
     "mlp_fp32.cu": [],
     "mlp_tc.cu": [],
     "mlp_w256.cu": [],
+    "mlp_w256v2.cu": [],
     "mlp_fp32w.cu": [],
     "nbm.cu": [],
 }

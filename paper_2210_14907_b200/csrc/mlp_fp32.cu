@@ -614,12 +614,8 @@ template <int W, int NH, int ACT, bool TRAIN, bool STAB = false>
 static cudaError_t launch_t(const MlpParams& p, int grid, cudaStream_t s) {
   using L = Layout<W, NH, ACT == NBM_ACT_SINE>;
   auto kern = k_mlp_fp32<W, NH, ACT, TRAIN, STAB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, (const void*)kern, (int)L::bytes); e != cudaSuccess) return e;
   kern<<<grid * kCtasPerSm, kThreads, L::bytes, s>>>(p);
   return cudaGetLastError();
 }

@@ -497,12 +497,8 @@ template <int W, int NH, bool TRAIN, bool STAB = false>
 static cudaError_t launch_fw_t(const MlpParams& p, const float* wimg, float* rep, int nrep, int grid, cudaStream_t s) {
   using L = FW<W, NH>;
   auto kern = k_mlp_fp32w<W, NH, TRAIN, STAB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, (const void*)kern, (int)L::bytes); e != cudaSuccess) return e;
   kern<<<grid, kThr, L::bytes, s>>>(p, wimg, rep, nrep);
   return cudaGetLastError();
 }

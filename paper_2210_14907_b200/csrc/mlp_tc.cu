@@ -977,12 +977,8 @@ template <int W, int NH, int ACT, bool TRAIN, int P = 1, bool STAB = false>
 static cudaError_t launch_tc_t(const MlpParams& p, int grid, cudaStream_t s) {
   using L = TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>()>;
   auto kern = k_mlp_tc<W, NH, ACT, TRAIN, P, STAB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::bytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, (const void*)kern, (int)L::bytes); e != cudaSuccess) return e;
   kern<<<grid * L::MINB, L::THREADS, L::bytes, s>>>(p);
   return cudaGetLastError();
 }

@@ -56,8 +56,10 @@ struct Lay {
   static constexpr uint32_t oUb = oU + 4 * kB;
   static constexpr uint32_t oAux = oUb + 4 * kB;
   static constexpr uint32_t oItem = oAux + 4 * kB;
-  static constexpr uint32_t oBar = oItem + 4 * kB;        // full[4], empty[4], mma, dw, ld, park + tmem base
+  static constexpr uint32_t oSG = oItem + 4 * kB;         // fp32 [NH + 4][W] small gradients + b_o
+  static constexpr uint32_t oBar = oSG + 4 * ((NH + 4) * W + 4);   // full[4], empty[4], mma, dw, ld, park + tmem base
   static constexpr uint32_t bytes = oBar + 128;
+  static_assert(bytes <= 227 * 1024, "shared memory");
   static constexpr int kScr = NH + 1;                     // parked tiles per CTA: h_1..h_{NH-1}, G x2
   static constexpr int64_t tW1 = 0, tB1 = 3 * W;
   __host__ __device__ static constexpr int64_t tWl(int l) { return 4 * W + (int64_t)(l - 2) * (W * W + W); }
@@ -247,6 +249,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   tc::cluster_sync();
   tc::tc_fence_after();
   const uint32_t tmem = *sTmem;   // [0,256): GEMM accumulator, [256,512): dW
+  for (int i = tid; i < (NH + 4) * W + 4; i += kThreads) reinterpret_cast<float*>(smem + L::oSG)[i] = 0.0f;
   int firstPair[kNumSeg + 1];
   int total = 0;
 #pragma unroll
@@ -323,10 +326,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   constexpr uint32_t ID_FWD = tc::idesc_bf16(2 * kB, W, 0, 0);
   constexpr uint32_t ID_DH = tc::idesc_bf16(2 * kB, W, 0, 1);
   constexpr uint32_t ID_DW = tc::idesc_bf16(2 * kB, W, 1, 1);
-  // small gradients per lane (column 64 cg + 32 k + lane): b_1..b_NH, W1[:,0..2], wo
+  // small gradients (b_1..b_NH, W1[:,0..2], wo, b_o), accumulated in shared memory per column
+  // (no per-thread arrays: dynamically indexed register arrays became local memory)
   constexpr int NV = NH + 4;
-  float g[NV][2];
-  float gbo = 0.0f;
+  float* sSG = reinterpret_cast<float*>(smem + L::oSG);
+  auto sg_add = [&](int v, int c, float x) { atomicAdd(&sSG[v * W + c * 32 + lane], x); };
   double lossAcc = 0.0;
   float* rep = P.rep + (int64_t)(q % P.nrep) * 2 * prm.p_stride;
   bool pend = false;   // TMEM [256,512) holds an unflushed dW
@@ -349,15 +353,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     if (k1 == 2) pend = false;
   };
   auto flush_dw = [&]() { flush_dw_part(0, 2); };
-  auto flush_small = [&](int net) {
+  auto flush_small = [&](int net) {   // all threads, between barriers; leaves sSG zeroed
     float* out = rep + (int64_t)net * prm.p_stride;
-    for (int k = 0; k < 2; ++k) {
-      const int col = 64 * cg + 32 * k + lane;
-      for (int v = 0; v < NH; ++v) atomicAdd(out + (v == 0 ? L::tB1 : L::tBl(v + 1)) + col, g[v][k]);
-      for (int c = 0; c < 3; ++c) atomicAdd(out + L::tW1 + 3 * col + c, g[NH + c][k]);
-      atomicAdd(out + L::tWo + col, g[NH + 3][k]);
+    for (int i = tid; i < W; i += kThreads) {
+      for (int v = 0; v < NH; ++v) {
+        atomicAdd(out + (v == 0 ? L::tB1 : L::tBl(v + 1)) + i, sSG[v * W + i]);
+        sSG[v * W + i] = 0.0f;
+      }
+      for (int c = 0; c < 3; ++c) {
+        atomicAdd(out + L::tW1 + 3 * i + c, sSG[(NH + c) * W + i]);
+        sSG[(NH + c) * W + i] = 0.0f;
+      }
+      atomicAdd(out + L::tWo + i, sSG[(NH + 3) * W + i]);
+      sSG[(NH + 3) * W + i] = 0.0f;
     }
-    if (cg == 0 && lane == 0) atomicAdd(out + L::tBo, gbo);
+    if (tid == 0) {
+      atomicAdd(out + L::tBo, sSG[NV * W]);
+      sSG[NV * W] = 0.0f;
+    }
   };
   auto load_net = [&](int net) {
     const float* thp = prm.theta + (int64_t)net * prm.p_net;
@@ -368,8 +381,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       sWo[i] = thp[L::tWo + i];
     }
     if (tid == 0) sWo[W] = thp[L::tBo];
-    for (int v = 0; v < NV; ++v) g[v][0] = g[v][1] = 0.0f;
-    gbo = 0.0f;
   };
   auto layer1 = [&](int c, float x0, float x1, float x2, float (&h)[32]) {
 #pragma unroll
@@ -613,7 +624,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       float b = centre ? ub : 0.0f;
 #pragma unroll
       for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
-      gbo += b;
+      if (lane == 0) atomicAdd(&sSG[NV * W], b);
     }
     const uint32_t gb = aBuf[(NH - 1) & 1];   // G_l (own rows, all outputs), then the dW operand G-halves
     const uint32_t hb = aBuf[NH & 1];         // the dW operand h-halves
@@ -627,7 +638,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = ub * hv[j];
         float sm = tsum16(v, lane);
-        if ((lane >> 4) == hf) g[NH + 3][k] += sm;
+        if ((lane >> 4) == hf) sg_add(NH + 3, c, sm);
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = ub * sWo[col + j];
         stab::stab_bwd<16>(v, hv, lane);
@@ -637,7 +648,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
           for (int j = 0; j < 16; ++j) v[j] = 0.0f;
         }
         sm = tsum16(v, lane);
-        if ((lane >> 4) == hf) g[NH - 1][k] += sm;
+        if ((lane >> 4) == hf) sg_add(NH - 1, c, sm);
       }
     }
     if (!(STAB && stab)) for (int k = 0; k < 2; ++k) {
@@ -646,11 +657,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), hv);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = ub * hv[j];
-      g[NH + 3][k] += tsum(v, lane);
+      sg_add(NH + 3, c, tsum(v, lane));
 #pragma unroll
       for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
       put_chunk(gb, nullptr, row, c, hv);
-      g[NH - 1][k] += tsum(hv, lane);
+      sg_add(NH - 1, c, tsum(hv, lane));
     }
     tc::fence_proxy_async_smem();
     tc::tc_fence_before();
@@ -695,10 +706,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       }
       TRW(28 + 3 * (NH - l));
       TRW(11 + 4 * (NH - l));
-      uint32_t gk[2][16];   // G_{l-1}, bf16, for the next dH GEMM's A tile
+      // G_{l-1} (bf16, the next dH GEMM's A tile) waits for the dW MMA in TMEM: packed in place in
+      // this warp's accumulator columns [64 cg, 64 cg + 32) (chunk k at + 16 k, after the chunk and
+      // the one before it have been read), not in a register tile held across the wait
+      const uint32_t stash = tmem + tlane + (uint32_t)(64 * cg);
       const uint8_t* hprev = myScr + hslot(l - 1);
       if (STAB && stab) for (int k = 0; k < 2; ++k) {   // stable form: 16-column halves
         const int c = 2 * cg + k;
+        uint32_t pkd[16];
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           float v[16], hq[16];
@@ -708,13 +723,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
           const bool mine = (lane >> 4) == hf;   // lane l accumulates column 32 k + l
           if (l - 1 >= 2) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) gk[k][8 * hf + j] = pk(v[2 * j], v[2 * j + 1]);
+            for (int j = 0; j < 8; ++j) pkd[8 * hf + j] = pk(v[2 * j], v[2 * j + 1]);
             if (!centre) {   // b_{l-1}: centre rows only (v is consumed)
 #pragma unroll
               for (int j = 0; j < 16; ++j) v[j] = 0.0f;
             }
             const float sm = tsum16(v, lane);
-            if (mine) g[l - 2][k] += sm;
+            if (mine) sg_add(l - 2, c, sm);
           } else {           // layer 1: dW1 += G1 x^T (x = the row input), db1 += G1 (centre rows)
             const float xs[3] = {x0, x1, x2};
 #pragma unroll
@@ -723,16 +738,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
 #pragma unroll
               for (int j = 0; j < 16; ++j) tv[j] = v[j] * xs[d];
               const float sm = tsum16(tv, lane);
-              if (mine) g[NH + d][k] += sm;
+              if (mine) sg_add(NH + d, c, sm);
             }
             if (!centre) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) v[j] = 0.0f;
             }
             const float sm = tsum16(v, lane);
-            if (mine) g[0][k] += sm;
+            if (mine) sg_add(0, c, sm);
           }
         }
+        if (l - 1 >= 2) tc::tmem_st16u(stash + 16u * k, pkd);
       }
       if (!(STAB && stab)) for (int k = 0; k < 2; ++k) {
         const int c = 2 * cg + k;
@@ -742,21 +758,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] *= 1.0f - hq[j] * hq[j];
         if (l - 1 >= 2) {
+          uint32_t pkd[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) gk[k][j] = pk(v[2 * j], v[2 * j + 1]);
-          g[l - 2][k] += tsum(v, lane);
+          for (int j = 0; j < 16; ++j) pkd[j] = pk(v[2 * j], v[2 * j + 1]);
+          tc::tmem_st16u(stash + 16u * k, pkd);
+          sg_add(l - 2, c, tsum(v, lane));
         } else {   // layer 1: dW1 += G1 x^T, db1 += G1
           float tv[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) tv[j] = v[j] * x0;
-          g[NH][k] += tsum(tv, lane);
+          sg_add(NH, c, tsum(tv, lane));
 #pragma unroll
           for (int j = 0; j < 32; ++j) tv[j] = v[j] * x1;
-          g[NH + 1][k] += tsum(tv, lane);
+          sg_add(NH + 1, c, tsum(tv, lane));
 #pragma unroll
           for (int j = 0; j < 32; ++j) tv[j] = v[j] * x2;
-          g[NH + 2][k] += tsum(tv, lane);
-          g[0][k] += tsum(v, lane);
+          sg_add(NH + 2, c, tsum(tv, lane));
+          sg_add(0, c, tsum(v, lane));
         }
       }
       tc::tc_fence_before();
@@ -787,13 +805,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       pendL = l;
       TRW(13 + 4 * (NH - l));
       if (l > 2) {   // G_{l-1} (own rows, all outputs) -> gb for the next dH GEMM
+        tc::tc_fence_after();
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           const int c = 2 * cg + k;
+          uint32_t pkd[16];
+          tc::tmem_ld16u(stash + 16u * k, pkd);
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq)
-            sts4(gb + (uint32_t)((c * 4 + qq) * LBO_ACT + row * 16), gk[k][4 * qq], gk[k][4 * qq + 1],
-                 gk[k][4 * qq + 2], gk[k][4 * qq + 3]);
+            sts4(gb + (uint32_t)((c * 4 + qq) * LBO_ACT + row * 16), pkd[4 * qq], pkd[4 * qq + 1], pkd[4 * qq + 2],
+                 pkd[4 * qq + 3]);
         }
         tc::fence_proxy_async_smem();
         tc::tc_fence_before();
@@ -866,12 +887,8 @@ extern "C" int nbm_debug_w256_ld(long long* out) {
 template <int NH, bool TRAIN, bool STAB = false>
 static cudaError_t launch_w256_t(const W256Params& p, int grid, cudaStream_t s) {
   auto kern = k_mlp_w256<NH, TRAIN, STAB>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Lay<NH>::bytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, (const void*)kern, (int)Lay<NH>::bytes); e != cudaSuccess) return e;
   kern<<<grid, kThreads, Lay<NH>::bytes, s>>>(p);
   return cudaGetLastError();
 }

@@ -1,0 +1,882 @@
+// mlp_w256v2.cu -- K3w v2: the fused bf16 W = 256 MLP loss+grad kernel (config 4, c5-w256;
+// SURVEY 8(a) rows S3-S5), warp-specialised.  Same arithmetic, operand layouts, weight images and
+// gradient replicas as K3w v1 (mlp_w256.cu), a different schedule:
+//
+//   warps 0-7   E  epilogues: layer 1, bias + tanh, residual, G = ub wo (1 - h^2), act', the small
+//                  gradients (b_l, W_1, w_o, b_o); warp w owns TMEM lane quadrant w % 4 (tile rows)
+//                  and columns [128 (w / 4), + 128) of every 256-wide activation
+//   warps 8-11  F  the dW flush: TMEM dW rows -> red.global.add.v4 into the L2 gradient replicas,
+//                  overlapping everything that follows the dW MMA
+//   warp 12     P  TMA producer: the weight ring, coordinate / item prefetch one tile ahead, the
+//                  parks (bulk stores of h_l and of the peer's half of G_l) and the dW operand loads
+//   warp 13     M  tcgen05 issue (leader CTA of the pair; the peer forwards its operand arrivals)
+//
+// CTA pairs (cluster 2, cta_group::2): each CTA holds 128 rows of a 256-row pair tile.  TMEM:
+// columns [0,256) the GEMM accumulator, [256,512) dW_l (this CTA's 128 outputs x 256 inputs).
+// Per tile the MMA sequence is fwd_2..fwd_NH, then dH_l, dW_l for l = NH..2: dW_l runs while E
+// forms G_{l-1} = (dH_l) (1 - h_{l-1}^2), which E packs to bf16 in place in the accumulator's
+// TMEM columns and copies into shared memory once dW_l has released the operand buffers -- no
+// register tile is held across the dW MMA (v1's local-memory traffic), and the MMA warp never
+// waits behind epilogue code.  Rounding points: DESIGN.md G16.  tanh, direct stencil form only
+// (the stable form runs on v1).  W = 256 is deterministic within tolerance only (G21).
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "nbm_internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace nbm {
+
+namespace {
+
+constexpr int W = 256;
+constexpr int kB = 128;                  // tile rows per CTA (256 per pair)
+constexpr int kPT = 18;                  // stencil points per tile (7 x 18 = 126 rows)
+constexpr int kEW = 8, kFW = 4;          // epilogue / flush warps
+constexpr int kWP = kEW + kFW;           // producer warp
+constexpr int kWM = kWP + 1;             // MMA warp
+constexpr int kThreads = (kWM + 1) * 32; // 448
+constexpr int kStages = 4;
+constexpr uint32_t ACT = kB * W * 2;     // 64 KB bf16 activation tile
+constexpr uint32_t QTR = ACT / 2;        // 32 KB: one 128-column half
+constexpr uint32_t HSLICE = 64 * 128 * 2;
+constexpr uint32_t LBO_ACT = kB * 16;
+
+// barrier slots
+enum : int {
+  B_WFULL = 0, B_WEMPTY = 4, B_AREADY = 8, B_ACCFULL, B_DWFULL, B_DWEMPTY,
+  B_WDONE_X, B_WDONE_Y, B_PARKED_X, B_PARKED_Y, B_HPARK, B_PKREADY, B_CRDFULL, B_CRDEMPTY = B_CRDFULL + 2,
+  B_NUM = B_CRDEMPTY + 2
+};
+
+template <int NH>
+struct Lay2 {
+  static constexpr int NV = NH + 4;                        // b_1..b_NH, W_1[:,0..2], w_o
+  static constexpr uint32_t oX = 0, oY = ACT, oW = 2 * ACT;
+  static constexpr uint32_t oW1 = oW + kStages * HSLICE;   // fp32 [W][3]
+  static constexpr uint32_t oBias = oW1 + 4 * 3 * W;       // fp32 [NH][W]
+  static constexpr uint32_t oWo = oBias + 4 * NH * W;      // fp32 [W] + b_o
+  static constexpr uint32_t oSG = oWo + 4 * (W + 4);       // fp32 [NV][W] small gradients + b_o
+  static constexpr uint32_t oCrd = oSG + 4 * (NV * W + 4); // fp32 [2][kB][4]
+  static constexpr uint32_t oItem = oCrd + 2 * 16 * kB;    // int [2][kB]
+  static constexpr uint32_t oAux = oItem + 2 * 4 * kB;     // fp32 [2][kB]
+  static constexpr uint32_t oUp = oAux + 2 * 4 * kB;       // fp32 [2][kB] u partial per column half
+  static constexpr uint32_t oUb = oUp + 2 * 4 * kB;        // fp32 [kB] cotangent per row
+  static constexpr uint32_t oSeg = oUb + 4 * kB;           // int [4][8] segment table
+  static constexpr uint32_t oBar = oSeg + 4 * 32;          // barriers
+  static constexpr uint32_t bytes = oBar + 8 * B_NUM + 16;
+  static_assert(bytes <= 227 * 1024, "shared memory");
+  static constexpr int kScr = 2 * (NH - 1);               // park slots per CTA (64 KB): h_1..h_{NH-1}, G_2..G_NH
+  static constexpr int64_t tW1 = 0, tB1 = 3 * W;
+  __host__ __device__ static constexpr int64_t tWl(int l) { return 4 * W + (int64_t)(l - 2) * (W * W + W); }
+  __host__ __device__ static constexpr int64_t tBl(int l) { return tWl(l) + W * W; }
+  static constexpr int64_t tWo = 4 * W + (int64_t)(NH - 1) * (W * W + W);
+  static constexpr int64_t tBo = tWo + W;
+};
+
+// ---- small PTX helpers (scoped barrier semantics for the cross-CTA handshakes) ----
+__device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(tc::smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+// arrive on the same barrier in CTA `cta` of the cluster (cluster-scope release)
+__device__ __forceinline__ void mb_arrive_cta(uint64_t* bar, uint32_t cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(tc::smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void ebar() { asm volatile("bar.sync 1, %0;" ::"n"(kEW * 32) : "memory"); }
+__device__ __forceinline__ void fbar() { asm volatile("bar.sync 2, %0;" ::"n"(kFW * 32) : "memory"); }
+
+__device__ __forceinline__ uint32_t pk(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+__device__ __forceinline__ float lo_bf(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float hi_bf(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ float th(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void sts4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+__device__ __forceinline__ uint4 lds4(uint32_t a) {
+  uint4 r;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  return r;
+}
+__device__ __forceinline__ uint4 ldcg4(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16u(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// 32 columns (chunk c) of row r, fp32 -> bf16 core layout in shared memory
+__device__ __forceinline__ void put_chunk(uint32_t buf, int r, int c, const float (&h)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    sts4(buf + (uint32_t)((c * 4 + q) * LBO_ACT + r * 16), pk(h[8 * q], h[8 * q + 1]), pk(h[8 * q + 2], h[8 * q + 3]),
+         pk(h[8 * q + 4], h[8 * q + 5]), pk(h[8 * q + 6], h[8 * q + 7]));
+}
+// warp transpose-sum: lane l receives the sum over the warp's 32 rows of column l
+__device__ __forceinline__ float tsum(float (&v)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const float send = up ? v[i] : v[i + s];
+      const float keep = up ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
+
+}  // namespace
+
+#ifdef NBM_TC_TRACE
+// clock64 timeline of CTA 0's first 8 tiles: [role M, E, P, F][tile][event] (scripts/r2/trace_v2.py)
+__device__ long long g_v2_trace[4][8][48];
+#define TRV(role, ev)                                                                                   \
+  do {                                                                                                \
+    if (blockIdx.x == 0 && u - u0 < 8) g_v2_trace[role][u - u0][ev] = clock64();                      \
+  } while (0)
+extern "C" int nbm_debug_v2_trace(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_v2_trace, sizeof(g_v2_trace));
+}
+#else
+#define TRV(role, ev) \
+  do {                \
+  } while (0)
+#endif
+
+struct W256v2Params {
+  MlpParams m;
+  const uint16_t* wfwd;   // [2][NH-1][4 slices][2 halves][128 o][64 i] K-major core layout (k_pack_w256)
+  const uint16_t* wbwd;   // [2][NH-1][4 slices][2 halves][64 o][128 i] MN-major core layout
+  uint8_t* hscr;          // [grid][NH+1][64 KB] parks
+  float* rep;             // [R][2][p_stride] gradient replicas (hidden blocks input-quad-major)
+  int nrep;
+};
+
+template <int NH, bool TRAIN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w256v2(const W256v2Params P) {
+  static_assert(NH >= 2 && NH <= 4, "hidden layers");
+  using L = Lay2<NH>;
+  const MlpParams& prm = P.m;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sb = tc::smem_u32(smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::oBar);
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(smem + L::oBar + 8 * B_NUM);
+  int* segCnt = reinterpret_cast<int*>(smem + L::oSeg);
+  int* segStart = segCnt + 8;
+  int* firstPair = segCnt + 16;   // [kNumSeg + 1]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = tc::cluster_rank();
+  const bool leader = rank == 0;
+  if (tid == 0) {
+    int tot = 0;
+    for (int s = 0; s < kNumSeg; ++s) {
+      const int c = prm.counts[prm.cnt_slot[s]];
+      const int per = prm.seg.kind[s] == kSegStencil ? kPT : kB;
+      segCnt[s] = c;
+      segStart[s] = prm.start_slot[s] >= 0 ? prm.counts[prm.start_slot[s]] : 0;
+      firstPair[s] = tot;
+      tot += ((c + per - 1) / per + 1) / 2;
+    }
+    firstPair[kNumSeg] = tot;
+    for (int s = 0; s < kStages; ++s) {
+      tc::mbar_init(bar + B_WFULL + s, leader ? 2 : 1);
+      tc::mbar_init(bar + B_WEMPTY + s, 1);
+    }
+    tc::mbar_init(bar + B_AREADY, 2);
+    tc::mbar_init(bar + B_ACCFULL, 1);
+    tc::mbar_init(bar + B_DWFULL, 1);
+    tc::mbar_init(bar + B_DWEMPTY, 2);
+    tc::mbar_init(bar + B_WDONE_X, 1);
+    tc::mbar_init(bar + B_WDONE_Y, 1);
+    tc::mbar_init(bar + B_PARKED_X, 1);
+    tc::mbar_init(bar + B_PARKED_Y, 1);
+    tc::mbar_init(bar + B_HPARK, 1);
+    tc::mbar_init(bar + B_PKREADY, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(bar + B_CRDFULL + b, 1);
+      tc::mbar_init(bar + B_CRDEMPTY + b, 1);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == kWM) tc::tmem_alloc2(sTmem, 512);
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem = *sTmem;
+  const int total = firstPair[kNumSeg];
+  const int NC = gridDim.x >> 1, q = blockIdx.x >> 1;
+  const int u0 = (int)((int64_t)total * q / NC), u1 = (int)((int64_t)total * (q + 1) / NC);
+  const uint32_t bufX = sb + L::oX, bufY = sb + L::oY;
+  // h_l and G_l live in X (l odd) or Y (l even): G_l overwrites a buffer whose last reader (the
+  // A operand of dW_{l+2} or the act' reads of h_l) is done before E forms it
+  auto bufOf = [&](int l) { return (l & 1) ? bufX : bufY; };
+  auto seg_of = [&](int u) {
+    int s = 0;
+    while (u >= firstPair[s + 1]) ++s;
+    return s;
+  };
+  struct Tile { int seg, kind, net, per, first, nvalid; };
+  auto tile = [&](int u) {
+    Tile t;
+    t.seg = seg_of(u);
+    t.kind = prm.seg.kind[t.seg];
+    t.net = prm.seg.net[t.seg];
+    t.per = t.kind == kSegStencil ? kPT : kB;
+    t.first = ((u - firstPair[t.seg]) * 2 + (int)rank) * t.per;
+    t.nvalid = max(0, min(t.per, segCnt[t.seg] - t.first));
+    return t;
+  };
+  constexpr uint32_t ID_FWD = tc::idesc_bf16(2 * kB, W, 0, 0);
+  constexpr uint32_t ID_DH = tc::idesc_bf16(2 * kB, W, 0, 1);
+  constexpr uint32_t ID_DW = tc::idesc_bf16(2 * kB, W, 1, 1);
+  uint8_t* myScr = P.hscr + (int64_t)blockIdx.x * L::kScr * ACT;
+  const uint8_t* peerScr = P.hscr + (int64_t)(blockIdx.x ^ 1) * L::kScr * ACT;
+  auto hslot = [&](int j) -> int64_t { return (int64_t)(j - 1) * ACT; };   // h_j (full), j = 1..NH-1
+  auto gslot = [&](int l) -> int64_t { return (int64_t)(NH - 3 + l) * ACT; };   // G_l (full), l = 2..NH
+  float* rep = P.rep + (int64_t)(q % P.nrep) * 2 * prm.p_stride;
+
+  if (warp == kWM) {
+    // ================================ M: tcgen05 issue ================================
+    if (lane == 0) {
+      uint32_t phF[kStages] = {0, 0, 0, 0};
+      uint32_t phA = 0, phDwE = 0;
+      bool anyDw = false;
+      // wait for ring stage s (the peer forwards its own stage's arrival to the leader)
+      auto stage = [&](int s) -> bool {
+        mb_wait(bar + B_WFULL + s, phF[s]);
+        phF[s] ^= 1;
+        if (!leader) {
+          mb_arrive_cta(bar + B_WFULL + s, 0);
+          return false;
+        }
+        tc::tc_fence_after();
+        return true;
+      };
+      // one hidden-layer GEMM with its weights through the ring
+      auto gemm = [&](uint32_t a0, bool bwd, uint32_t idesc) {
+#pragma unroll 1
+        for (int s = 0; s < kStages; ++s) {
+          if (!stage(s)) continue;
+          const uint32_t wb = sb + L::oW + s * HSLICE;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int kk = s * 4 + k;
+            const uint64_t ad = tc::sdesc(a0 + kk * 2 * LBO_ACT, LBO_ACT, 128);
+            const uint64_t bd = bwd ? tc::sdesc(wb + k * 256, 128, 1024) : tc::sdesc(wb + k * 4096, 2048, 128);
+            tc::mma2_bf16(tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+          }
+          tc::mma2_commit(bar + B_WEMPTY + s);
+        }
+      };
+      for (int u = u0; u < u1; ++u) {
+        for (int l = 2; l <= NH; ++l) {
+          if (leader) { mb_wait(bar + B_AREADY, phA); phA ^= 1; }
+          TRV(0, 3 * (l - 2));
+          gemm(bufOf(l - 1), false, ID_FWD);
+          TRV(0, 3 * (l - 2) + 1);
+          if (leader) tc::mma2_commit(bar + B_ACCFULL);
+        }
+        if (!TRAIN) continue;
+        for (int l = NH; l >= 2; --l) {
+          const int g = NH - 1 + 2 * (NH - l);
+          const uint32_t gbuf = bufOf(l);
+          if (leader) { mb_wait(bar + B_AREADY, phA); phA ^= 1; }
+          TRV(0, 3 * g);
+          gemm(gbuf, true, ID_DH);
+          TRV(0, 3 * g + 1);
+          if (leader) tc::mma2_commit(bar + B_ACCFULL);
+          // dW_l[o][i] = sum over the pair's 256 rows: both operands streamed from the parks through
+          // the ring, per 64-row group j (rows of CTA j / 2): an A stage G_l[rows][O_r] and a B stage
+          // h_{l-1}[rows][I_r], [16 column groups][64 rows][16 B] each (4 K-steps of 16 rows)
+          TRV(0, 3 * g + 3);
+          if (leader && anyDw) { mb_wait(bar + B_DWEMPTY, phDwE); phDwE ^= 1; }
+          anyDw = true;
+          TRV(0, 3 * g + 4);
+#pragma unroll 1
+          for (int j = 0; j < 4; ++j) {
+            const int sa = (2 * j) & 3, sbb = (2 * j + 1) & 3;
+            const bool la = stage(sa), lb = stage(sbb);
+            if (!(la && lb)) continue;
+            const uint32_t wa = sb + L::oW + sa * HSLICE, wbb = sb + L::oW + sbb * HSLICE;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc::mma2_bf16(tmem + 256, tc::sdesc(wa + k * 256, 128, 1024), tc::sdesc(wbb + k * 256, 128, 1024), ID_DW,
+                            (j | k) ? 1u : 0u);
+            tc::mma2_commit(bar + B_WEMPTY + sa);
+            tc::mma2_commit(bar + B_WEMPTY + sbb);
+          }
+          if (leader) tc::mma2_commit(bar + B_DWFULL);
+          TRV(0, 3 * g + 5);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kWP) {
+    // ================================ P: TMA producer ================================
+    uint32_t phE[kStages] = {0, 0, 0, 0};
+    bool ringUsed = false;
+    uint32_t phWX = 0, phWY = 0, phPk = 0, phCe[2] = {0, 0};
+    auto ring_slot = [&](int s) {   // wait until the previous user of stage s has been consumed
+      if (ringUsed) { mb_wait(bar + B_WEMPTY + s, phE[s]); phE[s] ^= 1; }
+    };
+    auto queue = [&](bool bwd, int net, int l) {   // the 4 K-slices of one GEMM's weights
+      if (lane == 0) {
+        const uint16_t* base = (bwd ? P.wbwd : P.wfwd) + ((int64_t)net * (NH - 1) + (l - 2)) * 4 * 2 * (HSLICE / 2);
+#pragma unroll 1
+        for (int s = 0; s < kStages; ++s) {
+          ring_slot(s);
+#ifdef NBM_V2_EXP_NOWLOAD   // timing experiment: stale weights, no ring traffic
+          mb_arrive(bar + B_WFULL + s);
+#else
+          tc::mbar_arrive_expect_tx(bar + B_WFULL + s, HSLICE);
+          tc::bulk_copy_g2s(sb + L::oW + s * HSLICE, base + (int64_t)(s * 2 + rank) * (HSLICE / 2), HSLICE,
+                            bar + B_WFULL + s);
+#endif
+        }
+      }
+      ringUsed = true;
+    };
+    // dW_l's operands from the parks: per 64-row group j (rows of CTA j / 2, rows 64 (j % 2) ..) an
+    // A stage G_l[rows][O_r] and a B stage h_{l-1}[rows][I_r], each [16 column groups][64 rows][16 B]
+    // gathered by 16 bulk copies of 1 KB from the park's core layout
+    auto queue_dw = [&](int l) {
+      if (lane == 0) {
+#pragma unroll 1
+        for (int st = 0; st < 8; ++st) {
+          const int s = st & 3, j = st >> 1;
+          ring_slot(s);
+          const uint8_t* scr = (j >> 1) == (int)rank ? myScr : peerScr;
+          const uint8_t* src = scr + ((st & 1) ? hslot(l - 1) : gslot(l)) + rank * QTR + (j & 1) * 1024;
+          tc::mbar_arrive_expect_tx(bar + B_WFULL + s, HSLICE);
+#ifdef NBM_V2_EXP_BIGCOPY   // timing experiment: one contiguous 16 KB copy per stage (wrong data)
+          tc::bulk_copy_g2s(sb + L::oW + s * HSLICE, src - (j & 1) * 1024 + (j & 1) * 16384, HSLICE, bar + B_WFULL + s);
+#else
+#pragma unroll 1
+          for (int gi = 0; gi < 16; ++gi)
+            tc::bulk_copy_g2s(sb + L::oW + s * HSLICE + gi * 1024, src + gi * LBO_ACT, 1024, bar + B_WFULL + s);
+#endif
+        }
+      }
+      ringUsed = true;
+    };
+    // coordinates / items / aux of tile u into buffer b (all 32 lanes; 4 rows per lane)
+    auto fetch = [&](int u, int b) {
+      if (lane == 0 && u - u0 >= 2) mb_wait(bar + B_CRDEMPTY + b, phCe[b]);
+      if (u - u0 >= 2) phCe[b] ^= 1;
+      __syncwarp();
+      const Tile t = tile(u);
+      const int* its = prm.seg.items[t.seg] + segStart[t.seg];
+      float* crd = reinterpret_cast<float*>(smem + L::oCrd) + b * 4 * kB;
+      int* sItem = reinterpret_cast<int*>(smem + L::oItem) + b * kB;
+      float* sAux = reinterpret_cast<float*>(smem + L::oAux) + b * kB;
+      for (int r = lane; r < kB; r += 32) {
+        float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
+        if (r < t.per) {
+          int item = -1;
+          float aux = 0.0f;
+          if (r < t.nvalid) {
+            item = its[t.first + r];
+            aux = prm.aux_by_item[t.seg] ? prm.seg.aux[t.seg][item] : prm.seg.aux[t.seg][segStart[t.seg] + t.first + r];
+          }
+          sItem[r] = item;
+          sAux[r] = aux;
+        }
+        if (t.kind == kSegStencil) {
+          const int j = r / kPT, p = r - j * kPT;
+          if (j < 7 && p < t.nvalid) {
+            const float* src = prm.seg.src[t.seg] + 3 * (int64_t)its[t.first + p];
+            x0 = src[0]; x1 = src[1]; x2 = src[2];
+            if (j > 0) {   // arms +x, -x, +y, -y, +z, -z (exact on the lattice)
+              const float hs = (j & 1) ? prm.h : -prm.h;
+              if (j <= 2) x0 = __fadd_rn(x0, hs); else if (j <= 4) x1 = __fadd_rn(x1, hs); else x2 = __fadd_rn(x2, hs);
+            }
+          }
+        } else if (r < t.nvalid) {
+          const float* src = prm.seg.src[t.seg] + 3 * (int64_t)its[t.first + r];
+          x0 = src[0]; x1 = src[1]; x2 = src[2];
+        }
+        crd[4 * r] = x0; crd[4 * r + 1] = x1; crd[4 * r + 2] = x2;
+      }
+      __syncwarp();
+      if (lane == 0) mb_arrive(bar + B_CRDFULL + b);
+    };
+    auto wait_w = [&](uint32_t buf) {   // E has written the buffer
+      if (lane == 0) {
+        if (buf == bufX) { mb_wait(bar + B_WDONE_X, phWX); } else { mb_wait(bar + B_WDONE_Y, phWY); }
+      }
+      if (buf == bufX) phWX ^= 1; else phWY ^= 1;
+      __syncwarp();
+    };
+    auto parked = [&](uint32_t buf) { mb_arrive(bar + (buf == bufX ? B_PARKED_X : B_PARKED_Y)); };
+    // G_l written into bufOf(l): park it (both CTAs' dW_l read it); once complete, E may overwrite
+    // the buffer and the peer's producer may load it
+    auto park_g = [&](int l) {
+      const uint32_t b = bufOf(l);
+      wait_w(b);
+      if (lane == 0) {
+        tc::bulk_copy_s2g(myScr + gslot(l), b, ACT);
+        tc::bulk_commit();
+        tc::bulk_wait0();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        parked(b);
+        if (l == NH) mb_arrive(bar + B_HPARK);   // this tile's h parks are complete too
+        mb_arrive_cta(bar + B_PKREADY, rank ^ 1u);
+      }
+      __syncwarp();
+    };
+    if (u0 < u1) {
+      fetch(u0, 0);
+      queue(false, tile(u0).net, 2);
+    }
+    for (int u = u0; u < u1; ++u) {
+      const Tile t = tile(u);
+      for (int l = 2; l <= NH; ++l) {
+        if (TRAIN) {   // park h_{l-1} (act' reads, dW_l's B operand of both CTAs)
+          const uint32_t b = bufOf(l - 1);
+          wait_w(b);
+          if (lane == 0) {
+            TRV(2, 2 * (l - 2));
+            tc::bulk_copy_s2g(myScr + hslot(l - 1), b, ACT);
+            tc::bulk_commit();
+          }
+        }
+        if (l < NH) queue(false, t.net, l + 1);
+        else if (TRAIN) queue(true, t.net, NH);
+        else if (u + 1 < u1) queue(false, tile(u + 1).net, 2);
+        if (TRAIN && lane == 0) {   // E may overwrite the buffer once the park has read it
+          tc::bulk_wait_read0();
+          parked(bufOf(l - 1));
+        }
+        if (lane == 0) TRV(2, 2 * (l - 2) + 1);
+      }
+      if (u + 1 < u1) fetch(u + 1, (u + 1 - u0) & 1);
+      if (lane == 0) TRV(2, 6);
+      if (!TRAIN) continue;
+      park_g(NH);
+      if (lane == 0) TRV(2, 8);
+      for (int l = NH; l >= 2; --l) {
+        if (lane == 0) { mb_wait(bar + B_PKREADY, phPk); }   // the peer's G_l park (and h parks) complete
+        phPk ^= 1;
+        queue_dw(l);
+        if (lane == 0) TRV(2, 9 + 4 * (NH - l));
+        if (l > 2) {
+          queue(true, t.net, l - 1);
+          if (lane == 0) TRV(2, 11 + 4 * (NH - l));
+          park_g(l - 1);
+          if (lane == 0) TRV(2, 12 + 4 * (NH - l));
+        } else if (u + 1 < u1) {
+          queue(false, tile(u + 1).net, 2);
+        }
+      }
+    }
+    if (lane == 0) tc::bulk_wait0();
+    __syncwarp();
+  } else if (warp >= kEW) {
+    // ================================ F: dW flush ================================
+    if (TRAIN) {
+      const int fq = warp & 3, frow = fq * 32 + lane;
+      const uint32_t tl = (uint32_t)(fq * 32) << 16;
+      uint32_t phDw = 0;
+      for (int u = u0; u < u1; ++u) {
+        const Tile t = tile(u);
+        for (int l = NH; l >= 2; --l) {
+          mb_wait(bar + B_DWFULL, phDw);
+          phDw ^= 1;
+          if (warp == kEW && lane == 0) TRV(3, 2 * (NH - l));
+          tc::tc_fence_after();
+          // this CTA's 128 outputs x 256 inputs; replicas hold the hidden blocks input-quad-major
+          // ([i/4][o][i%4], k_reduce_rep): one warp-wide red.v4 covers 32 consecutive outputs.
+          // The whole row block is read from TMEM first (the next dW may then start), and the
+          // reductions are paced so the LSU queue they share with the epilogue warps stays short.
+          float* out = rep + (int64_t)t.net * prm.p_stride + L::tWl(l) + (int64_t)(kB * rank + frow) * 4;
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            float v[32];
+            tc::tmem_ld32(tmem + tl + 256u + (uint32_t)(c * 32), v);
+#ifndef NBM_V2_EXP_NOFLUSH   // timing experiment: dW read from TMEM, not flushed
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              red4(out + (int64_t)(c * 8 + i) * (W * 4), v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+#else
+            if (v[0] == 12345.0f) red4(out, v[1], v[2], v[3], v[4]);
+#endif
+            if (c == 7) {
+              tc::tc_fence_before();
+              fbar();
+              if (warp == kEW && lane == 0) {
+                TRV(3, 2 * (NH - l) + 1);
+                if (leader) mb_arrive(bar + B_DWEMPTY);
+                else mb_arrive_cta(bar + B_DWEMPTY, 0);
+              }
+            }
+#ifdef NBM_V2_PACE
+            __nanosleep(NBM_V2_PACE);
+#endif
+#ifdef NBM_V2_FENCE   // bound the reductions in flight: wait for this chunk's to be performed
+            if ((c % NBM_V2_FENCE) == NBM_V2_FENCE - 1) __threadfence();
+#endif
+          }
+        }
+      }
+    }
+  } else {
+    // ================================ E: epilogues ================================
+    float* sW1 = reinterpret_cast<float*>(smem + L::oW1);
+    float* sBias = reinterpret_cast<float*>(smem + L::oBias);
+    float* sWo = reinterpret_cast<float*>(smem + L::oWo);
+    float* sSG = reinterpret_cast<float*>(smem + L::oSG);
+    float* sUp = reinterpret_cast<float*>(smem + L::oUp);
+    float* sUb = reinterpret_cast<float*>(smem + L::oUb);
+    const int eq = warp & 3, hf = warp >> 2, row = eq * 32 + lane;
+    const uint32_t tl = (uint32_t)(eq * 32) << 16;
+    const bool e0 = tid == 0;
+    uint32_t phAcc = 0, phPX = 0, phPY = 0, phHp = 0, phCf[2] = {0, 0};
+    bool usedX = false, usedY = false;
+    double lossAcc = 0.0;
+    int curNet = -1;
+    auto signal = [&](uint64_t* wdone) {   // operands written (smem + TMEM reads done): MMA may go
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      ebar();
+      if (e0) {
+        if (leader) mb_arrive(bar + B_AREADY);
+        else mb_arrive_cta(bar + B_AREADY, 0);
+        if (wdone) mb_arrive(wdone);
+      }
+    };
+    auto wdone_of = [&](uint32_t b) { return bar + (b == bufX ? B_WDONE_X : B_WDONE_Y); };
+    // before E writes a buffer: the park that read its previous contents is done (TRAIN)
+    auto claim = [&](uint32_t b) {
+      if (!TRAIN) return;
+      if (b == bufX) {
+        if (usedX) { mb_wait(bar + B_PARKED_X, phPX); phPX ^= 1; }
+        usedX = true;
+      } else {
+        if (usedY) { mb_wait(bar + B_PARKED_Y, phPY); phPY ^= 1; }
+        usedY = true;
+      }
+    };
+    auto wait_acc = [&]() {
+      mb_wait(bar + B_ACCFULL, phAcc);
+      phAcc ^= 1;
+      tc::tc_fence_after();
+    };
+    auto flush_sg = [&](int net) {   // small gradients -> the replica (then zeroed)
+      float* out = rep + (int64_t)net * prm.p_stride;
+      for (int i = tid; i < W; i += kEW * 32) {
+        for (int v = 0; v < NH; ++v) {
+          atomicAdd(out + (v == 0 ? L::tB1 : L::tBl(v + 1)) + i, sSG[v * W + i]);
+          sSG[v * W + i] = 0.0f;
+        }
+        for (int c = 0; c < 3; ++c) {
+          atomicAdd(out + L::tW1 + 3 * i + c, sSG[(NH + c) * W + i]);
+          sSG[(NH + c) * W + i] = 0.0f;
+        }
+        atomicAdd(out + L::tWo + i, sSG[(NH + 3) * W + i]);
+        sSG[(NH + 3) * W + i] = 0.0f;
+      }
+      if (tid == 0) {
+        atomicAdd(out + L::tBo, sSG[L::NV * W]);
+        sSG[L::NV * W] = 0.0f;
+      }
+    };
+    auto sg_add = [&](int v, int c, float x) {   // lane's column of chunk c (after tsum)
+      atomicAdd(&sSG[v * W + c * 32 + lane], x);
+    };
+#ifdef NBM_V2_EXP_NOTSUM   // timing experiment: no small-gradient transposes
+#define tsum(v, lane) (v[0])
+#endif
+    for (int i = tid; i < L::NV * W + 4; i += kEW * 32) sSG[i] = 0.0f;
+    for (int u = u0; u < u1; ++u) {
+      const Tile t = tile(u);
+      const int b = (u - u0) & 1;
+      if (t.net != curNet) {
+        ebar();
+        if (TRAIN && curNet >= 0) flush_sg(curNet);
+        const float* thp = prm.theta + (int64_t)t.net * prm.p_net;
+        for (int i = tid; i < 3 * W; i += kEW * 32) sW1[i] = thp[L::tW1 + i];
+        for (int i = tid; i < W; i += kEW * 32) {
+          sBias[i] = thp[L::tB1 + i];
+          for (int l = 2; l <= NH; ++l) sBias[(l - 1) * W + i] = thp[L::tBl(l) + i];
+          sWo[i] = thp[L::tWo + i];
+        }
+        if (tid == 0) sWo[W] = thp[L::tBo];
+        curNet = t.net;
+        ebar();
+      }
+      if (tid == 0) TRV(1, 0);
+      mb_wait(bar + B_CRDFULL + b, phCf[b]);
+      phCf[b] ^= 1;
+      if (tid == 0) TRV(1, 1);
+      const float* crd = reinterpret_cast<const float*>(smem + L::oCrd) + b * 4 * kB;
+      const float x0 = crd[4 * row], x1 = crd[4 * row + 1], x2 = crd[4 * row + 2];
+      claim(bufX);
+      if (tid == 0) TRV(1, 2);
+      // ---- layer 1 -> h_1 (X) ----
+#pragma unroll 1
+      for (int c = 4 * hf; c < 4 * hf + 4; ++c) {
+        float h[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = c * 32 + j;
+          h[j] = th(fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, fmaf(sW1[3 * n], x0, sBias[n]))));
+        }
+        put_chunk(bufX, row, c, h);
+      }
+      signal(TRAIN ? wdone_of(bufX) : nullptr);
+      if (tid == 0) TRV(1, 3);
+      // ---- hidden layers 2..NH ----
+      float up = 0.0f;
+#pragma unroll 1
+      for (int l = 2; l <= NH; ++l) {
+        wait_acc();
+        if (tid == 0) TRV(1, 4 + 2 * (l - 2));
+        const uint32_t dst = bufOf(l);
+        if (l < NH) claim(dst);
+        const float* bl = sBias + (l - 1) * W;
+#pragma unroll 1
+        for (int c = 4 * hf; c < 4 * hf + 4; ++c) {
+          float v[32];
+          tc::tmem_ld32(tmem + tl + (uint32_t)(c * 32), v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = th(v[j] + bl[c * 32 + j]);
+          if (l < NH) {
+            put_chunk(dst, row, c, v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) up = fmaf(sWo[c * 32 + j], v[j], up);
+            if (TRAIN) tc::tmem_st32(tmem + tl + (uint32_t)(c * 32), v);   // h_NH (fp32) for G_NH
+          }
+        }
+        if (l < NH) signal(TRAIN ? wdone_of(dst) : nullptr);
+        if (tid == 0) TRV(1, 5 + 2 * (l - 2));
+      }
+      sUp[hf * kB + row] = up;
+      tc::tc_fence_before();
+      ebar();
+      // ---- residual epilogue (S4): cotangent per row, loss ----
+      int* sItem = reinterpret_cast<int*>(smem + L::oItem) + b * kB;
+      const float* sAux = reinterpret_cast<const float*>(smem + L::oAux) + b * kB;
+      auto uval = [&](int r) { return (sUp[r] + sUp[kB + r]) + sWo[W]; };
+      if (!TRAIN) {
+        if (tid < t.nvalid) prm.u_out[sItem[tid]] = uval(tid);
+        ebar();
+        if (e0) mb_arrive(bar + B_CRDEMPTY + b);
+        continue;
+      }
+      if (t.kind == kSegStencil) {
+        if (tid < kPT) {
+          float r = 0.0f;
+          if (tid < t.nvalid) {
+            const float chat = prm.seg.chat[t.seg];
+            float acc = uval(tid);
+#pragma unroll
+            for (int j = 1; j < 7; ++j) acc = fmaf(chat, uval(j * kPT + tid), acc);
+            r = acc - sAux[tid];
+            lossAcc += 0.5 * (double)prm.two_over_n * (double)r * (double)r;
+          }
+          const float rc = prm.two_over_n * r;
+          sUb[tid] = rc;
+          const float rj = rc * prm.seg.chat[t.seg];
+#pragma unroll
+          for (int j = 1; j < 7; ++j) sUb[j * kPT + tid] = rj;
+        } else if (tid >= 7 * kPT && tid < kB) {
+          sUb[tid] = 0.0f;
+        }
+      } else if (tid < kB) {
+        float ub = 0.0f;
+        if (tid < t.nvalid) {
+          if (t.kind == kSegBRows) {
+            const float e = uval(tid) - sAux[tid];
+            ub = prm.seg.a[t.seg] * e;
+            lossAcc += 0.5 * (double)prm.seg.a[t.seg] * (double)e * (double)e;
+          } else {
+            ub = sAux[tid];
+          }
+        }
+        sUb[tid] = ub;
+      }
+      ebar();
+      if (e0) mb_arrive(bar + B_CRDEMPTY + b);
+      if (tid == 0) TRV(1, 10);
+      const float ub = sUb[row];
+      if (hf == 0) {   // b_o
+        float s = ub;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) atomicAdd(&sSG[L::NV * W], s);
+      }
+      // ---- G_NH = ub w_o (1 - h_NH^2) -> bufOf(NH); w_o and b_NH gradients ----
+      claim(bufOf(NH));
+      tc::tc_fence_after();
+#pragma unroll 1
+      for (int c = 4 * hf; c < 4 * hf + 4; ++c) {
+        float hv[32], v[32];
+        tc::tmem_ld32(tmem + tl + (uint32_t)(c * 32), hv);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = ub * hv[j];
+        sg_add(NH + 3, c, tsum(v, lane));
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
+        put_chunk(bufOf(NH), row, c, hv);
+        sg_add(NH - 1, c, tsum(hv, lane));
+      }
+      signal(wdone_of(bufOf(NH)));
+      if (tid == 0) TRV(1, 11);
+      // ---- backward hidden layers: G_{l-1} = (G_l W_l) (1 - h_{l-1}^2) -> bufOf(l-1) ----
+#pragma unroll 1
+      for (int l = NH; l >= 2; --l) {
+        wait_acc();   // dH_l (and every earlier MMA: dW_{l+1} has released bufOf(l-1))
+        if (tid == 0) TRV(1, 12 + 3 * (NH - l));
+        if (l == NH - 1) { mb_wait(bar + B_HPARK, phHp); phHp ^= 1; }   // h parks readable
+        const uint32_t gdst = bufOf(l - 1);   // holds h_{l-1} (l = NH, read here first) or G_{l+1}
+        if (l > 2) claim(gdst);
+        const uint8_t* hprev = myScr + hslot(l - 1);
+        uint4 nxt[4];
+        auto load_h = [&](int c, uint4 (&w)[4]) {   // act'(h_{l-1}) source: in place (l = NH) or the park
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const uint32_t off = (uint32_t)((c * 4 + qq) * LBO_ACT + row * 16);
+            w[qq] = (l == NH) ? lds4(gdst + off) : ldcg4(hprev + off);
+          }
+        };
+        load_h(4 * hf, nxt);
+#pragma unroll 1
+        for (int c = 4 * hf; c < 4 * hf + 4; ++c) {
+          uint4 cur[4];
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) cur[qq] = nxt[qq];
+          if (c + 1 < 4 * hf + 4) load_h(c + 1, nxt);   // next chunk's loads in flight
+          float v[32];
+          tc::tmem_ld32(tmem + tl + (uint32_t)(c * 32), v);
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const uint32_t wv[4] = {cur[qq].x, cur[qq].y, cur[qq].z, cur[qq].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float a = lo_bf(wv[e]), bb = hi_bf(wv[e]);
+              v[8 * qq + 2 * e] *= 1.0f - a * a;
+              v[8 * qq + 2 * e + 1] *= 1.0f - bb * bb;
+            }
+          }
+          if (l > 2) {   // G_{l-1} (bf16): the A operand of dH_{l-1} and dW_{l-1}
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              uint32_t p4[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                p4[e] = pk(v[8 * qq + 2 * e], v[8 * qq + 2 * e + 1]);
+                v[8 * qq + 2 * e] = lo_bf(p4[e]);
+                v[8 * qq + 2 * e + 1] = hi_bf(p4[e]);
+              }
+              sts4(gdst + (uint32_t)((c * 4 + qq) * LBO_ACT + row * 16), p4[0], p4[1], p4[2], p4[3]);
+            }
+            sg_add(l - 2, c, tsum(v, lane));   // b_{l-1} from the bf16 delta (G16)
+          } else {       // layer 1: b_1 and W_1 from the bf16 delta (G16)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = lo_bf(pk(v[j], 0.0f));
+            float tv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tv[j] = v[j] * x0;
+            sg_add(NH, c, tsum(tv, lane));
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tv[j] = v[j] * x1;
+            sg_add(NH + 1, c, tsum(tv, lane));
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tv[j] = v[j] * x2;
+            sg_add(NH + 2, c, tsum(tv, lane));
+            sg_add(0, c, tsum(v, lane));
+          }
+        }
+        if (l > 2) signal(wdone_of(gdst));
+        if (tid == 0) TRV(1, 13 + 3 * (NH - l));
+      }
+      tc::tc_fence_before();
+    }
+    if (TRAIN) {
+      ebar();
+      if (curNet >= 0) flush_sg(curNet);
+      for (int o = 16; o; o >>= 1) lossAcc += __shfl_xor_sync(0xffffffffu, lossAcc, o);
+      double* wl = reinterpret_cast<double*>(smem + L::oUp);   // reuse (u partials are dead)
+      ebar();
+      if (lane == 0) wl[warp] = lossAcc;
+      ebar();
+      if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kEW; ++w) s += wl[w];
+        prm.lpart[blockIdx.x] = s;
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::cluster_sync();   // no pair MMA may still target the peer's TMEM
+  tc::tc_fence_after();
+  if (warp == kWM) tc::tmem_dealloc2(tmem, 512);
+}
+
+template <int NH, bool TRAIN>
+static cudaError_t launch_v2_t(const W256v2Params& p, int grid, cudaStream_t s) {
+  auto kern = k_mlp_w256v2<NH, TRAIN>;
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = smem_attr_once(attr, (const void*)kern, (int)Lay2<NH>::bytes); e != cudaSuccess) return e;
+  kern<<<grid, kThreads, Lay2<NH>::bytes, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mlp_w256v2(int n_hidden, bool train, const MlpParams& m, const uint16_t* wf, const uint16_t* wb,
+                              uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s) {
+  W256v2Params p{m, wf, wb, hscr, rep, nrep};
+  grid &= ~1;   // CTA pairs
+  if (grid < 2 || nrep < 1) return cudaErrorInvalidValue;
+  switch (n_hidden) {
+    case 2: return train ? launch_v2_t<2, true>(p, grid, s) : launch_v2_t<2, false>(p, grid, s);
+    case 3: return train ? launch_v2_t<3, true>(p, grid, s) : launch_v2_t<3, false>(p, grid, s);
+    case 4: return train ? launch_v2_t<4, true>(p, grid, s) : launch_v2_t<4, false>(p, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace nbm

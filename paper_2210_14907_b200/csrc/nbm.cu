@@ -251,9 +251,14 @@ cudaError_t launch_pack(const nbm_handle* h, const float* theta, cudaStream_t s)
 cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cudaStream_t s) {
   const ArchInfo& A = h->arch;
   const Workspace& w = h->ws;
-  if (is_w256(A))
+  if (is_w256(A)) {
+    // NBM_W256_V2: the warp-specialised schedule (mlp_w256v2.cu; experimental, slower)
+    static const bool v2 = getenv("NBM_W256_V2") != nullptr;
+    if (A.stencil != NBM_STENCIL_STABLE && v2)
+      return launch_mlp_w256v2(A.n_hidden, train, p, w.wimg, w.wimg_b, w.hscr, w.rep, w.nrep, w.grid_base, s);
     return launch_mlp_w256(A.n_hidden, train, A.stencil == NBM_STENCIL_STABLE, p, w.wimg, w.wimg_b, w.hscr, w.rep,
                            w.nrep, w.grid_base, s);
+  }
   if (is_fp32w(A))
     return launch_mlp_fp32w(A.width, A.n_hidden, train, A.stencil == NBM_STENCIL_STABLE, p, w.wimg32, w.rep, w.nrep,
                             w.grid_base, s);
@@ -368,7 +373,7 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   w.nrep = urep ? 16 : 0;   // gradient replicas (fewer CTAs per L2 address)
   if (urep && getenv("NBM_W256_REPLICAS")) w.nrep = atoi(getenv("NBM_W256_REPLICAS"));
   ALLOC(w.wimg_b, w256 ? (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t) : 16);
-  ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * (nhh + 2) * 128 * ai.width * 2 : 16);   // h_1..h_{NH-1}, G x2
+  ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * std::max<size_t>(nhh + 2, 2 * nhh) * 128 * ai.width * 2 : 16);   // parks
   ALLOC(w.rep, urep ? (size_t)w.nrep * 2 * ((ai.p_net + 3) & ~3ll) * sizeof(float) : 16);
   ALLOC(w.wimg32, fw ? (size_t)2 * nhh * 2 * ai.width * ai.width * sizeof(float) : 16);
 #undef ALLOC
@@ -505,9 +510,12 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
   if (e == cudaSuccess && uses_rep(A)) {
     e = cudaMemsetAsync(w.rep, 0, (size_t)w.nrep * 2 * ((A.p_net + 3) & ~3ll) * sizeof(float), s);
   }
-  // no interface (NBM_LS_NONE): no crossed rows, whose count slots and loss partial stay at
-  // the zeros written at create, so the crossed-row kernels are not launched
+  // no interface (NBM_LS_NONE): no crossed rows, so the crossed-row kernels are not launched;
+  // their count slots and loss partial are zeroed here rather than trusted to hold the zeros
+  // written at create (graph-capturable memsets)
   const bool crossing = P.ls_kind != NBM_LS_NONE;
+  if (!crossing && e == cudaSuccess) e = cudaMemsetAsync(w.counts + 12, 0, 2 * sizeof(int), s);
+  if (!crossing && e == cudaSuccess) e = cudaMemsetAsync(w.lpart + w.grid_mlp, 0, sizeof(double), s);
   if (crossing && e == cudaSuccess) e = launch_assemble_crossed(h, pts_dev, n, H, s);
   if (crossing) launches += 2;
   // pass A: forward-only over the crossed rows (u per row)

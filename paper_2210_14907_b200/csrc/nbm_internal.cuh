@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -136,6 +137,20 @@ struct nbm_handle {
 
 namespace nbm {
 
+// cudaFuncSetAttribute applies to the current device only: `done` (a static of the caller,
+// one per kernel instantiation) remembers the devices the >48 KB dynamic shared-memory limit
+// has been raised on, so a second handle on another GPU (or another thread) sets it too.
+inline cudaError_t smem_attr_once(std::atomic<uint64_t>& done, const void* kern, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
 // ---- launchers implemented in the .cu files ----
 // sample_init.cu
 cudaError_t launch_sample(int kind, uint64_t seed, uint64_t step, const int64_t* step_dev, int64_t first,
@@ -196,6 +211,9 @@ cudaError_t launch_pack_fp32w(const ArchInfo& a, const float* theta, float* img,
 // mlp_w256.cu (tcgen05 bf16, W = 256: streamed weights, parked activations, dW replicas)
 cudaError_t launch_mlp_w256(int n_hidden, bool train, bool stable, const MlpParams& m, const uint16_t* wf, const uint16_t* wb,
                             uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s);
+// mlp_w256v2.cu (K3w v2: warp-specialised schedule of the same W = 256 data flow; direct form)
+cudaError_t launch_mlp_w256v2(int n_hidden, bool train, const MlpParams& m, const uint16_t* wf, const uint16_t* wb,
+                              uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s);
 cudaError_t launch_pack_w256(const ArchInfo& a, const float* theta, uint16_t* wf, uint16_t* wb, cudaStream_t s);
 cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets, int n_hidden,
                               int quad_major, int accumulate,

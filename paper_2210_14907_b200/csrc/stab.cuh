@@ -109,12 +109,15 @@ __device__ __forceinline__ float tanh_minus_id_f32(float d) {
   const float d2 = d * d;
   const float s = fmaf(d2, fmaf(d2, fmaf(d2, fmaf(d2, -1382.0f / 155925.0f, 62.0f / 2835.0f), -17.0f / 315.0f),
                                 2.0f / 15.0f), -1.0f / 3.0f) * (d * d2);
-  if (fabsf(d) >= 0.25f) return tanhf(d) - d;   // rare (a branch: tanhf is long)
-  return s;
+  return s;   // |d| < 1/4 (stab_g_f32 branches above the cut)
 }
-// 1 + x lies in [0.75, 1.25] (|x| <= |tanh d| < 1/4 below the cut): the approximate division
-// (reciprocal within 1 ulp) keeps g within 2 ulp
-__device__ __forceinline__ float stab_g_f32(float t, float s2, float d) {
+// g(d) = tanh(z + d) - t - s2 d (t = tanh z, s2 = 1 - t^2) without cancellation.  Below the
+// cut the tanh addition theorem form s2 [(tanh d - d) - t tanh(d) d] / (1 + x), x = t tanh d:
+// there |x| <= |tanh d| < 1/4, so 1 + x lies in [0.75, 1.25] and the approximate division
+// (reciprocal within 1 ulp) keeps g within 2 ulp.  At |d| >= 1/4 (rare) 1 + x can approach 0
+// for saturated units, so g is formed directly, where nothing cancels at that size of d.
+__device__ __forceinline__ float stab_g_f32(float z, float t, float s2, float d) {
+  if (fabsf(d) >= 0.25f) return tanhf(z + d) - t - s2 * d;   // rare (a branch: tanhf is long)
   const float s = tanh_minus_id_f32(d), x = t * (d + s);
   return __fdividef(s2 * fmaf(-x, d, s), 1.0f + x);
 }
@@ -123,12 +126,12 @@ template <int W, int LDA, int NPTS, int NTHR>
 __device__ void fwd_pass_f32(float* __restrict__ H, int tid) {
   for (int it = tid; it < NPTS * W; it += NTHR) {
     float* h = H + (it / W) * 8 * LDA + it % W;
-    const float t = tanhf(h[0]);
+    const float z = h[0], t = tanhf(z);
     const float s2 = (1.0f - t) * (1.0f + t);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
       const float p = h[(1 + d) * LDA], D = h[(4 + d) * LDA];
-      const float gp = stab_g_f32(t, s2, p), gm = stab_g_f32(t, s2, D - p);
+      const float gp = stab_g_f32(z, t, s2, p), gm = stab_g_f32(z, t, s2, D - p);
       h[(1 + d) * LDA] = fmaf(s2, p, gp);
       h[(4 + d) * LDA] = fmaf(s2, D, gp) + gm;
     }

@@ -11,6 +11,8 @@ import torch
 
 from paper_2210_14907_b200 import inputs, nbm
 
+from _bars import floor_tol
+
 pytestmark = pytest.mark.gpu
 
 LOSS_TOL, GRAD_TOL = 1e-5, 1e-4
@@ -109,8 +111,10 @@ def _parity(orc, cfg, n, nb, seed=0, theta_seed=None, step=0, floor_factor=4):
             continue
         ltol, gtol = LOSS_TOL, GRAD_TOL
         if k < 2:   # ill-conditioned uncrossed terms: noise floor of fp32 (SURVEY 8c rule 2)
-            ltol = max(ltol, floor_factor * abs(lt32[k] - lt[k]) / lt[k])
-            gtol = max(gtol, floor_factor * np.linalg.norm(gt32[k] - gt[k]) / np.linalg.norm(gt[k]))
+            ltol = floor_tol(ltol, abs(lt32[k] - lt[k]) / lt[k], floor_factor)
+            gtol = floor_tol(gtol, np.linalg.norm(gt32[k] - gt[k]) / np.linalg.norm(gt[k]), floor_factor)
+            if ltol is None or gtol is None:   # unresolved in fp32 at this h (tolerance would exceed 0.1)
+                continue
         assert abs(tl - lt[k]) <= ltol * lt[k], (k, tl, lt[k], ltol)
         assert np.linalg.norm(tg - gt[k]) <= gtol * np.linalg.norm(gt[k]), (k, gtol)
     s.close()
@@ -177,8 +181,10 @@ def test_ragged_and_empty_batches(orc):
         L, _, g, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"])
         L32, _, g32, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"],
                                        mode=orc.MODE_F32)
-        ltol = max(LOSS_TOL, 4 * abs(L32 - L) / L)          # noise floor when only uncrossed rows
-        gtol = max(GRAD_TOL, 4 * np.linalg.norm(g32 - g) / np.linalg.norm(g))
+        ltol = floor_tol(LOSS_TOL, abs(L32 - L) / L)          # noise floor when only uncrossed rows
+        gtol = floor_tol(GRAD_TOL, np.linalg.norm(g32 - g) / np.linalg.norm(g))
+        if ltol is None or gtol is None:   # a few uncrossed residuals only: unresolved in fp32
+            continue
         assert abs(gl - L) <= ltol * L, (len(p_), len(b_), gl, L)
         assert np.linalg.norm(gg - g) <= gtol * np.linalg.norm(g)
     gl, gg = _gpu_loss_grad(s, dth, None, None)
@@ -327,8 +333,9 @@ def test_parity_config5_fp32_wide_ragged(orc, w, nh, n, nb):
     gl, gg = _gpu_loss_grad(s, _dev(th), _dev(p_) if n else None, _dev(b_) if nb else None)
     L, _, g, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"])
     L32, _, g32, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"], mode=orc.MODE_F32)
-    ltol = max(LOSS_TOL, 4 * abs(L32 - L) / L)
-    gtol = max(GRAD_TOL, 4 * np.linalg.norm(g32 - g) / np.linalg.norm(g))
+    ltol = floor_tol(LOSS_TOL, abs(L32 - L) / L)
+    gtol = floor_tol(GRAD_TOL, np.linalg.norm(g32 - g) / np.linalg.norm(g))
+    assert ltol is not None and gtol is not None
     assert abs(gl - L) <= ltol * L, (gl, L)
     assert np.linalg.norm(gg - g) <= gtol * np.linalg.norm(g)
     assert s.status() == 0
@@ -400,8 +407,9 @@ def test_multiresolution_parity(orc, name, levels, weights, n, nb):
     gl, gg = float(loss.item()), grad.double().cpu().numpy()
     L, g = orc.loss_grad_ml(pb, ar, th, p_, b_, cfg["h"], levels, weights)
     L32, g32 = orc.loss_grad_ml(pb, ar, th, p_, b_, cfg["h"], levels, weights, mode=orc.MODE_F32)
-    ltol = max(LOSS_TOL, 4 * abs(L32 - L) / L)
-    gtol = max(GRAD_TOL, 4 * np.linalg.norm(g32 - g) / np.linalg.norm(g))
+    ltol = floor_tol(LOSS_TOL, abs(L32 - L) / L)
+    gtol = floor_tol(GRAD_TOL, np.linalg.norm(g32 - g) / np.linalg.norm(g))
+    assert ltol is not None and gtol is not None
     assert abs(gl - L) <= ltol * L, (gl, L)
     assert np.linalg.norm(gg - g) <= gtol * np.linalg.norm(g)
     l1, _ = _gpu_loss_grad(s, _dev(th), _dev(p_), _dev(b_))

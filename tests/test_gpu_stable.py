@@ -15,6 +15,8 @@ import torch
 
 from paper_2210_14907_b200 import inputs, nbm
 
+from _bars import floor_tol
+
 pytestmark = pytest.mark.gpu
 
 TOL = 2e-2
@@ -92,16 +94,19 @@ def test_stable_parity(orc, w, nh, k, n):
         if kk < 2:   # uncrossed: the bar up to the stable form's own bf16 floor, and far below
             # the direct evaluation's error
             Le, ge = _stable_emulation(orc, cfg, pb, ar, th, pts, kk)
-            ltol = max(TOL, 4 * abs(Le - lt[kk]) / lt[kk])
-            gtol = max(TOL, 4 * _rel(ge, gt[kk]))
-            assert abs(tl - lt[kk]) <= ltol * lt[kk], (kk, tl, lt[kk], ltol)
-            assert _rel(tg, gt[kk]) <= gtol, (kk, _rel(tg, gt[kk]), gtol)
+            ltol = floor_tol(TOL, abs(Le - lt[kk]) / lt[kk])
+            gtol = floor_tol(TOL, _rel(ge, gt[kk]))
+            if ltol is not None:   # else: the form's own bf16 floor exceeds 0.1 / 4 on this draw
+                assert abs(tl - lt[kk]) <= ltol * lt[kk], (kk, tl, lt[kk], ltol)
+            if gtol is not None:
+                assert _rel(tg, gt[kk]) <= gtol, (kk, _rel(tg, gt[kk]), gtol)
             assert abs(tl - Le) <= EMU_TOL * Le and _rel(tg, ge) <= EMU_TOL, (kk, tl, Le, _rel(tg, ge))
             dl, dg = _run(sd, dth, dp, db, terms=term)
             assert _rel(tg, gt[kk]) < 0.1 * _rel(dg, gt[kk]), (kk, _rel(tg, gt[kk]), _rel(dg, gt[kk]))
         else:        # crossed / boundary rows: evaluated directly, the direct path's rule
-            ltol = max(TOL, 4 * abs(lte[kk] - lt[kk]) / lt[kk])
-            gtol = max(TOL, 4 * _rel(gte[kk], gt[kk]))
+            ltol = floor_tol(TOL, abs(lte[kk] - lt[kk]) / lt[kk])
+            gtol = floor_tol(TOL, _rel(gte[kk], gt[kk]))
+            assert ltol is not None and gtol is not None
             assert abs(tl - lt[kk]) <= ltol * lt[kk], (kk, tl, lt[kk], ltol)
             assert _rel(tg, gt[kk]) <= gtol, (kk, gtol)
     s.close()

@@ -11,6 +11,8 @@ import torch
 
 from paper_2210_14907_b200 import inputs, nbm
 
+from _bars import floor_tol
+
 pytestmark = pytest.mark.gpu
 
 TOL = 2e-2
@@ -59,8 +61,13 @@ def test_tc_parity(orc, name, w, nh):
             continue
         # noise floor of the bf16 rounding points (SURVEY 8c rule 2): the uncrossed terms, and
         # for config 3 (h = 1/512, beta 2:80) also the crossed term, sit below bf16 resolution
-        ltol = max(TOL, 4 * abs(lte[k] - lt[k]) / lt[k])
-        gtol = max(TOL, 4 * np.linalg.norm(gte[k] - gt[k]) / np.linalg.norm(gt[k]))
+        # at the configs' h; where the floor-derived tolerance would exceed 0.1 the term is not
+        # asserted here (test_gpu_r2_parity.test_bf16_coarse_h_per_term resolves it at h = 1/4)
+        ltol = floor_tol(TOL, abs(lte[k] - lt[k]) / lt[k])
+        gtol = floor_tol(TOL, np.linalg.norm(gte[k] - gt[k]) / np.linalg.norm(gt[k]))
+        if ltol is None or gtol is None:
+            assert k < 2 or name == "c3", (k, name)   # only the unresolved stencil terms
+            continue
         assert abs(tl - lt[k]) <= ltol * lt[k], (k, tl, lt[k], ltol)
         assert np.linalg.norm(tg - gt[k]) <= gtol * np.linalg.norm(gt[k]), (k, gtol)
     s.close()
@@ -208,8 +215,10 @@ def test_tc_ragged_and_empty(orc, name, w, nh):
         gl, gg = _run(s, _dev(th), _dev(p_) if len(p_) else None, _dev(b_) if len(b_) else None)
         L, _, g, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"])
         Le, _, ge, _ = orc.loss_grad(pb, ar, th, p_.reshape(-1, 3), b_.reshape(-1, 3), cfg["h"], mode=orc.MODE_BF16)
-        ltol = max(TOL, 4 * abs(Le - L) / L)
-        gtol = max(TOL, 4 * np.linalg.norm(ge - g) / np.linalg.norm(g))
+        ltol = floor_tol(TOL, abs(Le - L) / L)
+        gtol = floor_tol(TOL, np.linalg.norm(ge - g) / np.linalg.norm(g))
+        if ltol is None or gtol is None:   # interior-only rows at the config's h: unresolved
+            continue
         assert abs(gl - L) <= ltol * L, (len(p_), len(b_), gl, L)
         assert np.linalg.norm(gg - g) <= gtol * np.linalg.norm(g), (len(p_), len(b_))
     gl, gg = _run(s, _dev(th), None, None)
