@@ -381,19 +381,25 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
     } else if (kind == kSegStencil) {
       if (tid < PT) {
         float r = 0.0f;
+        float cj[6];   // arm coefficients c_j / d: uniform (constant beta) or per point (variable mu)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) cj[j] = prm.seg.chat[seg];
+        if (prm.pcoef && tid < nvalid) {
+          const float* pc = prm.pcoef + 6 * (int64_t)sItem[tid];
+#pragma unroll
+          for (int j = 0; j < 6; ++j) cj[j] = pc[j];
+        }
         if (tid < nvalid) {
-          const float chat = prm.seg.chat[seg];
           float acc = sU[tid];
 #pragma unroll
-          for (int j = 1; j < 7; ++j) acc = fmaf(chat, sU[j * PT + tid], acc);
+          for (int j = 1; j < 7; ++j) acc = fmaf(cj[j - 1], sU[j * PT + tid], acc);
           r = acc - sAux[tid];
           lossAcc += 0.5 * (double)prm.two_over_n * (double)r * (double)r;   // r^2 / N
         }
         const float rc = prm.two_over_n * r;
         sUb[tid] = rc;
-        const float rj = rc * prm.seg.chat[seg];
 #pragma unroll
-        for (int j = 1; j < 7; ++j) sUb[j * PT + tid] = rj;
+        for (int j = 1; j < 7; ++j) sUb[j * PT + tid] = rc * cj[j - 1];
       } else if (tid >= 7 * PT && tid < R) {
         sUb[tid] = 0.0f;
       }

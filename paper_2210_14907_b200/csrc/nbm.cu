@@ -314,8 +314,8 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   if (rc) { g_create_error = why; return rc; }
   rc = check_arch(arch, &ai, &why);
   if (rc) { g_create_error = why; return rc; }
-  if (dp.mu_kind != NBM_MU_CONST && !(ai.prec == NBM_PREC_FP32 && ai.width <= 64)) {
-    g_create_error = "variable mu: supported by the fp32 kernel with W <= 64 in this build";
+  if (dp.mu_kind != NBM_MU_CONST && ai.prec == NBM_PREC_FP32X) {
+    g_create_error = "variable mu: not supported by the split-plane fp32x kernel";
     return NBM_E_INVALID_ARCH;
   }
   if (dp.mu_kind != NBM_MU_CONST && ai.stencil == NBM_STENCIL_STABLE) {

@@ -37,7 +37,7 @@ def epoch_plan(N: int, batch: int):
 
 def train(cfg: dict, N: int, epochs: int, batch: int = 16384, lr: float = 1e-3, seed: int = 0,
           levels: int = 1, eval_M: int | None = None, log_every: int = 0, device: int = 0,
-          lr_schedule=None) -> dict:
+          lr_schedule=None, return_theta: bool = False) -> dict:
     """Train the configuration's network pair at base resolution N for `epochs` epochs and
     report the RMSE / L-inf errors on the (M+1)^3 nodal grid (M = N unless eval_M).
     lr_schedule: optional [(fraction of the epochs, lr), ...] phases (one captured graph per
@@ -84,6 +84,8 @@ def train(cfg: dict, N: int, epochs: int, batch: int = 16384, lr: float = 1e-3, 
            "steps_per_epoch": steps_per_epoch, "steps": epochs * steps_per_epoch, "levels": levels, "lr": lr if lr_schedule is None else list(lr_schedule),
            "seconds": t_train, "sec_per_epoch": t_train / epochs, "rmse": rmse, "linf": linf,
            "rmse_init": rmse0, "linf_init": linf0, "eval_M": eval_M or N, "loss_history": history}
+    if return_theta:
+        out["theta"] = s.theta.cpu().numpy()
     s.close()
     return out
 

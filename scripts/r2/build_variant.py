@@ -1,4 +1,4 @@
-"""Build an experimental libnbm variant with extra nvcc flags on the W = 256 v2 kernel only:
+"""Build an experimental libnbm variant with extra nvcc flags on the W = 256 kernels only:
 python scripts/r2/build_variant.py NAME -DFLAG ... -> paper_2210_14907_b200/libnbm_NAME.so (NBM_LIB=...)."""
 import os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
@@ -10,7 +10,7 @@ os.makedirs(od, exist_ok=True)
 objs = []
 for src, extra in b.SOURCES.items():
     o = os.path.join(b.OBJ, src.replace(".cu", ".o"))
-    if src == "mlp_w256v2.cu":
+    if src in ("mlp_w256v2.cu", "mlp_w256.cu"):
         o = os.path.join(od, src.replace(".cu", ".o"))
         subprocess.check_call([b.NVCC, *b.ARCH, *[c for c in b.COMMON if c not in ("-v", "-Xptxas")], *flags,
                                *extra, "-c", os.path.join(b.CSRC, src), "-o", o])

@@ -7,7 +7,7 @@ import pytest
 import torch
 
 from paper_2210_14907_b200 import inputs, nbm
-from test_gpu_parity import _dev, _parity
+from test_gpu_parity import TERMS, _dev, _parity
 
 pytestmark = pytest.mark.gpu
 
@@ -77,9 +77,55 @@ def test_paper41_eval(orc):
     s.close()
 
 
-def test_variable_mu_rejected_on_tensor_core_paths(orc):
+def test_variable_mu_rejected_on_split_plane_path(orc):
     cfg = inputs.config("p41")
-    cfg.update(sizes=[3, 128, 128, 1], act=inputs.ACT_TANH, prec=inputs.PREC_BF16)
+    cfg.update(sizes=[3, 64, 64, 1], act=inputs.ACT_TANH, prec=inputs.PREC_FP32X)
     with pytest.raises(nbm.NbmError) as e:
         nbm.Solver(cfg, 0, max_points=16)
     assert e.value.code == 1
+
+
+@pytest.mark.parametrize("w,nh,prec,hh", [(128, 3, inputs.PREC_BF16, 0.25), (64, 4, inputs.PREC_BF16, 0.25),
+                                          (256, 3, inputs.PREC_BF16, 0.25), (128, 3, inputs.PREC_FP32, 1 / 16),
+                                          (256, 2, inputs.PREC_FP32, 1 / 16)])
+def test_variable_mu_tensor_core_and_wide_paths(orc, w, nh, prec, hh):
+    """The section 4.1 coefficients mu-(x) = y^2 ln(x+2) + 4, mu+(x) = e^-z on K3t (bf16 W =
+    64, 128), K3w (bf16 W = 256) and K3fw (fp32 W = 128, 256): per-point arm coefficients c_j/d
+    (S:256 face midpoints, reading G24) in the residual epilogue.  Tanh networks with steep first
+    layers at a coarse h so every term is resolved at the kernel's precision; each term and each
+    parameter block against fp64 at the bar (bf16 2e-2 / fp32 1e-5, 1e-4), up to 4 x the
+    oracle's own emulation floor (capped at 0.1)."""
+    from _bars import check_blocks, floor_tol, rel
+    cfg = inputs.config("p41")
+    cfg.update(sizes=[3] + [w] * nh + [1], act=inputs.ACT_TANH, prec=prec, H=inputs.h_lattice(hh))
+    cfg["h"] = cfg["H"] / inputs.LATTICE
+    pb, ar = orc.from_config(cfg)
+    n, nb = 2048, 256
+    pts = orc.sample(0, 3, 0, 0, n, cfg["H"])
+    bpts = orc.sample(1, 3, 0, 0, nb, cfg["H"])
+    th = inputs.random_theta(cfg["sizes"], 2, 21)
+    P1 = inputs.param_count(cfg["sizes"], 1)
+    for net in range(2):
+        th[net * P1:net * P1 + 3 * w] *= 16.0
+    mode = orc.MODE_BF16 if prec == inputs.PREC_BF16 else orc.MODE_F32
+    bl, bg = (2e-2, 2e-2) if prec == inputs.PREC_BF16 else (1e-5, 1e-4)
+    L, lt, g, gt = orc.loss_grad(pb, ar, th, pts, bpts, cfg["h"], per_term=True)
+    Le, lte, ge, gte = orc.loss_grad(pb, ar, th, pts, bpts, cfg["h"], per_term=True, mode=mode)
+    s = nbm.Solver(cfg, 0, max_points=n)
+    dth, dp, db = _dev(th), _dev(pts), _dev(bpts)
+    loss, grad = s.loss_grad(dp, db, theta=dth)
+    torch.cuda.synchronize()
+    gl, gg = float(loss.item()), grad.double().cpu().numpy()
+    assert abs(gl - L) <= floor_tol(bl, abs(Le - L) / L) * L and rel(gg, g) <= floor_tol(bg, rel(ge, g))
+    assert check_blocks(gg, g, ge, cfg["sizes"], 2, bg) >= 2 * nh
+    for k, term in enumerate(TERMS):
+        assert lt[k] > 0, k
+        tl, tg = s.loss_grad(dp, db, terms=term, theta=dth)
+        torch.cuda.synchronize()
+        tl, tg = float(tl.item()), tg.double().cpu().numpy()
+        ltol, gtol = floor_tol(bl, abs(lte[k] - lt[k]) / lt[k]), floor_tol(bg, rel(gte[k], gt[k]))
+        assert ltol is not None and gtol is not None, k
+        assert abs(tl - lt[k]) <= ltol * lt[k], (k, tl, lt[k], ltol)
+        assert rel(tg, gt[k]) <= gtol, (k, rel(tg, gt[k]), gtol)
+    assert s.status() == 0
+    s.close()
