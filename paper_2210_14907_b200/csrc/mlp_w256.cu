@@ -139,6 +139,51 @@ __device__ __forceinline__ void get_half_g(const uint8_t* gbuf, int r, int c, in
     }
   }
 }
+// Two / four transpose-sums interleaved stage by stage (independent shuffle chains: the single
+// chain's 5 dependent stages are latency-bound).  tsum2: lane l receives column l of a and of b.
+__device__ __forceinline__ void tsum2(float (&a)[32], float (&b)[32], int lane, float& ra, float& rb) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const float sa = up ? a[i] : a[i + s], ka = up ? a[i + s] : a[i];
+      const float sb = up ? b[i] : b[i + s], kb = up ? b[i + s] : b[i];
+      a[i] = ka + __shfl_xor_sync(0xffffffffu, sa, s);
+      b[i] = kb + __shfl_xor_sync(0xffffffffu, sb, s);
+    }
+  }
+  ra = a[0];
+  rb = b[0];
+}
+// column sums over the warp's rows of v x0, v x1, v x2 and v (layer-1 gradients): the first
+// stage forms the products on the fly, so only 4 x 16 partial sums are live after it
+__device__ __forceinline__ void tsum_x4(const float (&v)[32], float x0, float x1, float x2, int lane, float (&r)[4]) {
+  float p[4][16];
+  {
+    const bool up = (lane & 16) != 0;
+    const float xs[4] = {x0, x1, x2, 1.0f};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float send = up ? v[i] : v[i + 16], keep = up ? v[i + 16] : v[i];
+#pragma unroll
+      for (int d = 0; d < 4; ++d) p[d][i] = keep * xs[d] + __shfl_xor_sync(0xffffffffu, send * xs[d], 16);
+    }
+  }
+#pragma unroll
+  for (int s = 8; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i)
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        const float send = up ? p[d][i] : p[d][i + s], keep = up ? p[d][i + s] : p[d][i];
+        p[d][i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+      }
+  }
+#pragma unroll
+  for (int d = 0; d < 4; ++d) r[d] = p[d][0];
+}
 // 16-column warp transpose-sum: lanes l and l + 16 receive the sum over the warp's 32 rows of
 // column l % 16
 __device__ __forceinline__ float tsum16(float (&v)[16], int lane) {
@@ -443,6 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   Fetch cur = fetch(u0), nxt;
   if (u0 < u1 && tid == 0) queue_gemm(false, prm.seg.net[seg_of(u0)], 2);
   int curNet = -1;
+  bool h1Staged = false;   // the tile's h_1 was formed under the previous tile's dW_2 (TMEM stash)
   for (int u = u0; u < u1; ++u) {
     const int seg = seg_of(u);
     const int kind = prm.seg.kind[seg], net = prm.seg.net[seg];
@@ -460,18 +506,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       __syncthreads();
     }
     // ---- gather: items, aux and coordinates were prefetched during the previous tile ----
-    if (tid < kB) {
-      if (tid < per) {
-        sItem[tid] = cur.item;
-        sAux[tid] = cur.aux;
+    if (!h1Staged) {
+      if (tid < kB) {
+        if (tid < per) {
+          sItem[tid] = cur.item;
+          sAux[tid] = cur.aux;
+        }
+        sX[4 * tid] = cur.x0; sX[4 * tid + 1] = cur.x1; sX[4 * tid + 2] = cur.x2;
       }
-      sX[4 * tid] = cur.x0; sX[4 * tid + 1] = cur.x1; sX[4 * tid + 2] = cur.x2;
+      __syncthreads();
     }
-    __syncthreads();
     TRW(0);
     const float x0 = sX[4 * row], x1 = sX[4 * row + 1], x2 = sX[4 * row + 2];
     // ---- layer 1 -> h1 (tile 0, parked copy) ----
-    for (int k = 0; k < 2; ++k) {
+    if (h1Staged) {   // formed under the previous dW_2: TMEM stash -> tile 0
+      tc::tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int c = 2 * cg + k;
+        uint32_t pkd[16];
+        tc::tmem_ld16u(tmem + tlane + (uint32_t)(64 * cg) + 16u * k, pkd);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq)
+          sts4(aBuf[0] + (uint32_t)((c * 4 + qq) * LBO_ACT + row * 16), pkd[4 * qq], pkd[4 * qq + 1], pkd[4 * qq + 2],
+               pkd[4 * qq + 3]);
+      }
+      h1Staged = false;
+    } else for (int k = 0; k < 2; ++k) {
       if (STAB && stab) {
         for (int hf = 0; hf < 2; ++hf) {
           float h[16];
@@ -663,18 +724,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), hv);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = ub * hv[j];
-      sg_add(NH + 3, c, tsum(v, lane));
 #pragma unroll
       for (int j = 0; j < 32; ++j) hv[j] = ub * sWo[c * 32 + j] * (1.0f - hv[j] * hv[j]);
       put_chunk(gb, nullptr, row, c, hv);
-      sg_add(NH - 1, c, tsum(hv, lane));
+      float s_wo, s_b;
+      tsum2(v, hv, lane, s_wo, s_b);
+      sg_add(NH + 3, c, s_wo);
+      sg_add(NH - 1, c, s_b);
     }
     tc::fence_proxy_async_smem();
     tc::tc_fence_before();
-    if (tid == 0) {   // all parked h are complete: the epilogues read them back with ld.global
-      tc::bulk_wait0();
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
     __syncthreads();
     tc::cluster_sync_relaxed();
     tc::tc_fence_after();
@@ -693,11 +752,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       if (tid == 0) {
         if (l > 2) queue_gemm(true, net, l - 1);
         else if (nextNet >= 0) queue_gemm(false, nextNet, 2);
-        tc::bulk_wait0();                 // parked G_l is complete (and gb has been read)
+        tc::bulk_wait0();                 // parked G_l (and, at l = NH, every parked h) is complete
+        if (l == NH) asm volatile("fence.proxy.async.global;" ::: "memory");
         tc::arrive_remote(bpark, rank ^ 1u);
       }
       TRW(27 + 3 * (NH - l));
       wait_bar(bmma, ph_mma);
+      if (l == NH) __syncthreads();       // the parked h are readable (ld.global) from here on
       if (tid == 0) {
         tc::mbar_wait(bpark, ph_park);    // the peer's parked G_l is complete
         ph_park ^= 1;
@@ -770,17 +831,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
           tc::tmem_st16u(stash + 16u * k, pkd);
           sg_add(l - 2, c, tsum(v, lane));
         } else {   // layer 1: dW1 += G1 x^T, db1 += G1
-          float tv[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) tv[j] = v[j] * x0;
-          sg_add(NH, c, tsum(tv, lane));
-#pragma unroll
-          for (int j = 0; j < 32; ++j) tv[j] = v[j] * x1;
-          sg_add(NH + 1, c, tsum(tv, lane));
-#pragma unroll
-          for (int j = 0; j < 32; ++j) tv[j] = v[j] * x2;
-          sg_add(NH + 2, c, tsum(tv, lane));
-          sg_add(0, c, tsum(v, lane));
+          float r4[4];
+          tsum_x4(v, x0, x1, x2, lane, r4);
+          sg_add(NH, c, r4[0]);
+          sg_add(NH + 1, c, r4[1]);
+          sg_add(NH + 2, c, r4[2]);
+          sg_add(0, c, r4[3]);
         }
       }
       tc::tc_fence_before();
@@ -800,6 +856,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
                             tc::sdesc(hb + t * QTR + kk * 256, 128, LBO_ACT), ID_DW, (t | kk) ? 1u : 0u);
           tc::mma2_commit(bdw);
         }
+      }
+      // the next tile's gather and layer 1 under dW_2 (same network, direct form): h_1 bf16 into this
+      // warp's accumulator columns (free at l = 2), copied to tile 0 once dW_2 has released it
+      if (!STAB && TRAIN && l == 2 && nextNet == net) {
+        if (tid < kB) {   // (slots past the next tile's item count hold item -1 / aux 0: unread)
+          sItem[tid] = cur.item;
+          sAux[tid] = cur.aux;
+          sX[4 * tid] = cur.x0; sX[4 * tid + 1] = cur.x1; sX[4 * tid + 2] = cur.x2;
+        }
+        __syncthreads();
+        const float y0 = sX[4 * row], y1 = sX[4 * row + 1], y2 = sX[4 * row + 2];
+        for (int k = 0; k < 2; ++k) {
+          float h[32];
+          layer1(2 * cg + k, y0, y1, y2, h);
+          uint32_t pkd[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pkd[j] = pk(h[2 * j], h[2 * j + 1]);
+          tc::tmem_st16u(tmem + tlane + (uint32_t)(64 * cg) + 16u * k, pkd);
+        }
+        tc::tc_fence_before();
+        h1Staged = true;
       }
       wait_bar(bdw, ph_dw);
       // both CTAs' bulk loads of h_{l-1} and G_l (and this CTA's act' reads) are complete: the
