@@ -295,11 +295,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   tc::tc_fence_after();
   const uint32_t tmem = *sTmem;   // [0,256): GEMM accumulator, [256,512): dW
   for (int i = tid; i < (NH + 4) * W + 4; i += kThreads) reinterpret_cast<float*>(smem + L::oSG)[i] = 0.0f;
-  int firstPair[kNumSeg + 1];
-  int total = 0;
-#pragma unroll
-  for (int s = 0; s < kNumSeg; ++s) { firstPair[s] = total; total += segPairs[s]; }
-  firstPair[kNumSeg] = total;
+  __shared__ int firstPair[kNumSeg + 1];   // shared: a per-thread array indexed at run time is local memory
+  if (tid == 0) {
+    int tot = 0;
+    for (int s = 0; s < kNumSeg; ++s) { firstPair[s] = tot; tot += segPairs[s]; }
+    firstPair[kNumSeg] = tot;
+  }
+  __syncthreads();
+  const int total = firstPair[kNumSeg];
   const int NC = gridDim.x >> 1, q = blockIdx.x >> 1;
   const int u0 = (int)((int64_t)total * q / NC), u1 = (int)((int64_t)total * (q + 1) / NC);
   const uint32_t aBuf[2] = {sb + L::oX, sb + L::oY};
