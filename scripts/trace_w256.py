@@ -1,6 +1,6 @@
 import ctypes, os, sys
 sys.path.insert(0, '.')
-os.environ["NBM_LIB"] = os.path.abspath("paper_2210_14907_b200/libnbm_exp.so")
+os.environ.setdefault("NBM_LIB", os.path.abspath("paper_2210_14907_b200/libnbm_trace.so"))
 import numpy as np, torch
 from paper_2210_14907_b200 import inputs, nbm
 cfg = inputs.config("c4"); cfg["N"] = 1 << 18; cfg["Nb"] = 1 << 15
