@@ -23,12 +23,13 @@ SOURCES = {
     "geometry.cu": ["-fmad=false"],
     "mlp_fp32.cu": [],
     "mlp_tc.cu": [],
+    "mlp_tch.cu": [],
     "mlp_w256.cu": [],
     "mlp_w256v2.cu": [],
     "mlp_fp32w.cu": [],
     "nbm.cu": [],
 }
-HEADERS = ["nbm_internal.cuh", "tc_ptx.cuh", "stab.cuh"]
+HEADERS = ["nbm_internal.cuh", "tc_ptx.cuh", "tc_epi.cuh", "stab.cuh"]
 
 
 def _mtime(p):

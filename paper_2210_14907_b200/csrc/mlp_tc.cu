@@ -31,10 +31,13 @@
 #include "nbm_internal.cuh"
 #include "stab.cuh"
 #include "tc_ptx.cuh"
+#include "tc_epi.cuh"
 
 namespace nbm {
 
 namespace {
+
+using namespace epi;
 
 constexpr int kTB = 128;   // rows per tile (= MMA M = TMEM lanes)
 constexpr int kTPT = 18;   // stencil points per tile
@@ -95,53 +98,6 @@ struct TcLayout {
   static constexpr int64_t tWo = 4 * W + (int64_t)NHH * (W * W + W);
   static constexpr int64_t tBo = tWo + W;
 };
-
-// core-matrix (8 rows x 16 B) layout of an [R][C] bf16 tile: element (r, c) at
-// (c/8)*R*16 + r*16 + (c%8)*2 bytes.
-__device__ __forceinline__ uint32_t core_off(int R, int r, int c8) { return (uint32_t)(c8 * R * 16 + r * 16); }
-
-// two fp32 -> packed bf16x2 (RNE), one cvt.rn.bf16x2.f32 (F2FP) instruction; a -> low half
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
-  return r;
-}
-__device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
-
-__device__ __forceinline__ float sigmoid_fast(float z);
-// bf16 path activation: MUFU tanh.approx.f32 (max relative error 2^-10.99, below the bf16
-// operand rounding; the fp32 configs use the accurate tanhf, G15).
-__device__ __forceinline__ float tanh_fast(float x) {
-  float y;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-// logistic via one MUFU op: sg(z) = 0.5 + 0.5 tanh(z / 2)
-__device__ __forceinline__ float sigmoid_fast(float z) { return fmaf(0.5f, tanh_fast(0.5f * z), 0.5f); }
-
-// lane j of the warp receives the sum over the warp's 32 rows of v[j] (fixed butterfly)
-__device__ __forceinline__ float warp_transpose_sum(float (&v)[32], int lane) {
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool up = (lane & s) != 0;
-#pragma unroll
-    for (int i = 0; i < s; ++i) {
-      const float send = up ? v[i] : v[i + s];
-      const float keep = up ? v[i + s] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-    }
-  }
-  return v[0];
-}
-
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-__device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
-  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr) : "memory");
-}
 
 // one thread's 32 columns of a row -> bf16 core-matrix buffer
 __device__ __forceinline__ void store_chunk_bf16(uint32_t buf, int row, int chunk, const float (&h)[32]) {
@@ -296,15 +252,18 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
   uint32_t wphase = 0;
   int wnet = -1, wl = -1;
   bool wpending = false;
-  auto wload = [&](int net, int l) {   // tid 0 only; the stage must be free (no MMA in flight)
+  // the MMA-issuing warp (warp 0, converged): every lane keeps the same bookkeeping
+  auto wload = [&](int net, int l) {   // warp 0 only; the stage must be free (no MMA in flight)
     if (!STREAM || (net == wnet && l == wl)) return;
-    tc::mbar_arrive_expect_tx(wbar, L::WMAT_BYTES);
-    tc::bulk_copy_g2s(aWh, prm.wimg + ((int64_t)net * NHH + (l - 2)) * W * W, L::WMAT_BYTES, wbar);
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(wbar, L::WMAT_BYTES);
+      tc::bulk_copy_g2s(aWh, prm.wimg + ((int64_t)net * NHH + (l - 2)) * W * W, L::WMAT_BYTES, wbar);
+    }
     wnet = net;
     wl = l;
     wpending = true;
   };
-  auto wwait = [&]() {   // tid 0 only, before an MMA reading the stage
+  auto wwait = [&]() {   // warp 0 only, before an MMA reading the stage
     if (STREAM && wpending) {
       tc::mbar_wait(wbar, wphase);
       wphase ^= 1;
@@ -412,19 +371,21 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       }
     }
     tc::fence_proxy_async_smem();
-    if (tid == 0) wload(net, 2);
+    if (warp == 0) wload(net, 2);
 #pragma unroll
     for (int v = 0; v < NT; ++v) tg[v] = 0.0f;
     gWo = gBN = gbo = 0.0f;
   };
 
-  // one GEMM of ksteps x K=16 on the tensor core (single thread)
+  // one GEMM of ksteps x K=16 on the tensor core, issued by warp 0 (one elected lane); the
+  // descriptors advance by the K step in their 16-byte address field
   auto gemm = [&](uint32_t dcol, uint32_t a0, uint32_t a_step, uint32_t a_lbo, uint32_t a_sbo, uint32_t b0,
                   uint32_t b_step, uint32_t b_lbo, uint32_t b_sbo, uint32_t idesc, int ksteps, bool acc) {
-#pragma unroll 1
+    const uint64_t ad = tc::sdesc(a0, a_lbo, a_sbo), bd = tc::sdesc(b0, b_lbo, b_sbo);
+#pragma unroll 4
     for (int s = 0; s < ksteps; ++s)
-      tc::mma_bf16(tmem + dcol, tc::sdesc(a0 + s * a_step, a_lbo, a_sbo), tc::sdesc(b0 + s * b_step, b_lbo, b_sbo),
-                   idesc, (acc || s > 0) ? 1u : 0u);
+      tc::mma_bf16_w(tmem + dcol, ad + (uint64_t)((s * a_step) >> 4), bd + (uint64_t)((s * b_step) >> 4), idesc,
+                     (acc || s > 0) ? 1u : 0u);
   };
   // the plane products of a split GEMM (P = 3): planes i + j <= 2, the smallest first; P = 1: one
   auto gemm_p = [&](uint32_t dcol, uint32_t a0, uint32_t a_step, uint32_t a_lbo, uint32_t a_sbo, uint32_t a_pl,
@@ -661,16 +622,16 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
     Fetch nxt;
 #pragma unroll 1
     for (int l = 2; l <= NH; ++l) {
-      if (tid == 0) {
+      if (warp == 0) {
         wwait();
         tc::tc_fence_after();
         gemm_p(0, aAct + (l - 2) * L::ABUF, 2 * LBO_ACT, LBO_ACT, 128, AP, wmat(l), 2 * LBO_W, LBO_W, 128, WP, ID_FWD,
                W / 16, false);
-        tc::mma_commit(bar);
+        tc::mma_commit_w(bar);
       }
       if (!TRAIN && l == 2) nxt = fetch(t + 1);   // the next tile's loads overlap this tile
       wait_mma();
-      if (tid == 0 && l < NH) wload(curNet, l + 1);   // prefetch the next layer's weights
+      if (warp == 0 && l < NH) wload(curNet, l + 1);   // prefetch the next layer's weights
       TR(2 + 2 * (l - 2));
       float v[32];
       tc::tmem_ld32(tmem + tlane + ccol, v);
@@ -849,21 +810,21 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
     for (int l = NH; l >= 2; --l) {
       const uint32_t gbuf = (l == NH) ? gbufNH : aAct + (l - 1) * L::ABUF;   // G_l
       const uint32_t hbuf = aAct + (l - 2) * L::ABUF;                        // h_{l-1}
-      if (tid == 0) {
+      if (warp == 0) {
         wwait();
         tc::tc_fence_after();
         // acc = G_l W_l: A = G (K-major), B = W_l (N = i, K = o: MN-major); its epilogue starts
         // while the dW MMA below still runs
         gemm_p(0, gbuf, 2 * LBO_ACT, LBO_ACT, 128, AP, wmat(l), 256, 128, LBO_W, WP, ID_DH, W / 16, false);
-        tc::mma_commit(bar);
+        tc::mma_commit_w(bar);
         // dW_l += G_l^T h_{l-1}: A = G (M = o, MN-major), B = h (N = i, MN-major), K = rows
         gemm_p((uint32_t)(W * (l - 1)), gbuf, 256, 128, LBO_ACT, AP, hbuf, 256, 128, LBO_ACT, AP, ID_DW, kTB / 16,
                !dwFresh);
-        tc::mma_commit(dwbar);
+        tc::mma_commit_w(dwbar);
       }
       if (l == NH) nxt = fetch(t + 1);   // the next tile's loads, under the longest MMA phase
       wait_mma();
-      if (tid == 0) wload(curNet, l > 2 ? l - 1 : 2);   // next GEMM's weights (W_2 for the next tile)
+      if (warp == 0) wload(curNet, l > 2 ? l - 1 : 2);   // next GEMM's weights (W_2 for the next tile)
       TR(11 + 2 * (NH - l));
       // G_{l-1} = acc * (1 - h~^2), h~ = the bf16 operand copy of h_{l-1} (own row, chunk)
       float v[32], hq[32];
@@ -936,7 +897,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       TR(12 + 2 * (NH - l));
     }
     // ---- tile tail: bias gradients of layers 1..NH-1 and dW_1 on the tensor core ----
-    if (tid == 0) {
+    if (warp == 0) {
       tc::tc_fence_after();
       for (int l = 2; l <= NH - 1; ++l)   // db_l = G_l^T 1   (G_l in buffer l-1; every plane of G)
         for (int p = 0; p < P; ++p)
@@ -946,7 +907,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       for (int p = 0; p < P; ++p)
         gemm((uint32_t)(16 * (NH - 2)), aAct + p * AP, 256, 128, LBO_ACT, aXm, 256, 128, 2048, ID_TAIL, kTB / 16,
              p > 0);
-      tc::mma_commit(bar);
+      tc::mma_commit_w(bar);
     }
     tailPending = true;   // collected under the next tile's gather and layer 1
     cur = nxt;

@@ -262,8 +262,14 @@ cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cu
   if (is_fp32w(A))
     return launch_mlp_fp32w(A.width, A.n_hidden, train, A.stencil == NBM_STENCIL_STABLE, p, w.wimg32, w.rep, w.nrep,
                             w.grid_base, s);
-  if (A.prec == NBM_PREC_BF16)
+  if (A.prec == NBM_PREC_BF16) {
+    // the training pass of the direct form at W = 64 / 128 (tanh): K3h (two half-tiles in flight);
+    // NBM_TCH_OFF selects K3t for comparison
+    static const bool tch_off = getenv("NBM_TCH_OFF") != nullptr;
+    if (train && A.stencil != NBM_STENCIL_STABLE && !tch_off && mlp_tch_supported(A.width, A.n_hidden, A.act))
+      return launch_mlp_tch(A.width, A.n_hidden, p, w.grid_base, s);
     return launch_mlp_tc(A.width, A.n_hidden, A.act, 1, train, A.stencil == NBM_STENCIL_STABLE, p, w.grid_base, s);
+  }
   if (A.prec == NBM_PREC_FP32X) return launch_mlp_tc(A.width, A.n_hidden, A.act, 3, train, false, p, w.grid_base, s);
   return launch_mlp_fp32(A.width, A.n_hidden, A.act, train, A.stencil == NBM_STENCIL_STABLE, p, w.grid_base, s);
 }

@@ -203,6 +203,9 @@ cudaError_t launch_mlp_tc(int width, int n_hidden, int act, int planes, bool tra
 int mlp_tc_supported(int width, int n_hidden, int act, int planes);
 int mlp_tc_ctas_per_sm(int width, int n_hidden, int planes);
 cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t* wimg, cudaStream_t s);
+// mlp_tch.cu (K3h: the bf16 training pass with two 64-row half-tiles in flight; tanh, direct form)
+int mlp_tch_supported(int width, int n_hidden, int act);
+cudaError_t launch_mlp_tch(int width, int n_hidden, const MlpParams& p, int grid, cudaStream_t s);
 // mlp_fp32w.cu (fp32, W = 128 / 256: streamed weights, per-tile dW flushes into replicas)
 int mlp_fp32w_supported(int width, int n_hidden);
 cudaError_t launch_mlp_fp32w(int width, int n_hidden, bool train, bool stable, const MlpParams& p, const float* wimg,

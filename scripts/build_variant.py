@@ -10,7 +10,7 @@ objs = []
 for src, extra in b.SOURCES.items():
     o = os.path.join(od, src.replace(".cu", ".o"))
     base = os.path.join(b.OBJ, src.replace(".cu", ".o"))
-    if src in ("mlp_w256.cu", "mlp_tc.cu", "mlp_fp32.cu", "nbm.cu") or not os.path.exists(base):
+    if src in ("mlp_w256.cu", "mlp_tc.cu", "mlp_tch.cu", "mlp_fp32.cu", "nbm.cu") or not os.path.exists(base):
         subprocess.check_call([b.NVCC, *b.ARCH, *[c for c in b.COMMON if c not in ("-v", "-Xptxas")], *flags,
                                *extra, "-c", os.path.join(b.CSRC, src), "-o", o])
     else:

@@ -9,6 +9,32 @@
 #include "tc_ptx.cuh"
 using namespace nbm::tc;
 
+// the MMA issued by one elected lane of a converged warp (the predicate from elect.sync inside
+// the asm, operands warp-uniform): no per-instruction waterfall loop around UTCHMMA
+__device__ __forceinline__ void mma_bf16_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b32 rx;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "elect.sync rx|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      ".reg .b32 rx;\n"
+      "elect.sync rx|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 __global__ void __launch_bounds__(512, 1) k(long long* out, int mode, int arg) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
@@ -43,6 +69,31 @@ __global__ void __launch_bounds__(512, 1) k(long long* out, int mode, int arg) {
       }
       out[0] = best_issue;
       out[1] = best_done;
+    }
+  } else if (mode == 4 || mode == 5) {   // A': the same R instructions issued by a converged warp 0
+    const int R = mode == 4 ? 64 : 8;
+    if (warp == 0) {
+      const uint32_t id = idesc_bf16(128, arg, 0, 0);
+      long long best_issue = 1 << 30, best_done = 1 << 30;
+      const uint64_t a0 = sdesc(sb, 2048, 128), b0 = sdesc(sb + 65536, 2048, 128);
+      for (int rep = 0; rep < 8; ++rep) {
+        __syncwarp();
+        const long long t0 = clock64();
+#pragma unroll 8
+        for (int i = 0; i < R; ++i)
+          mma_bf16_warp(tmem, a0 + (uint64_t)((i & 3) * 256), b0 + (uint64_t)((i & 3) * 256), id, i > 0);
+        const long long t1 = clock64();
+        mma_commit_warp(&bar);
+        mbar_wait(&bar, phase);
+        phase ^= 1;
+        const long long t2 = clock64();
+        if (t1 - t0 < best_issue) best_issue = t1 - t0;
+        if (t2 - t0 < best_done) best_done = t2 - t0;
+      }
+      if (tid == 0) {
+        out[0] = best_issue;
+        out[1] = best_done;
+      }
     }
   } else if (mode == 2) {   // B: round trip of one K = 16 * arg GEMM, N = 128
     if (tid == 0) {
@@ -95,12 +146,12 @@ int main() {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   long long h[2];
   for (int n : {16, 64, 128, 256}) {
-    for (int m : {0, 1}) {
+    for (int m : {0, 1, 4, 5}) {
       k<<<1, 512, 160 * 1024>>>(d, m, n);
       cudaError_t e = cudaDeviceSynchronize();
       cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-      const int R = m == 0 ? 64 : 8;
-      printf("A  %2d MMAs M128 N%-3d K16: issue %6lld cyc (%5.1f/instr)  done %6lld cyc (%5.1f/instr; floor %d)  %s\n", R,
+      const int R = (m == 0 || m == 4) ? 64 : 8;
+      printf("A%s %2d MMAs M128 N%-3d K16: issue %6lld cyc (%5.1f/instr)  done %6lld cyc (%5.1f/instr; floor %d)  %s\n", m >= 4 ? "'" : " ", R,
              n, h[0], (double)h[0] / R, h[1], (double)h[1] / R, 128 * n / 256, cudaGetErrorString(e));
     }
   }
