@@ -63,6 +63,13 @@ __global__ void __cluster_dims__(2, 1, 1) bench(long long* out, int mode) {
             ad = sdesc(A + kk * 2 * 2048, 2048, 128); bd = sdesc(B + (kk & 3) * 4096, 2048, 128);
             id = idesc_bf16(256, 128, 0, 0);
             mma2_bf16(tmem + 128, ad, bd, id, kk > 0);
+          } else if (mode == 6 || mode == 7) {   // M = 128 pairs (64 rows per CTA): two instructions per K-step
+            // (rows 0-63 -> D columns [0,128), rows 64-127 -> [128,256)); A [64][256] K-major blocks
+            ad = sdesc(A + kk * 2 * 1024, 1024, 128); bd = sdesc(B + kk * 2 * 2048, 2048, 128);
+            id = idesc_bf16(128, 256, 0, 0);
+            mma2_bf16(tmem, ad, bd, id, kk > 0);
+            ad = sdesc(A + 32768 + kk * 2 * 1024, 1024, 128);
+            if (mode == 7) d = tmem + 128;
           } else {                   // mode 5: fwd, A K-major 128B swizzle, B no swizzle
             const int kb = kk >> 2, ki = kk & 3;
             ad = sdesc_sw128(A + kb * 16384 + ki * 32, 1024); bd = sdesc(B + (kk & 3) * 4096, 2048, 128);
@@ -91,8 +98,9 @@ int main() {
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   const char* names[] = {"fwd  A K / B K (no swizzle)", "dH   A K / B MN (no swizzle)", "dW   A MN / B MN (no swizzle)",
                          "fwd  A K / B K (128B swizzle)", "fwd  N=128 x2 halves (no swizzle)",
-                         "fwd  A K sw128 / B K no swizzle"};
-  for (int m = 0; m < 6; ++m) {
+                         "fwd  A K sw128 / B K no swizzle", "fwd  2 x M128 pair, same D (K-major)",
+                         "fwd  2 x M128 pair, D halves (K-major)"};
+  for (int m = 0; m < 8; ++m) {
     bench<<<2, 128, 200 * 1024>>>(d, m);
     cudaError_t e = cudaDeviceSynchronize();
     long long v = 0;
