@@ -51,7 +51,12 @@ def kernel_name(cfg):
         return "k_mlp_tc<P=3> (tcgen05, 3-plane bf16 split)"
     if cfg.get("stencil", 0) == inputs.STENCIL_STABLE:
         return "k_mlp_tc<STAB> (tcgen05, difference propagation)"
-    return "k_mlp_w256 (tcgen05 cta_group::2)" if w == 256 else "k_mlp_tc (tcgen05)"
+    if w == 256:
+        return "k_mlp_w256 (tcgen05 cta_group::2)"
+    nh = len(cfg["sizes"]) - 2
+    if w == 128 and cfg["act"] == inputs.ACT_TANH and 3 <= nh <= 4 and not os.environ.get("NBM_TCH_OFF"):
+        return "k_mlp_tch (tcgen05, two 64-row half-tiles in flight)"
+    return "k_mlp_tc (tcgen05)"
 
 
 def load_peaks():

@@ -54,6 +54,7 @@ struct HLayout {
   static constexpr int NBUF = NH - 1 > 2 ? NH - 1 : 2;   // activation buffers per half
   static constexpr int CH = W / 32;                      // 32-column chunks per row
   static constexpr int NTR = NH + 5;                     // tail rows kept: [1, x_hi, x_lo, y_hi, y_lo, z_hi, z_lo] + db_2..db_{NH-1}
+  static constexpr int NTP = NTR | 1;                    // their stride per unit o (odd: the 16 row-lanes of a collect hit 16 banks)
   static constexpr uint32_t ACT = kHR * W * 2;           // one bf16 half-tile activation buffer
   static constexpr uint32_t WMAT = W * W * 2;            // one bf16 weight matrix
   static constexpr uint32_t TAILA = 16 * kHR * 2;        // one tail A operand: [16][64] bf16, K-major
@@ -63,8 +64,8 @@ struct HLayout {
   static constexpr uint32_t oTailO = oTailX + 2 * TAILA;  // [NH-2] A_l: ones in row 7 + (l-2)
   static constexpr uint32_t oTailPad = oTailO + (NH - 2) * TAILA;   // the M-groups 2..7 of the last
                                                                     // A operand read past it
-  static constexpr uint32_t oTacc = oTailPad + 1024;     // fp32 [half][NTR][W] tail accumulators
-  static constexpr uint32_t oW1 = oTacc + 4 * 2 * NTR * W;   // fp32 [W][3]
+  static constexpr uint32_t oTacc = oTailPad + 1024;     // fp32 [half][W][NTP] tail accumulators
+  static constexpr uint32_t oW1 = oTacc + 4 * 2 * NTP * W;   // fp32 [W][3]
   static constexpr uint32_t oBias = oW1 + 4 * 3 * W;     // fp32 [NH][W]
   static constexpr uint32_t oWo = oBias + 4 * NH * W;    // fp32 [W] + bo
   static constexpr uint32_t oHalf = oWo + 4 * (W + 4);   // per-half scalars
@@ -136,7 +137,7 @@ __device__ long long g_tch_trace[2][8][32];   // CTA 0: [half][half-tile][point]
 template <int W, int NH>
 __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB) k_mlp_tch(const MlpParams prm) {
   using L = HLayout<W, NH>;
-  constexpr int NWH = L::NWH, HT = NWH * 32, CH = L::CH, NTR = L::NTR;
+  constexpr int NWH = L::NWH, HT = NWH * 32, CH = L::CH, NTR = L::NTR, NTP = L::NTP;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = tc::smem_u32(smem);
   float* sW1 = reinterpret_cast<float*>(smem + L::oW1);
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
   float* sUb = reinterpret_cast<float*>(hs + L::hUb);
   float* sAux = reinterpret_cast<float*>(hs + L::hAux);
   int* sItem = reinterpret_cast<int*>(hs + L::hItem);
-  float* sTacc = reinterpret_cast<float*>(smem + L::oTacc) + half * NTR * W;
+  float* sTacc = reinterpret_cast<float*>(smem + L::oTacc) + half * NTP * W;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::oBar) + half;        // acc MMAs of this half
   uint64_t* dwbar = reinterpret_cast<uint64_t*>(smem + L::oBar + 16) + half;  // dW MMAs of this half
 
@@ -257,14 +258,14 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
         }
     }
     const float* T0 = reinterpret_cast<const float*>(smem + L::oTacc);
-    const float* T1 = T0 + NTR * W;
+    const float* T1 = T0 + NTP * W;
     for (int o = tid; o < W; o += L::THREADS) {   // tail reductions: halves in fixed order
-      out[L::tB1 + o] = T0[o] + T1[o];
+      const float* a = T0 + o * NTP;
+      const float* b = T1 + o * NTP;
+      out[L::tB1 + o] = a[0] + b[0];
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        out[L::tW1 + 3 * o + c] = (T0[(1 + 2 * c) * W + o] + T0[(2 + 2 * c) * W + o]) +
-                                  (T1[(1 + 2 * c) * W + o] + T1[(2 + 2 * c) * W + o]);
-      for (int l = 2; l <= NH - 1; ++l) out[L::tBl(l) + o] = T0[(5 + l) * W + o] + T1[(5 + l) * W + o];
+      for (int c = 0; c < 3; ++c) out[L::tW1 + 3 * o + c] = (a[1 + 2 * c] + a[2 + 2 * c]) + (b[1 + 2 * c] + b[2 + 2 * c]);
+      for (int l = 2; l <= NH - 1; ++l) out[L::tBl(l) + o] = a[5 + l] + b[5 + l];
     }
     // transposed gradients: [half][quad][2][W] + [half][quad] bo, summed in (half, quad) order
     float* scr = reinterpret_cast<float*>(smem + L::oAct);
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
     }
     tc::fence_proxy_async_smem();
     float* T = reinterpret_cast<float*>(smem + L::oTacc);
-    for (int i = tid; i < 2 * NTR * W; i += L::THREADS) T[i] = 0.0f;
+    for (int i = tid; i < 2 * NTP * W; i += L::THREADS) T[i] = 0.0f;
     {
       float z[32];
 #pragma unroll
@@ -379,9 +380,9 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
       float v[32];
       tc::tmem_ld16x2(tMine, v);
       if (r16 < NTR) {
-        float* t = sTacc + r16 * W + ccol;
+        float* t = sTacc + ccol * NTP + r16;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) t[j] += v[j];
+        for (int j = 0; j < 32; ++j) t[j * NTP] += v[j];
       }
     }
     tailPending = false;
