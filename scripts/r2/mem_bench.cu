@@ -7,6 +7,8 @@
 //   4  TMA loads by warp 0 while 480 threads issue reductions          (load rate, red rate)
 //   5  TMA loads while TMA stores of the same CTA run (both by warp 0) (combined)
 //   6  TMA loads while 480 threads issue plain stores
+//   7  TMA bulk reductions (cp.reduce.async.bulk .add.f32, 16 KB chunks, smem -> global)  alone
+//   8  TMA loads while the same warp issues TMA bulk reductions           (combined)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I ../../paper_2210_14907_b200/csrc mem_bench.cu -o mem_bench
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -36,7 +38,7 @@ __global__ void __launch_bounds__(512, 1) k(const uint8_t* src, float* dst, uint
   if (warp == 0) {
     if (tid == 0) {
       uint32_t ph[STAGES] = {0, 0, 0, 0};
-      if (mode == 0 || mode == 4 || mode == 5 || mode == 6) {
+      if (mode == 0 || mode == 4 || mode == 5 || mode == 6 || mode == 8) {
         for (int i = 0; i < LOADS; ++i) {
           const int s = i % STAGES;
           if (i >= STAGES) { mbar_wait(&full[s], ph[s]); ph[s] ^= 1; }
@@ -46,9 +48,21 @@ __global__ void __launch_bounds__(512, 1) k(const uint8_t* src, float* dst, uint
             bulk_copy_s2g(myd + (size_t)(i % 64) * CH, sb + 65536 + (i % 4) * CH, CH);
             bulk_commit();
           }
+          if (mode == 8) {   // interleave a 16 KB bulk reduction
+            bulk_reduce_add_f32(dst + (size_t)(blockIdx.x % 16) * 65536 + (size_t)(i % 16) * (CH / 4),
+                                sb + 65536 + (i % 4) * CH, CH);
+            bulk_commit();
+          }
         }
         for (int s = 0; s < STAGES; ++s) { mbar_wait(&full[s], ph[s]); ph[s] ^= 1; }
-        if (mode == 5) bulk_wait0();
+        if (mode == 5 || mode == 8) bulk_wait0();
+      } else if (mode == 7) {
+        float* rdst = dst + (size_t)(blockIdx.x % 16) * 65536;
+        for (int i = 0; i < LOADS; ++i) {
+          bulk_reduce_add_f32(rdst + (size_t)(i % 16) * (CH / 4), sb + (i % 4) * CH, CH);
+          bulk_commit();
+        }
+        bulk_wait0();
       } else if (mode == 1) {
         for (int i = 0; i < LOADS; ++i) {
           bulk_copy_s2g(myd + (size_t)(i % 64) * CH, sb + (i % 4) * CH, CH);
@@ -82,8 +96,9 @@ int main() {
   cudaMalloc(&out, 2 * 148 * sizeof(long long));
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   const char* names[] = {"TMA loads alone", "TMA stores alone", "red.v4 alone", "st.v4 alone",
-                         "TMA loads + red.v4", "TMA loads + TMA stores", "TMA loads + st.v4"};
-  for (int m = 0; m < 7; ++m) {
+                         "TMA loads + red.v4", "TMA loads + TMA stores", "TMA loads + st.v4",
+                         "TMA bulk reduce alone", "TMA loads + TMA bulk reduce"};
+  for (int m = 0; m < 9; ++m) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaMemset(out, 0, 2 * 148 * sizeof(long long));
       k<<<148, 512, 160 * 1024>>>(src, dst, sdst, m, out);
@@ -93,7 +108,7 @@ int main() {
       double l = 0, r = 0;
       for (int b = 0; b < 148; ++b) { l += h[2 * b]; r += h[2 * b + 1]; }
       l /= 148; r /= 148;
-      const double lkb = LOADS * 16.0 * (m == 5 ? 2 : 1), rkb = 480.0 * REDS * 16 / 1024;
+      const double lkb = LOADS * 16.0 * ((m == 5 || m == 8) ? 2 : 1), rkb = 480.0 * REDS * 16 / 1024;
       if (rep == 1)
         printf("%-26s load/store %8.0f cyc = %6.1f B/clk | red/st %8.0f cyc = %6.1f B/clk  %s\n", names[m], l,
                l > 0 ? lkb * 1024 / l : 0.0, r, r > 0 ? rkb * 1024 / r : 0.0, cudaGetErrorString(e));
