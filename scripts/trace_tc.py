@@ -1,9 +1,11 @@
 import ctypes, os, sys
 sys.path.insert(0, '.')
-os.environ["NBM_LIB"] = os.path.abspath("paper_2210_14907_b200/libnbm_exp.so")
+os.environ.setdefault("NBM_LIB", os.path.abspath("paper_2210_14907_b200/libnbm_exp.so"))
 import numpy as np, torch
 from paper_2210_14907_b200 import inputs, nbm
-cfg = inputs.config("c5", width=int(os.environ.get("TW", "128"))); cfg["N"] = 1 << 18; cfg["Nb"] = 1 << 15
+# CFG=c3 traces config 3 (SiLU, streamed weights); otherwise config 5 at width TW
+cfg = inputs.config("c3") if os.environ.get("CFG") == "c3" else inputs.config("c5", width=int(os.environ.get("TW", "128")))
+cfg["N"] = 1 << 18; cfg["Nb"] = 1 << 15
 s = nbm.Solver(cfg, 0); s.init_params(0)
 p = torch.empty(cfg["N"], 3, device="cuda"); b = torch.empty(cfg["Nb"], 3, device="cuda")
 s.sample(0, 0, 0, 0, cfg["N"], p); s.sample(1, 0, 0, 0, cfg["Nb"], b)
