@@ -25,7 +25,6 @@ SOURCES = {
     "mlp_tc.cu": [],
     "mlp_tch.cu": [],
     "mlp_w256.cu": [],
-    "mlp_w256v2.cu": [],
     "mlp_fp32w.cu": [],
     "nbm.cu": [],
 }

@@ -252,10 +252,6 @@ cudaError_t launch_mlp_h(const nbm_handle* h, bool train, const MlpParams& p, cu
   const ArchInfo& A = h->arch;
   const Workspace& w = h->ws;
   if (is_w256(A)) {
-    // NBM_W256_V2: the warp-specialised schedule (mlp_w256v2.cu; experimental, slower)
-    static const bool v2 = getenv("NBM_W256_V2") != nullptr;
-    if (A.stencil != NBM_STENCIL_STABLE && v2)
-      return launch_mlp_w256v2(A.n_hidden, train, p, w.wimg, w.wimg_b, w.hscr, w.rep, w.nrep, w.grid_base, s);
     return launch_mlp_w256(A.n_hidden, train, A.stencil == NBM_STENCIL_STABLE, p, w.wimg, w.wimg_b, w.hscr, w.rep,
                            w.nrep, w.grid_base, s);
   }
@@ -379,7 +375,7 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   w.nrep = urep ? 16 : 0;   // gradient replicas (fewer CTAs per L2 address)
   if (urep && getenv("NBM_W256_REPLICAS")) w.nrep = atoi(getenv("NBM_W256_REPLICAS"));
   ALLOC(w.wimg_b, w256 ? (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t) : 16);
-  ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * std::max<size_t>(nhh + 2, 2 * nhh) * 128 * ai.width * 2 : 16);   // parks
+  ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * (nhh + 2) * 128 * ai.width * 2 : 16);   // parks: NH + 1 tiles per CTA (mlp_w256.cu kScr)
   ALLOC(w.rep, urep ? (size_t)w.nrep * 2 * ((ai.p_net + 3) & ~3ll) * sizeof(float) : 16);
   ALLOC(w.wimg32, fw ? (size_t)2 * nhh * 2 * ai.width * ai.width * sizeof(float) : 16);
 #undef ALLOC

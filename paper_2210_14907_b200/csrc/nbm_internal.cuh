@@ -214,9 +214,6 @@ cudaError_t launch_pack_fp32w(const ArchInfo& a, const float* theta, float* img,
 // mlp_w256.cu (tcgen05 bf16, W = 256: streamed weights, parked activations, dW replicas)
 cudaError_t launch_mlp_w256(int n_hidden, bool train, bool stable, const MlpParams& m, const uint16_t* wf, const uint16_t* wb,
                             uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s);
-// mlp_w256v2.cu (K3w v2: warp-specialised schedule of the same W = 256 data flow; direct form)
-cudaError_t launch_mlp_w256v2(int n_hidden, bool train, const MlpParams& m, const uint16_t* wf, const uint16_t* wb,
-                              uint8_t* hscr, float* rep, int nrep, int grid, cudaStream_t s);
 cudaError_t launch_pack_w256(const ArchInfo& a, const float* theta, uint16_t* wf, uint16_t* wb, cudaStream_t s);
 cudaError_t launch_reduce_rep(const float* rep, int nrep, int64_t p_net, int64_t p_stride, int n_nets, int n_hidden,
                               int quad_major, int accumulate,
