@@ -87,9 +87,9 @@ struct TcLayout {
   // mlp_tc_ctas_per_sm, which must agree): the three-plane split runs one CTA per SM
   static constexpr int MINB = (P == 1 && TMEM_COLS <= 256) ? 2 : 1;
   static_assert(bytes <= 232448, "shared memory");
-  static constexpr int MDW = W < 128 ? 128 : W;            // M of the dW / tail MMAs: rows o >= W of
-                                                           // the MN-major A run into the next buffer
-                                                           // and land in TMEM lanes that are never read
+  static constexpr int MDW = W;                            // M of the dW / tail MMAs (o-rows); at W = 64
+                                                           // the M = 64 layout: unit o in TMEM lane
+                                                           // 32 (o / 16) + o % 16 (scripts/r2/m64_probe.cu)
   static_assert(4 * (4 * 2 * W + 4) <= (int)ABUF * NBUF, "flush scratch");
   // theta offsets within one network (G17)
   static constexpr int64_t tW1 = 0, tB1 = 3 * W;
@@ -213,6 +213,9 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
   const int row = quad * 32 + lane;                       // tile row = TMEM lane
   const uint32_t tlane = (uint32_t)(quad * 32) << 16;
   const uint32_t ccol = (uint32_t)(chunk * 32);            // this thread's column chunk
+  // the dW / tail unit o held in this thread's TMEM lane (-1: none): lane = o for M = 128, lane
+  // 32 (o / 16) + o % 16 for the M = 64 layout of W = 64
+  const int o_lane = L::MDW == 64 ? (lane < 16 ? quad * 16 + lane : -1) : (row < W ? row : -1);
   if (tid < kNumSeg) {
     int c = prm.counts[prm.cnt_slot[tid]];
     segCnt[tid] = c;
@@ -301,9 +304,9 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
 #pragma unroll 1
       for (int l = 2; l <= NH; ++l) {
         float v[32];
-        tc::tmem_ld32(tmem + tlane + (uint32_t)(W * (l - 1)) + ccol, v);   // dW_l[o = row][i]
-        if (row < W) {
-          float4* dst = reinterpret_cast<float4*>(out + L::tWl(l) + (int64_t)row * W + ccol);
+        tc::tmem_ld32(tmem + tlane + (uint32_t)(W * (l - 1)) + ccol, v);   // dW_l[o = o_lane][i]
+        if (o_lane >= 0) {
+          float4* dst = reinterpret_cast<float4*>(out + L::tWl(l) + (int64_t)o_lane * W + ccol);
 #pragma unroll
           for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
@@ -313,8 +316,8 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
         for (int i = tid; i < W * W; i += THREADS) out[L::tWl(l) + i] = 0.0f;
     }
     // tensor-core reduced gradients: one thread per unit o (chunk-0 warps)
-    if (chunk == 0 && row < W) {
-      const int o = row;
+    if (chunk == 0 && o_lane >= 0) {
+      const int o = o_lane;
 #pragma unroll
       for (int l = 2; l <= NH - 1; ++l) out[L::tBl(l) + o] = tg[l - 2];
       out[L::tB1 + o] = tg[NH - 2];
