@@ -847,6 +847,16 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
         for (int j = 0; j < 32; ++j) hq[j] = 1.0f - hq[j] * hq[j];
       } else if (l - 1 >= 2) {             // SiLU': stored bf16 derivative
         load_chunk_bf16(aDer + (l - 3) * L::ACT_BYTES, row, chunk, hq);
+      } else if (L::NDER >= 2) {           // SiLU' of layer 1 (fp32), formed with h1 at l = 3
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w[4];
+            ld_shared_v4(aDer + b * L::ACT_BYTES + core_off(kTB, row, chunk * 4 + q), w[0], w[1], w[2], w[3]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hq[16 * b + 4 * q + e] = __uint_as_float(w[e]);
+          }
       } else {                             // SiLU' of layer 1: recomputed exactly from x
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -863,7 +873,28 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       store_chunk_planes<P>(hbuf, AP, row, chunk, v);   // G_{l-1} in place: h_{l-1} is consumed
       if (l - 1 == 2 && NH >= 3) {   // h1 again for dW_2 (buffer 0's G_NH is consumed)
         float h[32];
-        layer1(x0, x1, x2, h, stab);
+        if (SILU && L::NDER >= 2) {
+          // with SiLU'(z1) in fp32 for the l = 2 epilogue, in this thread's own (row, chunk)
+          // blocks of the two act' buffers (layer 2's was read above, layer 3's at l = 4)
+          float d[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int n = ccol + j;
+            const float z = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, fmaf(sW1[3 * n], x0, sBias[n])));
+            const float sg = sigmoid_fast(z);
+            h[j] = z * sg;
+            d[j] = sg * fmaf(z, 1.0f - sg, 1.0f);
+          }
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_shared_v4(aDer + b * L::ACT_BYTES + core_off(kTB, row, chunk * 4 + q), __float_as_uint(d[16 * b + 4 * q]),
+                           __float_as_uint(d[16 * b + 4 * q + 1]), __float_as_uint(d[16 * b + 4 * q + 2]),
+                           __float_as_uint(d[16 * b + 4 * q + 3]));
+        } else {
+          layer1(x0, x1, x2, h, stab);
+        }
         store_chunk_planes<P>(aAct, AP, row, chunk, h);
       }
       if (l == 2 && chunk == 0) {   // tail operand row: [1, x_hi, x_lo, y_hi, y_lo, z_hi, z_lo, 0]
