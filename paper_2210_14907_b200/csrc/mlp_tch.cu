@@ -565,7 +565,10 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
           gemm(tAcc, gbuf, 2 * LBO_ACT, LBO_ACT, 128, wmat(l), 256, 128, LBO_W, ID_DH, W / 16, false);
           tc::mma_commit_w(bar);
           // dW_l += G_l^T h_{l-1}: A = G (M = o, MN-major), B = h (N = i, MN-major), K = rows
-          while (sTurn[l] != seq) {
+          {   // a broken turn order would hang the GPU: trap after ~10 s instead
+            const long long w0 = clock64();
+            while (sTurn[l] != seq)
+              if (clock64() - w0 > 20000000000ll) __trap();
           }
           gemm(tmem + (uint32_t)(W * (l - 1)), gbuf, 256, 128, LBO_ACT, hbuf, 256, 128, LBO_ACT, ID_DW, kHR / 16, true);
           tc::mma_commit_w(dwbar);
