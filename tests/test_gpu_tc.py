@@ -36,8 +36,9 @@ def _run(s, th, p, b, terms=nbm.TERM_ALL):
 def test_tc_parity(orc, name, w, nh):
     """c5: 32-sphere union, tanh (resident weights); c3: star interface, Gaussian charges,
     SiLU (weights streamed by TMA bulk copies, bf16 SiLU' buffers); W = 64 runs two CTAs
-    per SM and M = 128 dW MMAs over the 64 real output units; c4 (W = 256) streams weights,
-    parks activations and flushes per-tile dW by vector reductions."""
+    per SM with M = 64 dW / tail MMAs; the W = 128 tanh training pass at 3-4 hidden layers is
+    K3h (two 64-row half-tiles in flight), 2 layers K3t; c4 (W = 256) streams weights, parks
+    activations and flushes per-tile dW by vector reductions."""
     cfg = inputs.config(name, width=w) if name in ("c4", "c5") else inputs.config(name)
     cfg["sizes"] = [3] + [w] * nh + [1]
     n, nb = 1 << 13, 1 << 10
