@@ -55,15 +55,27 @@ struct TcLayout {
   static constexpr bool STREAM = SILU;                     // weights streamed (TMA bulk) to make room
   static constexpr int NHH = NH - 1;
   static constexpr int NWRES = STREAM ? 1 : NHH;           // weight matrices held in shared memory
+  static constexpr int NWRES_() { return STREAM ? 1 : NHH; }
   static constexpr int NDER = SILU ? (NH - 2 > 0 ? NH - 2 : 0) : 0;   // bf16 act' buffers, layers 2..NH-1
   static constexpr int CH = W / 32;                        // 32-column chunks per row
   static constexpr int THREADS = 128 * CH;                 // 4 lane quadrants x CH chunks
-  static constexpr int NBUF = NH - 1 > 2 ? NH - 1 : 2;
   static constexpr int NT = NH + 2;                        // tensor-core reduced gradient vectors
   static constexpr uint32_t ACT_BYTES = kTB * W * 2;       // one bf16 activation plane
   static constexpr uint32_t WMAT_BYTES = W * W * 2;        // one bf16 weight plane
   static constexpr uint32_t ABUF = P * ACT_BYTES;          // one activation buffer (P planes)
   static constexpr uint32_t WBUF = P * WMAT_BYTES;         // one weight matrix (P planes)
+  static constexpr uint32_t TMEM_COLS = (W * NH <= 128) ? 128 : (W * NH <= 256) ? 256 : 512;
+  // CTAs per SM requested from the launch (TMEM permitting; the host sizes the partial slots with
+  // mlp_tc_ctas_per_sm, which must agree): the three-plane split runs one CTA per SM
+  static constexpr int MINB = (P == 1 && TMEM_COLS <= 256) ? 2 : 1;
+  // activation buffers: h_1..h_{NH-1} (G_{l-1} written in place of h_{l-1}); G_NH takes h_1's
+  // buffer and h_1 is recomputed for dW_2 -- unless one more buffer fits the per-CTA shared
+  // memory (XBUF: W = 64, and W = 128 at 3 hidden layers), which then holds G_NH
+  static constexpr int NBUF0 = NH - 1 > 2 ? NH - 1 : 2;
+  static constexpr uint32_t FIXED = NWRES_() * WBUF + NDER * ACT_BYTES + 8192 + 4 * 3 * W + 4 * NH * W + 4 * (W + 4) +
+                                    16 * kTB + 4 * CH * kTB + 16 * kTB + 64 + (STG > 0 ? 4 * kTB * (STG + 4) : 0);
+  static constexpr bool XBUF = NH >= 3 && (NBUF0 + 1) * ABUF + FIXED <= (MINB == 2 ? 113u * 1024u : 232448u);
+  static constexpr int NBUF = NBUF0 + (XBUF ? 1 : 0);
   static constexpr uint32_t oAct = 0;
   static constexpr uint32_t oWh = oAct + NBUF * ABUF;
   static constexpr uint32_t oDer = oWh + NWRES * WBUF;     // bf16 act'(z_l), l = 2..NH-1 (SiLU)
@@ -82,10 +94,7 @@ struct TcLayout {
   static constexpr int SLD = STG + 4;                       // staging row stride (floats)
   static constexpr uint32_t oStg = oBar + 64;              // fp32 [kTB][SLD] (stable form, W = 64)
   static constexpr uint32_t bytes = oStg + (STG > 0 ? 4 * kTB * SLD : 0);
-  static constexpr uint32_t TMEM_COLS = (W * NH <= 128) ? 128 : (W * NH <= 256) ? 256 : 512;
-  // CTAs per SM requested from the launch (TMEM permitting; the host sizes the partial slots with
-  // mlp_tc_ctas_per_sm, which must agree): the three-plane split runs one CTA per SM
-  static constexpr int MINB = (P == 1 && TMEM_COLS <= 256) ? 2 : 1;
+  static_assert(bytes == NBUF * ABUF + FIXED, "FIXED mirrors the carve");
   static_assert(bytes <= 232448, "shared memory");
   static constexpr int MDW = W;                            // M of the dW / tail MMAs (o-rows); at W = 64
                                                            // the M = 64 layout: unit o in TMEM lane
@@ -758,7 +767,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       gbo += b;
     }
     // ---- output layer backward: dwo += ub h_NH; G_NH = ub wo (1 - h_NH^2) -> bf16 ----
-    const uint32_t gbufNH = (NH == 2) ? aAct + L::ABUF : aAct;
+    const uint32_t gbufNH = L::XBUF ? aAct + (NH - 1) * L::ABUF : (NH == 2) ? aAct + L::ABUF : aAct;
     {
       float hv[32], v[32];
       tc::tmem_ld32(tmem + tlane + ccol, hv);
@@ -847,7 +856,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
         for (int j = 0; j < 32; ++j) hq[j] = 1.0f - hq[j] * hq[j];
       } else if (l - 1 >= 2) {             // SiLU': stored bf16 derivative
         load_chunk_bf16(aDer + (l - 3) * L::ACT_BYTES, row, chunk, hq);
-      } else if (L::NDER >= 2) {           // SiLU' of layer 1 (fp32), formed with h1 at l = 3
+      } else if (L::NDER >= 2 && !L::XBUF) {   // SiLU' of layer 1 (fp32), formed with h1 at l = 3
 #pragma unroll
         for (int b = 0; b < 2; ++b)
 #pragma unroll
@@ -871,7 +880,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       tc::mbar_wait(dwbar, dwphase);           // dW_l has read h_{l-1} (and G_l)
       dwphase ^= 1;
       store_chunk_planes<P>(hbuf, AP, row, chunk, v);   // G_{l-1} in place: h_{l-1} is consumed
-      if (l - 1 == 2 && NH >= 3) {   // h1 again for dW_2 (buffer 0's G_NH is consumed)
+      if (l - 1 == 2 && NH >= 3 && !L::XBUF) {   // h1 again for dW_2 (buffer 0's G_NH is consumed)
         float h[32];
         if (SILU && L::NDER >= 2) {
           // with SiLU'(z1) in fp32 for the l = 2 epilogue, in this thread's own (row, chunk)
