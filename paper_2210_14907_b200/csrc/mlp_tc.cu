@@ -73,7 +73,7 @@ struct TcLayout {
   // memory (XBUF: W = 64, and W = 128 at 3 hidden layers), which then holds G_NH
   static constexpr int NBUF0 = NH - 1 > 2 ? NH - 1 : 2;
   static constexpr uint32_t FIXED = NWRES_() * WBUF + NDER * ACT_BYTES + 8192 + 4 * 3 * W + 4 * NH * W + 4 * (W + 4) +
-                                    16 * kTB + 4 * CH * kTB + 16 * kTB + 64 + (STG > 0 ? 4 * kTB * (STG + 4) : 0);
+                                    16 * kTB + 4 * CH * kTB + 16 * kTB + 64 + (STG > 0 ? 4 * (THREADS / 32) * 4 * (8 * 20 + 16) : 0);
   static constexpr bool XBUF = NH >= 3 && (NBUF0 + 1) * ABUF + FIXED <= (MINB == 2 ? 113u * 1024u : 232448u);
   static constexpr int NBUF = NBUF0 + (XBUF ? 1 : 0);
   static constexpr uint32_t oAct = 0;
@@ -91,9 +91,11 @@ struct TcLayout {
   static constexpr uint32_t oAux = oUb + 4 * kTB;          // fp32 [kTB]
   static constexpr uint32_t oItem = oAux + 4 * kTB;        // int  [kTB]
   static constexpr uint32_t oBar = oItem + 4 * kTB;        // mbarriers (MMA, weights) + tmem base
-  static constexpr int SLD = STG + 4;                       // staging row stride (floats)
-  static constexpr uint32_t oStg = oBar + 64;              // fp32 [kTB][SLD] (stable form, W = 64)
-  static constexpr uint32_t bytes = oStg + (STG > 0 ? 4 * kTB * SLD : 0);
+  static constexpr int SLD = 20;                          // staging row stride (floats): 16 columns + pad
+  static constexpr int SPB = 8 * SLD + 16;                 // staging point-block stride: points p and p+1
+                                                           // of one item instruction hit disjoint banks
+  static constexpr uint32_t oStg = oBar + 64;              // fp32 [warp][4 points][SPB] (stable form, W = 64)
+  static constexpr uint32_t bytes = oStg + (STG > 0 ? 4 * (THREADS / 32) * 4 * SPB : 0);
   static_assert(bytes == NBUF * ABUF + FIXED, "FIXED mirrors the carve");
   static_assert(bytes <= 232448, "shared memory");
   static constexpr int MDW = W;                            // M of the dW / tail MMAs (o-rows); at W = 64
@@ -418,41 +420,45 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
     phase ^= 1;
     tc::tc_fence_after();
   };
-  // ---- stable maps through shared memory (SST, W = 64): per 32-column round, the owners of the
-  // round's chunk stage their rows (fp32), one thread per (point, column) maps the point's 7 rows
-  // in place, the owners read them back ----
-  float* sStg = reinterpret_cast<float*>(smem + L::oStg);
-  constexpr int SLD = L::SLD;
-  auto stage_round = [&](float (&v)[32], int rc, auto&& item) {
-    if (chunk == rc) {
+  // ---- stable maps through shared memory (SST, W = 64), warp-local: a warp holds its lane
+  // quadrant's 4 points (rows 8p..8p+7) x its 32-column chunk, so it stages them in its own
+  // [32][SLD] fp32 block in two 16-column halves, each lane maps two (point, column) items in
+  // place, and the lanes read their rows back: __syncwarp only, no CTA barriers ----
+  float* sStg = reinterpret_cast<float*>(smem + L::oStg) + warp * 4 * L::SPB;
+  constexpr int SLD = L::SLD, SPB = L::SPB;
+  float* myStg = sStg + (lane >> 3) * SPB + (lane & 7) * SLD;   // this lane's row
+  auto stage_half = [&](float (&v)[32], int hf, auto&& item) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<float4*>(sStg + row * SLD + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    }
-    __syncthreads();
-    for (int it = tid; it < kTPTS * 32; it += THREADS) item(it >> 5, it & 31);
-    __syncthreads();
-    if (chunk == rc) {
+    for (int q = 0; q < 4; ++q)
+      *reinterpret_cast<float4*>(myStg + 4 * q) =
+          make_float4(v[16 * hf + 4 * q], v[16 * hf + 4 * q + 1], v[16 * hf + 4 * q + 2], v[16 * hf + 4 * q + 3]);
+    __syncwarp();
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 f = *reinterpret_cast<const float4*>(sStg + row * SLD + 4 * q);
-        v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
-      }
+    for (int k2 = 0; k2 < 2; ++k2) {
+      const int it = lane + 32 * k2, p = it >> 4, c = it & 15;
+      item(p, c, (int)ccol + 16 * hf + c, 4 * quad + p);
     }
-    __syncthreads();
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 f = *reinterpret_cast<const float4*>(myStg + 4 * q);
+      v[16 * hf + 4 * q] = f.x; v[16 * hf + 4 * q + 1] = f.y; v[16 * hf + 4 * q + 2] = f.z; v[16 * hf + 4 * q + 3] = f.w;
+    }
+    __syncwarp();
   };
   // forward: v = the row's raw pre-activation (no bias) -> a, P_d, Q_d; bl = the layer's biases
   auto stage_fwd = [&](float (&v)[32], const float* bl) {
-    for (int rc = 0; rc < L::CH; ++rc)
-      stage_round(v, rc, [&](int k, int c) {
-        float* h = sStg + 8 * k * SLD + c;
-        const float t = tanh_fast(h[0] + bl[32 * rc + c]);
+#pragma unroll   // compile-time halves: v stays in registers
+    for (int hf = 0; hf < 2; ++hf)
+      stage_half(v, hf, [&](int p, int c, int col, int k) {
+        float* h = sStg + p * SPB + c;
+        const float t = tanh_fast(h[0] + bl[col]);
         const float s2 = fmaf(-t, t, 1.0f);
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-          const float p = h[(1 + d) * SLD], D = h[(4 + d) * SLD];
-          const float gp = stab::stab_g(t, s2, p), gm = stab::stab_g(t, s2, D - p);
-          h[(1 + d) * SLD] = fmaf(s2, p, gp);
+          const float pp = h[(1 + d) * SLD], D = h[(4 + d) * SLD];
+          const float gp = stab::stab_g(t, s2, pp), gm = stab::stab_g(t, s2, D - pp);
+          h[(1 + d) * SLD] = fmaf(s2, pp, gp);
           h[(4 + d) * SLD] = fmaf(s2, D, gp) + gm;
         }
         h[0] = t;
@@ -463,10 +469,10 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
   // and the activations are the bf16 copies in hbufA.  v <- (g_z, g_p, g_D)
   auto stage_bwd = [&](float (&v)[32], uint32_t hbufA) {
     const uint16_t* hb16 = reinterpret_cast<const uint16_t*>(smem + (hbufA - sbase));
-    for (int rc = 0; rc < L::CH; ++rc)
-      stage_round(v, rc, [&](int k, int c) {
-        float* g = sStg + 8 * k * SLD + c;
-        const int col = 32 * rc + c;
+#pragma unroll   // compile-time halves: v stays in registers
+    for (int hf = 0; hf < 2; ++hf)
+      stage_half(v, hf, [&](int p, int c, int col, int k) {
+        float* g = sStg + p * SPB + c;
         float H[7], R[7];
 #pragma unroll
         for (int j = 0; j < 7; ++j) {
