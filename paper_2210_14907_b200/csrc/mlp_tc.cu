@@ -652,11 +652,21 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       if (warp == 0 && l < NH) wload(curNet, l + 1);   // prefetch the next layer's weights
       TR(2 + 2 * (l - 2));
       float v[32];
-      tc::tmem_ld32(tmem + tlane + ccol, v);
       const float* bl = sBias + (l - 1) * W + ccol;
+      if (STAB && stab && !SST) {   // the octet maps in two 16-column halves (bounded register working set)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          float a16[16];
+          tc::tmem_ld16(tmem + tlane + ccol + 16 * hf, a16);
+          stab::stab_fwd<16>(a16, bl + 16 * hf, lane);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[16 * hf + j] = a16[j];
+        }
+      } else {
+        tc::tmem_ld32(tmem + tlane + ccol, v);
+      }
       if (STAB && stab) {
         if (SST) stage_fwd(v, sBias + (l - 1) * W);
-        else stab::stab_fwd(v, bl, lane);
       } else if (!SILU) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = act_tanh(v[j] + bl[j]);
@@ -846,13 +856,29 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       TR(11 + 2 * (NH - l));
       // G_{l-1} = acc * (1 - h~^2), h~ = the bf16 operand copy of h_{l-1} (own row, chunk)
       float v[32], hq[32];
-      tc::tmem_ld32(tmem + tlane + ccol, v);
+      if (!(STAB && stab && !SST)) tc::tmem_ld32(tmem + tlane + ccol, v);
       if (STAB && stab) {                  // the backward map of the difference form (G27)
         if (SST) {
           stage_bwd(v, hbuf);
-        } else {
-          load_chunk_bf16(hbuf, row, chunk, hq);
-          stab::stab_bwd(v, hq, lane);
+        } else {   // the octet maps in two 16-column halves (a bounded register working set)
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            float a16[16], h16[16];
+            tc::tmem_ld16(tmem + tlane + ccol + 16 * hf, a16);
+#pragma unroll
+            for (int qq = 0; qq < 2; ++qq) {
+              uint32_t w[4];
+              ld_shared_v4(hbuf + core_off(kTB, row, chunk * 4 + 2 * hf + qq), w[0], w[1], w[2], w[3]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                h16[8 * qq + 2 * e] = bf_lo(w[e]);
+                h16[8 * qq + 2 * e + 1] = bf_hi(w[e]);
+              }
+            }
+            stab::stab_bwd<16>(a16, h16, lane);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[16 * hf + j] = a16[j];
+          }
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) hq[j] = 1.0f;
