@@ -515,7 +515,17 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
         h[j] = fmaf(sW1[3 * n + 2], x2, fmaf(sW1[3 * n + 1], x1, sW1[3 * n] * x0));
       }
       if (SST) stage_fwd(h, sBias);
-      else stab::stab_fwd(h, sBias + ccol, lane);
+      else {   // the octet maps in two 16-column halves (bounded register working set)
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          float a16[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) a16[j] = h[16 * hf + j];
+          stab::stab_fwd<16>(a16, sBias + ccol + 16 * hf, lane);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) h[16 * hf + j] = a16[j];
+        }
+      }
       return;
     }
 #pragma unroll
@@ -799,14 +809,22 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = hv[j];
           stage_bwd(hv, 0u);
-        } else {
-          float a[32];
+        } else {   // w_o's gradient first, then the octet maps in 16-column halves
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            v[j] = a[j] = hv[j];
-            hv[j] = ub * sWo[ccol + j];
+          for (int j = 0; j < 32; ++j) v[j] = hv[j] * ub;
+          gWo += warp_transpose_sum(v, lane);
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            float a16[16], g16[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              a16[j] = hv[16 * hf + j];
+              g16[j] = ub * sWo[ccol + 16 * hf + j];
+            }
+            stab::stab_bwd<16>(g16, a16, lane);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) hv[16 * hf + j] = g16[j];
           }
-          stab::stab_bwd(hv, a, lane);
         }
       } else {
 #pragma unroll
@@ -815,9 +833,11 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
           hv[j] = 1.0f - hv[j] * hv[j];
         }
       }
+      if (!(STAB && stab && !SST)) {   // (the octet-map branch above formed it already)
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] *= ub;
-      gWo += warp_transpose_sum(v, lane);
+        for (int j = 0; j < 32; ++j) v[j] *= ub;
+        gWo += warp_transpose_sum(v, lane);
+      }
       if (!(STAB && stab)) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) hv[j] *= ub * sWo[ccol + j];
