@@ -114,10 +114,11 @@ __device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.ar
 #ifndef NBM_TCH_OFFSET
 #define NBM_TCH_OFFSET 1
 #endif
-// element (m, k) of a tail A operand ([16][64] bf16, K-major core matrices: k-core stride 256 B,
-// m-group stride 128 B)
+// element (m, k) of a tail A operand ([16 m][64 k] bf16, MN-major core matrices: 8 k-rows x
+// 8 m (16 B) each, k-core stride 256 B, m-group stride 128 B): a row's [1, x, y, z] entries
+// m = 0..7 are one 16-byte store
 __device__ __forceinline__ uint32_t tail_off(int m, int k) {
-  return (uint32_t)((k >> 3) * 256 + (m >> 3) * 128 + (m & 7) * 16 + (k & 7) * 2);
+  return (uint32_t)((k >> 3) * 256 + (m >> 3) * 128 + (k & 7) * 16 + (m & 7) * 2);
 }
 
 }  // namespace
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
   constexpr uint32_t ID_FWD = tc::idesc_bf16(kHR, W, 0, 0);    // A K-major, B K-major
   constexpr uint32_t ID_DH = tc::idesc_bf16(kHR, W, 0, 1);     // A K-major, B MN-major
   constexpr uint32_t ID_DW = tc::idesc_bf16(128, W, 1, 1);     // M = o (padded to 128), both MN-major
-  constexpr uint32_t ID_TAIL = tc::idesc_bf16(kHR, W, 0, 1);   // M = tail rows, N = o
+  constexpr uint32_t ID_TAIL = tc::idesc_bf16(kHR, W, 1, 1);   // M = tail rows (MN-major), N = o
   const uint32_t tAcc = tmem + ((uint32_t)(half * 16) << 16);                      // MMA D of this half
   const uint32_t tMine = tmem + ((uint32_t)(quad * 32 + half * 16) << 16) + (uint32_t)(cg * 64);   // my rows / columns
   uint32_t phase = 0, dwphase = 0;
@@ -426,7 +427,7 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
           sItem[th] = cur.item;
           sAux[th] = cur.aux;
         }
-        sX[4 * th] = cur.x0; sX[4 * th + 1] = cur.x1; sX[4 * th + 2] = cur.x2;
+        *reinterpret_cast<float4*>(sX + 4 * th) = make_float4(cur.x0, cur.x1, cur.x2, 0.0f);
       }
       hsync();
       TRH(0);
@@ -592,15 +593,10 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
           store_row32(buf(0), row, chunk, h);
         }
         if (l == 2 && chunk == 0) {   // tail operand A_1 column `row`: [1, x_hi, x_lo, y_hi, y_lo, z_hi, z_lo, 0]
-          const float xs[3] = {x0, x1, x2};
-          __nv_bfloat16* ta = reinterpret_cast<__nv_bfloat16*>(smem + L::oTailX + half * L::TAILA);
-          ta[tail_off(0, row) / 2] = __float2bfloat16(1.0f);
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const __nv_bfloat16 hi = __float2bfloat16_rn(xs[c]);
-            ta[tail_off(1 + 2 * c, row) / 2] = hi;
-            ta[tail_off(2 + 2 * c, row) / 2] = __float2bfloat16_rn(xs[c] - __bfloat162float(hi));
-          }
+          const float xh = __bfloat162float(__float2bfloat16_rn(x0)), yh = __bfloat162float(__float2bfloat16_rn(x1)),
+                      zh = __bfloat162float(__float2bfloat16_rn(x2));
+          st_shared_v4(aTailX + tail_off(0, row), pack_bf16(1.0f, xh), pack_bf16(x0 - xh, yh), pack_bf16(x1 - yh, zh),
+                       pack_bf16(x2 - zh, 0.0f));
         }
         tc::fence_proxy_async_smem();
         tc::tc_fence_before();
@@ -610,7 +606,7 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
       // ---- tail: [db_1, dW_1 | db_l] = A_1 G_1^T + sum_l A_l G_l^T into the half's accumulator ----
       if (iw) {
         tc::tc_fence_after();
-        gemm(tAcc, aTailX, 512, 256, 128, buf(0), 256, 128, LBO_ACT, ID_TAIL, kHR / 16, false);
+        gemm(tAcc, aTailX, 512, 256, 128, buf(0), 256, 128, LBO_ACT, ID_TAIL, kHR / 16, false);   // A: lbo = k-core, sbo = m-group
         for (int l = 2; l <= NH - 1; ++l)
           gemm(tAcc, aTailO + (l - 2) * L::TAILA, 512, 256, 128, buf(l - 1), 256, 128, LBO_ACT, ID_TAIL, kHR / 16, true);
         tc::mma_commit_w(bar);
