@@ -385,7 +385,10 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       }
     }
     tc::fence_proxy_async_smem();
-    if (warp == 0) wload(net, 2);
+    if (warp == 0) {   // (a forward-only pass may still be prefetching the previous network's W_2)
+      wwait();
+      wload(net, 2);
+    }
 #pragma unroll
     for (int v = 0; v < NT; ++v) tg[v] = 0.0f;
     gWo = gBN = gbo = 0.0f;
@@ -659,7 +662,9 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       }
       if (!TRAIN && l == 2) nxt = fetch(t + 1);   // the next tile's loads overlap this tile
       wait_mma();
-      if (warp == 0 && l < NH) wload(curNet, l + 1);   // prefetch the next layer's weights
+      // prefetch the next layer's weights; a forward-only pass ends the tile on W_NH, so the next
+      // tile's W_2 is loaded here (the training pass reloads it through its backward)
+      if (warp == 0 && (l < NH || !TRAIN)) wload(curNet, l < NH ? l + 1 : 2);
       TR(2 + 2 * (l - 2));
       float v[32];
       const float* bl = sBias + (l - 1) * W + ccol;
@@ -1029,6 +1034,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
       prm.lpart[cta] = s;
     }
   }
+  if (warp == 0) wwait();   // no weight load may outlive the CTA (a forward-only pass prefetches W_2)
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();

@@ -93,6 +93,25 @@ def test_tc_eval_and_determinism(orc):
     s.close()
 
 
+def test_tc_eval_silu_many_tiles(orc):
+    """nbm_eval on the SiLU network (weights streamed through one shared-memory stage) with
+    several 128-row tiles per CTA (2^15 points, 148 CTAs): every tile's forward must start from
+    W_2 again (a stage left holding W_NH after the previous tile would go unnoticed with one
+    tile per CTA).  The bf16 bar against the fp64 oracle, point by point."""
+    cfg = inputs.config("c3")
+    n = 1 << 15
+    s = nbm.Solver(cfg, 0, max_points=n)
+    pb, ar = orc.from_config(cfg)
+    th = orc.init_params(ar, 2)
+    pts = orc.sample(0, 9, 0, 0, n, cfg["H"])
+    s.theta.copy_(_dev(th))
+    u = s.eval(_dev(pts)).double().cpu().numpy()
+    want = orc.evaluate(pb, ar, th, pts)
+    assert np.abs(u - want).max() <= TOL * np.abs(want).max()
+    assert s.status() == 0
+    s.close()
+
+
 def test_tc_full_size_config4(orc):
     """BASELINE config 4 at its full size (2^22 interior + 2^19 boundary points per step) in
     the bench's launch configuration (K3w, CTA pairs).  At this size the fp64 oracle can
