@@ -19,11 +19,14 @@
 //   layer 1 (K = 3, CUDA cores) -> bf16 h1;  l = 2..NH: acc = h_{l-1} W_l^T (M = 64, N = W)
 //   -> tanh -> bf16 h_l;  u = wo . h_NH + bo;  residual epilogue (cotangents 2 r c_j / N);
 //   G_NH = ub wo (1 - h_NH^2);  l = NH..2: acc = G_l W_l (M = 64), dW_l += G_l^T h_{l-1}
-//   (M = W o-rows (128, padded at W = 64), N = W, K = 64: both halves accumulate into the same
-//   TMEM dW_l, zeroed per network);  G_{l-1} = acc (1 - h~^2) in place of h_{l-1}.
+//   (M = W = 128 o-rows, N = W, K = 64: both halves accumulate into the same TMEM dW_l, zeroed
+//   per network, their dW MMAs issued in half-tile order);  G_{l-1} = acc (1 - h~^2) in place
+//   of h_{l-1}; h1 is recomputed (K = 3) for dW_2, its buffer having held G_NH.
 //   Tail: [db_1, dW_1 (x, y, z as hi/lo bf16 planes) | db_l] = A_l G_l^T as M = 64 MMAs into the
-//   half's own accumulator lanes (A_1 = [1, x_hi, x_lo, ...] rows, A_l = a ones row per layer;
-//   rows >= 16 of A are never read back), collected into fp32 shared accumulators.
+//   half's own accumulator lanes (A_1 = [1, x_hi, x_lo, ...] rows, A_l = a ones row per layer,
+//   MN-major; rows >= 16 of A are never read back), collected into fp32 shared accumulators.
+// Half 1 starts after half 0's first hidden GEMM of each network run (named barrier 3) and the
+// stagger persists; started together the halves ran in lock step and K3h was slower than K3t.
 // Warps: 2 halves x 4 lane quadrants x W/64 column groups.  Thread (half, quad, cg, lane):
 // row 16 quad + lane%16 of its half-tile, columns 64 cg + 32 (lane/16) .. +31 (the 16x32bx2
 // TMEM access shape).  Rounding points: as K3t (GEMM operands bf16 RNE, tanh.approx,
@@ -57,7 +60,7 @@ struct HLayout {
   static constexpr int NTP = NTR | 1;                    // their stride per unit o (odd: the 16 row-lanes of a collect hit 16 banks)
   static constexpr uint32_t ACT = kHR * W * 2;           // one bf16 half-tile activation buffer
   static constexpr uint32_t WMAT = W * W * 2;            // one bf16 weight matrix
-  static constexpr uint32_t TAILA = 16 * kHR * 2;        // one tail A operand: [16][64] bf16, K-major
+  static constexpr uint32_t TAILA = 16 * kHR * 2;        // one tail A operand: [16][64] bf16, MN-major
   static constexpr uint32_t oAct = 0;                    // [half][NBUF]
   static constexpr uint32_t oWh = oAct + 2 * NBUF * ACT;  // W_2..W_NH (core-matrix, [o][i])
   static constexpr uint32_t oTailX = oWh + NHH * WMAT;    // [half] A_1 = [1, x, y, z split] rows
