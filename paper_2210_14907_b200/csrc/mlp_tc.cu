@@ -1,8 +1,9 @@
 // mlp_tc.cu -- K3t: the fused MLP forward -> residual epilogue -> backward -> dW kernel
 // with the hidden x hidden GEMMs on the 5th-generation tensor cores (tcgen05, bf16 in,
-// fp32 accumulate in TMEM), configs 3 / 5-w128 (SURVEY 8a S3-S5, 7.3 hard parts 3-5).
+// fp32 accumulate in TMEM), configs 3 / 5-w64 (SURVEY 8a S3-S5, 7.3 hard parts 3-5); the
+// config 5-w128 training pass runs K3h (mlp_tch.cu), the two-half-tile schedule of this kernel.
 //
-// One CTA per SM walks a contiguous range of 128-row tiles (18 stencil points x 7
+// One CTA per SM (two at W = 64) walks a contiguous range of 128-row tiles (18 stencil points x 7
 // vertices, or 128 independent rows).  4 * W/32 warps: warp w owns rows 32*(w%4)..+31
 // (its TMEM lane quadrant) and columns 32*(w/4)..+31 of every activation, so the
 // epilogues are spread over 16 warps at W = 128.  Per tile, for NH hidden layers:
@@ -12,7 +13,7 @@
 //   output layer u = wo . h_NH + bo (per-chunk partials) -> residual epilogue
 //   (r = M^-1 A u - M^-1 b; cotangents 2 r chat_j / N)
 //   backward: G_NH = u_bar wo (1 - h_NH^2);  for l = NH..2:
-//       tcgen05.mma  dW_l += G_l^T h_{l-1}   (M=W, N=W, K=128; dW stays in TMEM for all
+//       tcgen05.mma  dW_l += G_l^T h_{l-1}   (M=W (64: the M = 64 lane layout), N=W, K=128; dW stays in TMEM for all
 //                                             the CTA's tiles and is written out once)
 //       tcgen05.mma  acc   = G_l W_l          (M=128, N=W, K=W)
 //       epilogue G_{l-1} = acc * (1 - h~_{l-1}^2) -> bf16 operand
@@ -21,7 +22,9 @@
 //       gradients: warp transpose-reductions into registers.
 // TMEM columns: [0,W) working accumulator, [W(l-1), W l) dW_l  (W * NH <= 512).
 // Shared memory (W=128, NH=4): 3 bf16 hidden weight matrices + 3 bf16 activation
-// buffers = 192 KB.  h1 is recomputed (K = 3) for dW_2 instead of being kept.
+// buffers = 192 KB.  h1 is recomputed (K = 3) for dW_2 instead of being kept, unless one more
+// activation buffer fits (XBUF) and holds G_NH.  The MMAs are issued by warp 0, converged
+// (elect.sync); the SiLU kernel streams its weights through one TMA stage.
 // Rounding points (G16): GEMM operands bf16 (RNE), accumulators and everything
 // else fp32; tanh' = 1 - h~^2 from the bf16 operand copy for hidden layers 1..NH-1,
 // exact fp32 for layer NH; activation = hardware tanh.approx.f32.
