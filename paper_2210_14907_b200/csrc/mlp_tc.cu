@@ -53,9 +53,11 @@ constexpr int kTPTS = 16;  // stencil points per tile of the stable form (G27): 
 // STG: columns of the fp32 staging tile of the shared-memory stable maps (0: none)
 template <int W, int NH, int ACT, int P = 1, int STG = 0>
 struct TcLayout {
-  static_assert(P == 1 || (P == 3 && ACT == NBM_ACT_TANH), "plane split: tanh with resident weights");
+  static_assert(P == 1 || (P == 3 && ACT == NBM_ACT_TANH), "plane split: tanh");
   static constexpr bool SILU = ACT == NBM_ACT_SILU;
-  static constexpr bool STREAM = SILU;                     // weights streamed (TMA bulk) to make room
+  // weights streamed (TMA bulk) to make room: for SiLU's act' buffers, and for the three-plane
+  // split at four hidden layers (three 48 KB activation buffers)
+  static constexpr bool STREAM = SILU || (P == 3 && NH >= 4);
   static constexpr int NHH = NH - 1;
   static constexpr int NWRES = STREAM ? 1 : NHH;           // weight matrices held in shared memory
   static constexpr int NWRES_() { return STREAM ? 1 : NHH; }
@@ -273,8 +275,9 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
   auto wload = [&](int net, int l) {   // warp 0 only; the stage must be free (no MMA in flight)
     if (!STREAM || (net == wnet && l == wl)) return;
     if (lane == 0) {
-      tc::mbar_arrive_expect_tx(wbar, L::WMAT_BYTES);
-      tc::bulk_copy_g2s(aWh, prm.wimg + ((int64_t)net * NHH + (l - 2)) * W * W, L::WMAT_BYTES, wbar);
+      // the P planes of W_l: the packed image holds [net][l][plane][W x W] (launch_pack_weights)
+      tc::mbar_arrive_expect_tx(wbar, L::WBUF);
+      tc::bulk_copy_g2s(aWh, prm.wimg + ((int64_t)net * NHH + (l - 2)) * P * W * W, L::WBUF, wbar);
     }
     wnet = net;
     wl = l;
@@ -1061,7 +1064,7 @@ extern "C" int nbm_debug_tc_trace(long long* out) {
 #endif
 
 int mlp_tc_supported(int width, int n_hidden, int act, int planes) {
-  if (planes == 3) return width == 64 && n_hidden >= 2 && n_hidden <= 3 && act == NBM_ACT_TANH;
+  if (planes == 3) return width == 64 && n_hidden >= 2 && n_hidden <= 4 && act == NBM_ACT_TANH;
   return (width == 64 || width == 128) && n_hidden >= 2 && n_hidden <= 4 &&
          (act == NBM_ACT_TANH || act == NBM_ACT_SILU);
 }
@@ -1114,6 +1117,7 @@ cudaError_t launch_mlp_tc(int width, int n_hidden, int act, int planes, bool tra
     switch (n_hidden) {
       case 2: return train ? launch_tc_t<64, 2, NBM_ACT_TANH, true, 3>(p, grid, s) : launch_tc_t<64, 2, NBM_ACT_TANH, false, 3>(p, grid, s);
       case 3: return train ? launch_tc_t<64, 3, NBM_ACT_TANH, true, 3>(p, grid, s) : launch_tc_t<64, 3, NBM_ACT_TANH, false, 3>(p, grid, s);
+      case 4: return train ? launch_tc_t<64, 4, NBM_ACT_TANH, true, 3>(p, grid, s) : launch_tc_t<64, 4, NBM_ACT_TANH, false, 3>(p, grid, s);
     }
     return cudaErrorInvalidValue;
   }
@@ -1121,24 +1125,31 @@ cudaError_t launch_mlp_tc(int width, int n_hidden, int act, int planes, bool tra
                              : launch_tc_act<NBM_ACT_TANH>(width, n_hidden, train, p, grid, s);
 }
 
-// bf16 image of the hidden weights in the tensor-core core-matrix layout ([o][i], R = W):
-// element (o, i) of W_l (net k) at ((k*(NH-1) + l-2)*W*W) + (i/8)*W*8 + o*8 + i%8.
-__global__ void k_pack_weights(const float* __restrict__ theta, int64_t p_net, int W, int nhh, int n_nets,
+// bf16 image of the hidden weights in the tensor-core core-matrix layout ([o][i], R = W), in
+// `planes` exact bf16 planes (1: the RNE copy; 3: the split of PREC_FP32X, plane p = bf16 of
+// what the planes before it leave): element (o, i) of plane p of W_l (net k) at
+// ((k*(NH-1) + l-2)*planes + p)*W*W + (i/8)*W*8 + o*8 + i%8.
+__global__ void k_pack_weights(const float* __restrict__ theta, int64_t p_net, int W, int nhh, int n_nets, int planes,
                                uint16_t* __restrict__ wimg) {
   const int64_t total = (int64_t)n_nets * nhh * W * W;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = e / ((int64_t)W * W);
     const int net = (int)(m / nhh), l = (int)(m % nhh) + 2;
     const int r = (int)(e % ((int64_t)W * W)), o = r / W, i = r % W;
-    const float v = theta[(int64_t)net * p_net + 4 * W + (int64_t)(l - 2) * (W * W + W) + r];
-    wimg[m * W * W + (int64_t)(i / 8) * W * 8 + o * 8 + (i % 8)] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    float v = theta[(int64_t)net * p_net + 4 * W + (int64_t)(l - 2) * (W * W + W) + r];
+    for (int p = 0; p < planes; ++p) {
+      const __nv_bfloat16 b = __float2bfloat16_rn(v);
+      wimg[(m * planes + p) * W * W + (int64_t)(i / 8) * W * 8 + o * 8 + (i % 8)] = __bfloat16_as_ushort(b);
+      v -= __bfloat162float(b);   // exact: the rounding error of a bf16 rounding is an fp32
+    }
   }
 }
 
 cudaError_t launch_pack_weights(const ArchInfo& a, const float* theta, uint16_t* wimg, cudaStream_t s) {
   const int nhh = a.n_hidden - 1;
   if (nhh <= 0) return cudaSuccess;
-  k_pack_weights<<<148 * 4, 256, 0, s>>>(theta, a.p_net, a.width, nhh, a.n_nets, wimg);
+  const int planes = a.prec == NBM_PREC_FP32X ? 3 : 1;
+  k_pack_weights<<<148 * 4, 256, 0, s>>>(theta, a.p_net, a.width, nhh, a.n_nets, planes, wimg);
   return cudaGetLastError();
 }
 

@@ -244,6 +244,7 @@ cudaError_t launch_pack(const nbm_handle* h, const float* theta, cudaStream_t s)
   const ArchInfo& A = h->arch;
   const Workspace& w = h->ws;
   if (is_fp32w(A)) return launch_pack_fp32w(A, theta, w.wimg32, s);
+  if (A.prec == NBM_PREC_FP32X) return launch_pack_weights(A, theta, w.wimg, s);   // three planes (streamed at NH = 4)
   if (A.prec != NBM_PREC_BF16) return cudaSuccess;
   return is_w256(A) ? launch_pack_w256(A, theta, w.wimg, w.wimg_b, s) : launch_pack_weights(A, theta, w.wimg, s);
 }
@@ -370,7 +371,7 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   ALLOC(w.epart, (size_t)2 * kErrBlocks * sizeof(double));
   ALLOC(w.bc, 2 * sizeof(float));
   const size_t nhh = ai.n_hidden > 1 ? ai.n_hidden - 1 : 1;
-  ALLOC(w.wimg, (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t));
+  ALLOC(w.wimg, (size_t)2 * nhh * ai.width * ai.width * (ai.prec == NBM_PREC_FP32X ? 3 : 1) * sizeof(uint16_t));
   const bool w256 = is_w256(ai), fw = is_fp32w(ai), urep = uses_rep(ai);
   w.nrep = urep ? 16 : 0;   // gradient replicas (fewer CTAs per L2 address)
   if (urep && getenv("NBM_W256_REPLICAS")) w.nrep = atoi(getenv("NBM_W256_REPLICAS"));
@@ -505,7 +506,7 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
   if (ev) cudaEventRecord(ev[0], s);
   cudaError_t e = launch_classify(h, pts_dev, n, bpts_dev, nb, H, dm, dpl, terms, false, s);
   launches += 3;
-  if (e == cudaSuccess && pack && (A.prec == NBM_PREC_BF16 || is_fp32w(A))) {
+  if (e == cudaSuccess && pack && (A.prec == NBM_PREC_BF16 || A.prec == NBM_PREC_FP32X || is_fp32w(A))) {
     e = launch_pack(h, theta_dev, s);
     launches += 1;
   }

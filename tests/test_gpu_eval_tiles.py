@@ -26,7 +26,8 @@ CASES = [
     ("c5", 64, None, 5e-2),                    # K3t W = 64, two CTAs per SM
     ("c5", 128, inputs.PREC_FP32, 1e-5),       # K3fw W = 128, streamed fp32 weights
     ("c5", 256, inputs.PREC_FP32, 1e-5),       # K3fw W = 256
-    ("c2", 64, inputs.PREC_FP32X, 1e-5),       # FP32X split planes
+    ("c2", 64, inputs.PREC_FP32X, 1e-5),       # FP32X split planes (resident weights)
+    ("c5", 64, inputs.PREC_FP32X, 1e-5),       # FP32X at four hidden layers (streamed planes)
     ("c2", 64, inputs.PREC_FP32, 1e-5),        # K3f
 ]
 
