@@ -131,7 +131,7 @@ typedef struct nbm_problem {
  *              W in {128, 256} with 2..4;
  *   FP32 sine: W <= 32 with 1..5 hidden layers (the paper's 5 x 10 nets);
  *   BF16 (tcgen05): W in {64, 128} tanh or SiLU, W = 256 tanh, 2..4 hidden layers;
- *   FP32X (tcgen05, three bf16 planes): W = 64 tanh, 2..3 hidden layers.
+ *   FP32X (tcgen05, three bf16 planes): W = 64 tanh, 2..4 hidden layers (4: streamed weights).
  * Variable mu (nbm_problem.mu_kind) runs on every direct-form kernel except FP32X.  stencil =
  * NBM_STENCIL_STABLE needs tanh with FP32 or BF16 (any of the widths above) and constant mu. */
 typedef struct nbm_arch {
