@@ -373,7 +373,10 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   const size_t nhh = ai.n_hidden > 1 ? ai.n_hidden - 1 : 1;
   ALLOC(w.wimg, (size_t)2 * nhh * ai.width * ai.width * (ai.prec == NBM_PREC_FP32X ? 3 : 1) * sizeof(uint16_t));
   const bool w256 = is_w256(ai), fw = is_fp32w(ai), urep = uses_rep(ai);
-  w.nrep = urep ? 16 : 0;   // gradient replicas (fewer CTAs per L2 address)
+  // gradient replicas in L2 (fewer CTAs per address): K3w measured fastest with one (c4: 64.2 vs
+  // 64.8 ms per launch with 16; its smaller L2 footprint outweighs the address sharing,
+  // scripts/r2/exp_rep.sh), K3fw keeps 16
+  w.nrep = urep ? (w256 ? 1 : 16) : 0;
   if (urep && getenv("NBM_W256_REPLICAS")) w.nrep = atoi(getenv("NBM_W256_REPLICAS"));
   ALLOC(w.wimg_b, w256 ? (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t) : 16);
   ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * (nhh + 2) * 128 * ai.width * 2 : 16);   // parks: NH + 1 tiles per CTA (mlp_w256.cu kScr)
