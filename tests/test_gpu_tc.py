@@ -245,3 +245,26 @@ def test_tc_ragged_and_empty(orc, name, w, nh):
     assert gl == 0.0 and np.all(gg == 0.0)
     assert s.status() == 0
     s.close()
+
+
+@pytest.mark.parametrize("w", [64, 128, 256])
+def test_tc_single_network_no_interface(orc, w):
+    """Config 1's problem (no interface: one network, no crossed rows, the sin(3 pi) source) on
+    the bf16 kernels (K3t W = 64, K3h W = 128, K3w W = 256): a single network run per CTA, the
+    crossed-row passes skipped.  Totals at the bf16 bar against fp64 and 3e-3 against the bf16
+    emulation, at h = 1/16 where the uncrossed residual is resolved in bf16."""
+    cfg = inputs.config("c1")
+    cfg.update(sizes=[3, w, w, w, w, 1], prec=inputs.PREC_BF16, H=inputs.h_lattice(1 / 16))
+    n, nb = 1 << 12, 1 << 9
+    s = nbm.Solver(cfg, 0, max_points=n)
+    pb, ar = orc.from_config(cfg)
+    th = orc.init_params(ar, 1)
+    pts = orc.sample(0, 3, 0, 0, n, cfg["H"])
+    b = orc.sample(1, 3, 0, 0, nb, cfg["H"])
+    L, _, g, _ = orc.loss_grad(pb, ar, th, pts, b, cfg["H"] / 2**24)
+    Le, _, ge, _ = orc.loss_grad(pb, ar, th, pts, b, cfg["H"] / 2**24, mode=orc.MODE_BF16)
+    gl, gg = _run(s, _dev(th), _dev(pts), _dev(b))
+    assert abs(gl - L) <= TOL * L and np.linalg.norm(gg - g) <= TOL * np.linalg.norm(g)
+    assert abs(gl - Le) <= EMU_TOL * Le and np.linalg.norm(gg - ge) <= EMU_TOL * np.linalg.norm(ge)
+    assert s.status() == 0
+    s.close()
