@@ -1,0 +1,8 @@
+# experiment (tooling): pipelined K3w forward with and without weight-slice loads (timing only)
+mkdir -p gpurun_out/r2
+for v in base sfl; do
+  L=$PWD/paper_2210_14907_b200/libnbm.so
+  [ $v = sfl ] && L=$PWD/paper_2210_14907_b200/libnbm_sfl.so
+  NBM_LIB=$L timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-secondary --steps 20 > gpurun_out/r2/sfl_$v.log 2>&1
+  echo "$v $(tail -1 gpurun_out/r2/sfl_$v.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["ms_per_step"], d["roofline"]["avg_launch_ms"])')"
+done
