@@ -57,8 +57,8 @@ struct Lay {
   static constexpr uint32_t oAux = oUb + 4 * kB;
   static constexpr uint32_t oItem = oAux + 4 * kB;
   static constexpr uint32_t oSG = oItem + 4 * kB;         // fp32 [NH + 4][W] small gradients + b_o
-  static constexpr uint32_t oBar = oSG + 4 * ((NH + 4) * W + 4);   // full[4], empty[4], mma, dw, ld, park, ready[4] + tmem base
-  static constexpr uint32_t bytes = oBar + 160;
+  static constexpr uint32_t oBar = oSG + 4 * ((NH + 4) * W + 4);   // full[4], empty[4], mma, dw, ld, park + tmem base
+  static constexpr uint32_t bytes = oBar + 128;
   static_assert(bytes <= 227 * 1024, "shared memory");
   static constexpr int kScr = NH + 1;                     // parked tiles per CTA: h_1..h_{NH-1}, G x2
   static constexpr int64_t tW1 = 0, tB1 = 3 * W;
@@ -262,8 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   uint64_t* bdw = bfull + 9;
   uint64_t* bld = bfull + 10;
   uint64_t* bpark = bfull + 11;   // the peer's parked G_l (and h) are complete in global memory
-  uint64_t* bready = bfull + 12;  // [4] K-slice s of the next forward GEMM's A tile is written (both CTAs)
-  uint32_t* sTmem = reinterpret_cast<uint32_t*>(smem + L::oBar + 144);
+  uint32_t* sTmem = reinterpret_cast<uint32_t*>(smem + L::oBar + 112);
   __shared__ int segPairs[kNumSeg], segCnt[kNumSeg], segStart[kNumSeg];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -288,7 +287,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     tc::mbar_init(bdw, 1);
     tc::mbar_init(bld, leader ? 2 : 1);
     tc::mbar_init(bpark, 1);
-    for (int s = 0; s < 4; ++s) tc::mbar_init(bready + s, leader ? kThreads / 32 + 1 : kThreads / 32);   // + the peer
     tc::mbar_fence_init();
   }
   if (warp == 0) tc::tmem_alloc2(sTmem, 512);
@@ -314,7 +312,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   auto hslot = [&](int j) -> int64_t { return (int64_t)(j - 1) * ACT; };                 // h_j, j in 1..NH-1
   auto gslot = [&](int l) -> int64_t { return (int64_t)(NH - 1 + (l & 1)) * ACT; };     // G_l
   uint32_t ph_full[kStages] = {0, 0, 0, 0}, ph_empty[kStages] = {0, 0, 0, 0};
-  uint32_t ph_mma = 0, ph_dw = 0, ph_ld = 0, ph_park = 0, ph_ready[4] = {0, 0, 0, 0};
+  uint32_t ph_mma = 0, ph_dw = 0, ph_ld = 0, ph_park = 0;
   bool ringUsed = false;
   int gcount = 0, qcount = 0;   // GEMMs issued / queued (trace)
 
@@ -331,9 +329,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
         tc::mbar_wait(bempty + s, ph_empty[s]);
         ph_empty[s] ^= 1;
       }
-#ifdef NBM_W256_NO_WLOAD   // timing only: stale weights after the first tiles
-      if (qcount >= 12) { tc::mbar_arrive(bfull + s); continue; }
-#endif
       tc::mbar_arrive_expect_tx(bfull + s, HSLICE);
       tc::bulk_copy_g2s(ring + s * HSLICE, base + (int64_t)(s * 2 + rank) * (HSLICE / 2), HSLICE, bfull + s);
 #ifdef NBM_TC_TRACE
@@ -370,40 +365,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     ringUsed = true;
     ++gcount;
   };
-  // forward GEMM K-slice s, issued as soon as columns [64 s, 64 s + 64) of its A tile are written in
-  // both CTAs (bready: the 16 warps of this CTA, + the peer's forward at the leader) and the slice's
-  // weights have landed; `last`: commit bmma.  Before the last slice each CTA's parked copies have
-  // left the tiles (the epilogue after bmma overwrites one of them).
-  auto issue_slice = [&](int s, uint32_t a0, uint32_t dacc, bool last) {
-    tc::mbar_wait(bready + s, ph_ready[s]);
-    ph_ready[s] ^= 1;
-    if (last && TRAIN) tc::bulk_wait_read0();
-    if (!leader) tc::arrive_leader(bready + s);
-    tc::mbar_wait(bfull + s, ph_full[s]);
-    ph_full[s] ^= 1;
-    if (!leader) {
-      tc::arrive_leader(bfull + s);
-      return;
-    }
-    tc::tc_fence_after();
-    const uint32_t wb = ring + s * HSLICE;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int kk = s * 4 + k;
-      tc::mma2_bf16(tmem + dacc, tc::sdesc(a0 + kk * 2 * LBO_ACT, LBO_ACT, 128), tc::sdesc(wb + k * 4096, 2048, 128),
-                    tc::idesc_bf16(2 * kB, W, 0, 0), kk > 0 ? 1u : 0u);
-    }
-    tc::mma2_commit(bempty + s);
-    if (last) tc::mma2_commit(bmma);
-  };
   auto wait_bar = [&](uint64_t* b, uint32_t& ph) {
     tc::mbar_wait(b, ph);
     ph ^= 1;
     tc::tc_fence_after();
   };
 
-  // TMEM column of the last hidden layer's accumulator (the pipelined forward alternates halves)
-  constexpr uint32_t accNH = STAB ? 0u : (uint32_t)(((NH - 2) & 1) * 256);
   constexpr uint32_t ID_FWD = tc::idesc_bf16(2 * kB, W, 0, 0);
   constexpr uint32_t ID_DH = tc::idesc_bf16(2 * kB, W, 0, 1);
   constexpr uint32_t ID_DW = tc::idesc_bf16(2 * kB, W, 1, 1);
@@ -592,140 +559,72 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     }
     TRW(1);
     // ---- forward hidden layers ----
-    if constexpr (!STAB) {
-      // Direct form, pipelined: K-slice s of GEMM l + 1 is issued as soon as every warp of both CTAs
-      // has written columns [64 s, 64 s + 64) of h_l, so the epilogue of layer l overlaps GEMM l + 1;
-      // GEMM l accumulates in TMEM [256 ((l - 2) & 1), + 256), alternating with the layer before.
-      // The previous tile's dW_2 (TMEM [256, 512)) is flushed under GEMM 2, before GEMM 3 reuses it.
-      if (tid == 0) issue_gemm(aBuf[0], false, ID_FWD);
-      nxt = fetch(u + 1);   // the next tile's loads overlap this tile
+    for (int l = 2; l <= NH; ++l) {
+      if (tid == 0) issue_gemm(aBuf[(l - 2) & 1], false, ID_FWD);
+      if (l == 3) TRW(24);
+      if (l == 2) nxt = fetch(u + 1);  // the next tile's loads overlap this tile
+      // the previous tile's dW_2 under this tile's forward GEMMs: split over the last two (the first
+      // one's weight slices are still arriving, and the flush's writes hold up their reads)
+#ifndef NBM_W256_FLUSH_AT_L2
+      if (TRAIN && pend) {
+        if (NH >= 4 && l == NH - 1) flush_dw_part(0, 1);
+        else if (NH >= 4 && l == NH) flush_dw_part(1, 2);
+        else if (NH < 4 && l == NH) flush_dw();
+      }
+#else
       if (TRAIN && pend) flush_dw();
-      if (tid == 0) {
-        if (NH > 2) queue_gemm(false, net, 3);
+#endif
+      if (tid == 0) {                  // the next GEMM's slices
+        if (l < NH) queue_gemm(false, net, l + 1);
         else if (TRAIN) queue_gemm(true, net, NH);
         else if (nextNet >= 0) queue_gemm(false, nextNet, 2);
       }
-      for (int l = 2; l < NH; ++l) {
-        const uint32_t accIn = (uint32_t)(((l - 2) & 1) * 256), accOut = 256u - accIn;
-        const uint32_t hbuf = aBuf[(l - 1) & 1];
-        wait_bar(bmma, ph_mma);
-        TRW(2 + 2 * (l - 2));
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {   // unrolled: the phase arrays stay in registers
-          const int col = 64 * s + 16 * cg;   // this warp's 16 columns of K-slice s
-          float v[16];
-          tc::tmem_ld16(tmem + tlane + accIn + (uint32_t)col, v);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = th(v[j] + sBias[(l - 1) * W + col + j]);
-#pragma unroll
-          for (int qq = 0; qq < 2; ++qq)
-            sts4(hbuf + (uint32_t)((col / 8 + qq) * LBO_ACT + row * 16), pk(v[8 * qq], v[8 * qq + 1]),
-                 pk(v[8 * qq + 2], v[8 * qq + 3]), pk(v[8 * qq + 4], v[8 * qq + 5]), pk(v[8 * qq + 6], v[8 * qq + 7]));
-          tc::fence_proxy_async_smem();
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(bready + s);
-          if (tid == 0) issue_slice(s, hbuf, accOut, s == 3);
-        }
-        if (tid == 0) {
-          if (TRAIN) {   // park h_l (every warp of this CTA has written it: bready[3])
-            tc::bulk_copy_s2g(myScr + hslot(l), hbuf, ACT);
-            tc::bulk_commit();
-          }
-          if (l + 1 < NH) queue_gemm(false, net, l + 2);
-          else if (TRAIN) queue_gemm(true, net, NH);
-          else if (nextNet >= 0) queue_gemm(false, nextNet, 2);
-        }
-        TRW(3 + 2 * (l - 2));
-      }
-      // the last hidden layer: u = w_o h_NH (+ b_o below); h_NH back into TMEM for the backward
+      if (l == 3) TRW(25);
       if (TRAIN && tid == 0) tc::bulk_wait_read0();   // parked copies have left the tiles
       wait_bar(bmma, ph_mma);
-      TRW(2 + 2 * (NH - 2));
+      TRW(2 + 2 * (l - 2));
       float up = 0.0f;
-      for (int k = 0; k < 2; ++k) {
+      if (STAB && stab) for (int k = 0; k < 2; ++k) {   // stable form: 16-column halves
+        const int c = 2 * cg + k;
+        for (int hf = 0; hf < 2; ++hf) {
+          const uint32_t col = (uint32_t)(c * 32 + hf * 16);
+          float v[16];
+          tc::tmem_ld16(tmem + tlane + col, v);
+          stab::stab_fwd<16>(v, sBias + (l - 1) * W + col, lane);
+          if (l < NH) {
+            put_half(aBuf[(l - 1) & 1], row, c, hf, v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) up = fmaf(sWo[col + j], v[j], up);
+            tc::tmem_st16(tmem + tlane + col, v);
+          }
+        }
+      }
+      if (!(STAB && stab)) for (int k = 0; k < 2; ++k) {
         const int c = 2 * cg + k;
         float v[32];
-        tc::tmem_ld32(tmem + tlane + accNH + (uint32_t)(c * 32), v);
+        tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = th(v[j] + sBias[(NH - 1) * W + c * 32 + j]);
+        for (int j = 0; j < 32; ++j) v[j] = th(v[j] + sBias[(l - 1) * W + c * 32 + j]);
+        if (l < NH) {
+          put_chunk(aBuf[(l - 1) & 1], nullptr, row, c, v);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) up = fmaf(sWo[c * 32 + j], v[j], up);
-        if (TRAIN) tc::tmem_st32(tmem + tlane + accNH + (uint32_t)(c * 32), v);
+          for (int j = 0; j < 32; ++j) up = fmaf(sWo[c * 32 + j], v[j], up);
+          if (TRAIN) tc::tmem_st32(tmem + tlane + (uint32_t)(c * 32), v);
+        }
       }
-      sUp[cg * kB + row] = up;
+      if (l == NH) sUp[cg * kB + row] = up;
       tc::tc_fence_before();
+      if (l < NH) tc::fence_proxy_async_smem();
       __syncthreads();
+      if (l < NH) tc::cluster_sync_relaxed();
       tc::tc_fence_after();
-      TRW(3 + 2 * (NH - 2));
-    } else {
-      for (int l = 2; l <= NH; ++l) {
-        if (tid == 0) issue_gemm(aBuf[(l - 2) & 1], false, ID_FWD);
-        if (l == 3) TRW(24);
-        if (l == 2) nxt = fetch(u + 1);  // the next tile's loads overlap this tile
-        // the previous tile's dW_2 under this tile's forward GEMMs: split over the last two (the first
-        // one's weight slices are still arriving, and the flush's writes hold up their reads)
-  #ifndef NBM_W256_FLUSH_AT_L2
-        if (TRAIN && pend) {
-          if (NH >= 4 && l == NH - 1) flush_dw_part(0, 1);
-          else if (NH >= 4 && l == NH) flush_dw_part(1, 2);
-          else if (NH < 4 && l == NH) flush_dw();
-        }
-  #else
-        if (TRAIN && pend) flush_dw();
-  #endif
-        if (tid == 0) {                  // the next GEMM's slices
-          if (l < NH) queue_gemm(false, net, l + 1);
-          else if (TRAIN) queue_gemm(true, net, NH);
-          else if (nextNet >= 0) queue_gemm(false, nextNet, 2);
-        }
-        if (l == 3) TRW(25);
-        if (TRAIN && tid == 0) tc::bulk_wait_read0();   // parked copies have left the tiles
-        wait_bar(bmma, ph_mma);
-        TRW(2 + 2 * (l - 2));
-        float up = 0.0f;
-        if (STAB && stab) for (int k = 0; k < 2; ++k) {   // stable form: 16-column halves
-          const int c = 2 * cg + k;
-          for (int hf = 0; hf < 2; ++hf) {
-            const uint32_t col = (uint32_t)(c * 32 + hf * 16);
-            float v[16];
-            tc::tmem_ld16(tmem + tlane + col, v);
-            stab::stab_fwd<16>(v, sBias + (l - 1) * W + col, lane);
-            if (l < NH) {
-              put_half(aBuf[(l - 1) & 1], row, c, hf, v);
-            } else {
-  #pragma unroll
-              for (int j = 0; j < 16; ++j) up = fmaf(sWo[col + j], v[j], up);
-              tc::tmem_st16(tmem + tlane + col, v);
-            }
-          }
-        }
-        if (!(STAB && stab)) for (int k = 0; k < 2; ++k) {
-          const int c = 2 * cg + k;
-          float v[32];
-          tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
-  #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = th(v[j] + sBias[(l - 1) * W + c * 32 + j]);
-          if (l < NH) {
-            put_chunk(aBuf[(l - 1) & 1], nullptr, row, c, v);
-          } else {
-  #pragma unroll
-            for (int j = 0; j < 32; ++j) up = fmaf(sWo[c * 32 + j], v[j], up);
-            if (TRAIN) tc::tmem_st32(tmem + tlane + (uint32_t)(c * 32), v);
-          }
-        }
-        if (l == NH) sUp[cg * kB + row] = up;
-        tc::tc_fence_before();
-        if (l < NH) tc::fence_proxy_async_smem();
-        __syncthreads();
-        if (l < NH) tc::cluster_sync_relaxed();
-        tc::tc_fence_after();
-        if (TRAIN && l < NH && tid == 0) {   // park h_l
-          tc::bulk_copy_s2g(myScr + hslot(l), aBuf[(l - 1) & 1], ACT);
-          tc::bulk_commit();
-        }
-        TRW(3 + 2 * (l - 2));
+      if (TRAIN && l < NH && tid == 0) {   // park h_l
+        tc::bulk_copy_s2g(myScr + hslot(l), aBuf[(l - 1) & 1], ACT);
+        tc::bulk_commit();
       }
+      TRW(3 + 2 * (l - 2));
     }
     if (tid < kB) {
       const float uu = ((sUp[tid] + sUp[kB + tid]) + sUp[2 * kB + tid]) + sUp[3 * kB + tid] +
@@ -825,7 +724,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     if (!(STAB && stab)) for (int k = 0; k < 2; ++k) {
       const int c = 2 * cg + k;
       float hv[32], v[32];
-      tc::tmem_ld32(tmem + tlane + accNH + (uint32_t)(c * 32), hv);
+      tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), hv);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = ub * hv[j];
 #pragma unroll
@@ -852,14 +751,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
     for (int l = NH; l >= 2; --l) {
       if (tid == 0) issue_gemm(gb, true, ID_DH);   // acc = G_l W_l
       TRW(26 + 3 * (NH - l));
-#ifdef NBM_W256_SPLIT_FLUSH
-      // dW_{l+1}: its first column half under the dH GEMM, the second between the epilogue's chunks
-      const bool splitFl = pend && !(STAB && stab);
-      if (pend) flush_dw_part(0, splitFl ? 1 : 2);
-#else
-      const bool splitFl = false;
       if (pend) flush_dw();            // dW_{l+1} under the dH GEMM
-#endif
       if (tid == 0) {
         if (l > 2) queue_gemm(true, net, l - 1);
         else if (nextNet >= 0) queue_gemm(false, nextNet, 2);
@@ -875,14 +767,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
         ph_park ^= 1;
         // the dW operands: h_{l-1}[rows of CTA t][this CTA's input half], t = 0, 1, and
         // G_l[rows of the peer][the outputs this CTA owns] (its own rows' block is in place)
-#ifndef NBM_W256_NO_DW   // (timing-only build: no dW MMA, flush or operand loads)
         tc::mbar_arrive_expect_tx(bld, 3 * QTR);
         for (int t = 0; t < 2; ++t) {
           const uint8_t* scr = pairScr0 + (int64_t)t * L::kScr * ACT + rank * QTR;
           tc::bulk_copy_g2s(hb + t * QTR, scr + hslot(l - 1), QTR, bld);
           if (t != (int)rank) tc::bulk_copy_g2s(gb + t * QTR, scr + gslot(l), QTR, bld);
         }
-#endif
       }
       TRW(28 + 3 * (NH - l));
       TRW(11 + 4 * (NH - l));
@@ -931,7 +821,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
         if (l - 1 >= 2) tc::tmem_st16u(stash + 16u * k, pkd);
       }
       if (!(STAB && stab)) for (int k = 0; k < 2; ++k) {
-        if (k == 1 && splitFl) flush_dw_part(1, 2);
         const int c = 2 * cg + k;
         float v[32], hq[32];
         tc::tmem_ld32(tmem + tlane + (uint32_t)(c * 32), v);
@@ -956,7 +845,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
       tc::tc_fence_before();
       __syncthreads();   // this CTA's TMEM reads (flush, epilogue) are done
       TRW(12 + 4 * (NH - l));
-#ifndef NBM_W256_NO_DW
       if (tid == 0) {
         tc::mbar_wait(bld, ph_ld);   // own halves landed (+ the peer's forward, leader)
         ph_ld ^= 1;
@@ -972,7 +860,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
           tc::mma2_commit(bdw);
         }
       }
-#endif
       // the next tile's gather and layer 1 under dW_2 (same network, direct form): h_1 bf16 into this
       // warp's accumulator columns (free at l = 2), copied to tile 0 once dW_2 has released it
       if (!STAB && TRAIN && l == 2 && nextNet == net) {
@@ -994,16 +881,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
         tc::tc_fence_before();
         h1Staged = true;
       }
-#ifndef NBM_W256_NO_DW
       wait_bar(bdw, ph_dw);
-#endif
       // both CTAs' bulk loads of h_{l-1} and G_l (and this CTA's act' reads) are complete: the
       // parked copies are dead, so they leave L2 without a write-back to HBM
       discard_l2(myScr + hslot(l - 1) + tid * 128);
       if (tid < kThreads / 2) discard_l2(myScr + gslot(l) + (rank ^ 1u) * QTR + tid * 128);
-#ifndef NBM_W256_NO_DW
       pend = true;
-#endif
       pendNet = net;
       pendL = l;
       TRW(13 + 4 * (NH - l));

@@ -1,4 +1,5 @@
 # experiment (tooling): K3w with the dW MMAs, their operand loads and the dW flush removed
+# (the build flags NBM_W256_NO_DW / NO_WLOAD / SPLIT_FLUSH and the pipelined forward exist in commit 2b2a58a only)
 # (timing only; gradients wrong) -- what the fused kernel would cost with dW computed elsewhere
 mkdir -p gpurun_out/r2
 for v in base nodw; do

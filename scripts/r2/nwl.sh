@@ -1,4 +1,5 @@
 # experiment (tooling): pipelined K3w forward with and without weight-slice loads (timing only)
+# (the build flags NBM_W256_NO_DW / NO_WLOAD / SPLIT_FLUSH and the pipelined forward exist in commit 2b2a58a only)
 mkdir -p gpurun_out/r2
 for v in base sfl; do
   L=$PWD/paper_2210_14907_b200/libnbm.so
