@@ -1,4 +1,4 @@
-"""Config 3 on the CUDA path against a closed form (tests/_c3_case.py), not the oracle: at
+"""Config 3 on the CUDA path against a closed form (tests/_zero_theta.py), not the oracle: at
 theta = 0 every network value is 0, so the loss is mean (f(p) h^2 / (6 beta_s))^2 over points
 whose stencils do not cross the star (G2, G13).  Config 3's own network
 (3-128^4-1 SiLU, bf16: K3t) and a 3-64-64-1 SiLU one (SiLU runs on the bf16 kernels only).  The GPU forms f in fp32 (expf) and
@@ -9,7 +9,7 @@ import torch
 
 from paper_2210_14907_b200 import inputs, nbm
 
-import _c3_case
+import _zero_theta
 
 pytestmark = pytest.mark.gpu
 
@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("sizes,prec", [([3, 128, 128, 128, 128, 1], inputs.PREC_BF16),
                                         ([3, 64, 64, 1], inputs.PREC_BF16)])
 def test_config3_zero_theta_loss_closed_form(sizes, prec):
-    cfg, pts, b, h, r, inside, _ = _c3_case.case(sizes, prec)
+    cfg, pts, b, h, r, inside, _ = _zero_theta.case_c3(sizes, prec)
     cfg["H"] = inputs.h_lattice(h)
     assert cfg["H"] / 2**24 == h
     s = nbm.Solver(cfg, 0, max_points=len(pts))
