@@ -51,3 +51,28 @@ def test_eval_many_tiles_per_cta(orc, name, w, prec, tol):
         assert e_emu <= 2e-2, e_emu
     assert s.status() == 0
     s.close()
+
+
+def test_eval_full_size_config4_sampled(orc):
+    """nbm_eval at config 4's full size (2^22 interior points, the bench's --eval launch) on
+    K3w, checked on 3000 sampled points one by one (bars as above)."""
+    cfg = inputs.config("c4")
+    n = 1 << 22
+    s = nbm.Solver(cfg, 0, max_points=n)
+    s.init_params(5)
+    pb, ar = orc.from_config(cfg)
+    th = s.theta.double().cpu().numpy()
+    pts = torch.empty(n, 3, device="cuda")
+    s.sample(nbm.POINTS_INTERIOR, 7, 3, 0, n, pts)
+    u = s.eval(pts).double().cpu().numpy()
+    idx = np.random.default_rng(0).choice(n, 3000, replace=False)
+    idx = np.concatenate([idx, [0, n - 1]])
+    sp = pts.cpu().numpy()[idx]
+    assert np.array_equal(sp, orc.sample(0, 7, 3, 0, n, cfg["H"])[idx])   # the sampled inputs
+    want = orc.evaluate(pb, ar, th, sp)
+    assert np.abs(u[idx] - want).max() / np.abs(want).max() <= 5e-2
+    emu = orc.evaluate(pb, ar, th, sp, mode=orc.MODE_BF16)
+    assert np.abs(u[idx] - emu).max() / np.abs(emu).max() <= 2e-2
+    assert np.all(np.isfinite(u))
+    assert s.status() == 0
+    s.close()
