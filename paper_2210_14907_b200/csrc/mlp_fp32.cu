@@ -18,6 +18,7 @@
 
 #include "nbm_internal.cuh"
 #include "stab.cuh"
+#include "tc_ptx.cuh"   // NBM_CHECK (bounds-checked builds)
 
 namespace nbm {
 
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
   };
   auto flush = [&](int net) {
     float* out = prm.part + ((int64_t)net * G + cta) * prm.p_stride;
+    NBM_CHECK(((int64_t)net * G + cta + 1) * prm.p_stride <= prm.part_len);
     const int t = tid & 255, half = tid >> 8;
     const int to = t >> 4, ti = t & 15;
     float* scr = sAct;   // free between tiles: [256][NHH][DB*DB] partials of the second row-half

@@ -18,6 +18,7 @@
 
 #include "nbm_internal.cuh"
 #include "stab.cuh"
+#include "tc_ptx.cuh"   // NBM_CHECK (bounds-checked builds)
 
 namespace nbm {
 
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(kThr, 1) k_mlp_fp32w(const MlpParams prm, cons
   const int G = gridDim.x, cta = blockIdx.x;
   const int t0 = (int)((int64_t)total * cta / G), t1 = (int)((int64_t)total * (cta + 1) / G);
   float* myRep = rep + (int64_t)(cta % nrep) * 2 * prm.p_stride;
+  NBM_CHECK((int64_t)(cta % nrep + 1) * 2 * prm.p_stride <= prm.rep_len);
 
   // ---- weight stream: slices of [KS][W] through a 2-deep ring ----
   const uint32_t slBase = (uint32_t)__cvta_generic_to_shared(sSl);

@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
 
   auto flush = [&](int net) {
     float* out = prm.part + ((int64_t)net * G + cta) * prm.p_stride;
+    NBM_CHECK(((int64_t)net * G + cta + 1) * prm.p_stride <= prm.part_len);
     if (!dwFresh) {
       tc::tc_fence_after();
 #pragma unroll 1

@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
 
   auto flush = [&](int net) {   // whole CTA
     float* out = prm.part + ((int64_t)net * G + cta) * prm.p_stride;
+    NBM_CHECK(((int64_t)net * G + cta + 1) * prm.p_stride <= prm.part_len);
     tc::tc_fence_after();
     {  // dW_l[o][i] from TMEM (o = lane)
       const int q = warp & 3, j = warp >> 2, o = q * 32 + lane;

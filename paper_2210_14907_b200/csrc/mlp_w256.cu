@@ -92,6 +92,7 @@ __device__ __forceinline__ float tsum(float (&v)[32], int lane) {   // warp tran
   return v[0];
 }
 __device__ __forceinline__ void sts4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  tc::check_smem(a, 16);
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 __device__ __forceinline__ void red4(float* p, float a, float b, float c, float d) {
@@ -381,6 +382,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   auto sg_add = [&](int v, int c, float x) { atomicAdd(&sSG[v * W + c * 32 + lane], x); };
   double lossAcc = 0.0;
   float* rep = P.rep + (int64_t)(q % P.nrep) * 2 * prm.p_stride;
+  NBM_CHECK((int64_t)(q % P.nrep + 1) * 2 * prm.p_stride <= prm.rep_len);
+  NBM_CHECK((int64_t)(blockIdx.x + 1) * L::kScr * ACT <= prm.hscr_len && (int64_t)(2 * q + 2) * L::kScr * ACT <= prm.hscr_len);
   bool pend = false;   // TMEM [256,512) holds an unflushed dW
   int pendNet = 0, pendL = 2;
 
@@ -390,6 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1) k_mlp_w
   // k0..k1-1: the thread's column chunks to flush (the forward spreads dW_2's flush over GEMMs)
   auto flush_dw_part = [&](int k0, int k1) {
     float* out = rep + (int64_t)pendNet * prm.p_stride + L::tWl(pendL) + (int64_t)(kB * rank + row) * 4;
+    NBM_CHECK(pendNet < 2 && (int64_t)(W / 4 - 1) * W * 4 + (kB * rank + row) * 4 + 4 <= (int64_t)W * W);   // inside W_pendL
     for (int k = k0; k < k1; ++k) {
       const int c = 2 * cg + k;
       float v[32];

@@ -231,6 +231,12 @@ void fill_common(const nbm_handle* h, MlpParams& p, const float* theta, float hf
   p.p_stride = (h->arch.p_net + 3) & ~3ll;
   p.touched = h->ws.touched;
   p.lpart = h->ws.lpart;
+  p.part_len = 2 * (int64_t)h->ws.grid_mlp * p.p_stride;
+  p.hscr_len = h->ws.hscr_len;
+  p.rep_len = h->ws.rep_len;
+#ifdef NBM_BOUNDS_SELFTEST
+  p.part_len = 0;   // scripts/r2/bounds_check.sh: every partial-slot flush violates, the checks must fire
+#endif
   for (int s = 0; s < kNumSeg; ++s) { p.cnt_slot[s] = kSlotZero; p.start_slot[s] = -1; p.seg.kind[s] = kSegXRows; }
 }
 
@@ -379,8 +385,10 @@ int nbm_create(const nbm_problem* problem, const nbm_arch* arch, int device, int
   w.nrep = urep ? (w256 ? 1 : 16) : 0;
   if (urep && getenv("NBM_W256_REPLICAS")) w.nrep = atoi(getenv("NBM_W256_REPLICAS"));
   ALLOC(w.wimg_b, w256 ? (size_t)2 * nhh * ai.width * ai.width * sizeof(uint16_t) : 16);
-  ALLOC(w.hscr, w256 ? (size_t)w.grid_mlp * (nhh + 2) * 128 * ai.width * 2 : 16);   // parks: NH + 1 tiles per CTA (mlp_w256.cu kScr)
-  ALLOC(w.rep, urep ? (size_t)w.nrep * 2 * ((ai.p_net + 3) & ~3ll) * sizeof(float) : 16);
+  w.hscr_len = w256 ? (int64_t)w.grid_mlp * (nhh + 2) * 128 * ai.width * 2 : 16;   // parks: NH + 1 tiles per CTA (mlp_w256.cu kScr)
+  w.rep_len = urep ? (int64_t)w.nrep * 2 * ((ai.p_net + 3) & ~3ll) : 4;
+  ALLOC(w.hscr, (size_t)w.hscr_len);
+  ALLOC(w.rep, (size_t)w.rep_len * sizeof(float));
   ALLOC(w.wimg32, fw ? (size_t)2 * nhh * 2 * ai.width * ai.width * sizeof(float) : 16);
 #undef ALLOC
   for (size_t i = 0; i < ptrs.size(); ++i) {

@@ -106,6 +106,8 @@ struct Workspace {
   float* wimg32;        // fp32 W >= 128: [2][NH-1][2][W*W] transposed / natural hidden weights
   uint8_t* hscr;        // W = 256: parked activations and G [grid][NH+1][64 KB]
   float* rep;           // bf16 W = 256 / fp32 W >= 128: gradient replicas [nrep][2][p_stride]
+  int64_t hscr_len;     // bytes of hscr
+  int64_t rep_len;      // floats of rep
   int nrep;
   // eval
   float* eval_aux;      // unused placeholder for symmetry
@@ -192,6 +194,9 @@ struct MlpParams {
   double* lpart;             // [grid]
   float* u_out;              // forward-only mode: u_out[item] = u
   const uint16_t* wimg;      // bf16 hidden weights in the tensor-core smem layout [2][NH-1][W*W]
+  // allocation lengths, for the bounds-checked build (NBM_CHECK): part (floats), the K3w parks
+  // (bytes) and the gradient replicas (floats)
+  int64_t part_len, hscr_len, rep_len;
 };
 cudaError_t launch_mlp_fp32(int width, int n_hidden, int act, bool train, bool stable, const MlpParams& p, int grid,
                             cudaStream_t s);

@@ -3,6 +3,8 @@
 #pragma once
 #include <stdint.h>
 
+#include "tc_ptx.cuh"   // check_smem (bounds-checked builds)
+
 namespace nbm {
 namespace epi {
 
@@ -66,9 +68,11 @@ __device__ __forceinline__ void warp_transpose_sum16(float (&v)[32], int lane, f
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  tc::check_smem(addr, 16);
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 __device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+  tc::check_smem(addr, 16);
   asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr) : "memory");
 }
 

@@ -3,6 +3,9 @@
 // matrix descriptors.  Written for this library (no CUTLASS/CuTe dependency).
 #pragma once
 #include <stdint.h>
+#ifdef NBM_BOUNDS
+#include <cstdio>
+#endif
 
 namespace nbm {
 namespace tc {
@@ -12,6 +15,38 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // ---- mbarrier ----
+// ---- bounds-checked build (-DNBM_BOUNDS, scripts/r2/bounds_check.sh): the sanitizer substitute.
+// Every shared-memory address passed to the helpers below (vector loads/stores, bulk copies, MMA
+// descriptors) must lie inside the launch's dynamic shared memory, every TMEM address inside 128
+// lanes x 512 columns; kernels add their own global-range checks with NBM_CHECK.  A violation
+// prints its site and traps (the launch fails with cudaErrorLaunchFailure). ----
+#ifdef NBM_BOUNDS
+static __device__ __noinline__ void nbm_bounds_fail(const char* file, int line) {
+  printf("NBM_BOUNDS violation %s:%d block %d thread %d\n", file, line, (int)blockIdx.x, (int)threadIdx.x);
+  __trap();
+}
+#define NBM_CHECK(c)                                   \
+  do {                                                 \
+    if (!(c)) ::nbm::tc::nbm_bounds_fail(__FILE__, __LINE__); \
+  } while (0)
+__device__ __forceinline__ void check_smem(uint32_t addr, uint32_t bytes) {
+  extern __shared__ __align__(16) uint8_t nbm_dyn_smem[];
+  uint32_t sz;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(sz));
+  const uint32_t base = smem_u32(nbm_dyn_smem);
+  NBM_CHECK(addr >= base && addr + bytes <= base + sz);
+}
+__device__ __forceinline__ void check_tmem(uint32_t taddr, uint32_t cols) {
+  NBM_CHECK((taddr >> 16) < 128u && (taddr & 0xFFFFu) + cols <= 512u);
+}
+#else
+#define NBM_CHECK(c) \
+  do {               \
+  } while (0)
+__device__ __forceinline__ void check_smem(uint32_t, uint32_t) {}
+__device__ __forceinline__ void check_tmem(uint32_t, uint32_t) {}
+#endif
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -35,6 +70,7 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 }
 // TMA 1-D bulk copy global -> shared, completion signalled on `bar` (complete_tx)
 __device__ __forceinline__ void bulk_copy_g2s(uint32_t dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  check_smem(dst_smem, bytes);
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst_smem),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
@@ -42,6 +78,7 @@ __device__ __forceinline__ void bulk_copy_g2s(uint32_t dst_smem, const void* src
 
 // TMA bulk reduction shared -> global: dst[i] += src[i] (f32), tracked by bulk groups
 __device__ __forceinline__ void bulk_reduce_add_f32(void* gdst, uint32_t src_smem, uint32_t bytes) {
+  check_smem(src_smem, bytes);
   asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gdst),
                "r"(src_smem), "r"(bytes)
                : "memory");
@@ -127,6 +164,7 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
 // 16 bytes, 128 contiguous bytes each).  lbo / sbo in bytes (leading = K-direction core
 // stride for K-major and MN-major alike in this layout; stride = the other direction).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  check_smem(saddr, 128);   // (the start core matrix; the extent depends on the instruction)
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
@@ -136,6 +174,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 
 // ---- TMEM <-> registers: 32 lanes x 32 columns of 32 bit, one row per thread ----
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  check_tmem(taddr, 32);
   uint32_t r[32];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
@@ -156,6 +195,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 // threads 0-15 read lanes taddr.lane + 0..15 at columns [c, c+32), threads 16-31 the same lanes
 // at [c+32, c+64) (scripts/r2/m64_probe.cu).
 __device__ __forceinline__ void tmem_ld16x2(uint32_t taddr, float (&v)[32]) {
+  check_tmem(taddr, 32);
   uint32_t r[32];
   asm volatile(
       "tcgen05.ld.sync.aligned.16x32bx2.x32.b32 "
@@ -171,6 +211,7 @@ __device__ __forceinline__ void tmem_ld16x2(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_st16x2(uint32_t taddr, const float (&v)[32]) {
+  check_tmem(taddr, 32);
   asm volatile(
       "tcgen05.st.sync.aligned.16x32bx2.x32.b32 [%0], 32, "
       "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -188,6 +229,7 @@ __device__ __forceinline__ void tmem_st16x2(uint32_t taddr, const float (&v)[32]
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  check_tmem(taddr, 16);
   uint32_t r[16];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -201,6 +243,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  check_tmem(taddr, 32);
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
       "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -221,6 +264,7 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
 }
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  check_tmem(taddr, 16);
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
       "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
@@ -236,6 +280,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
 
 // 16 columns of 32-bit raw words (e.g. packed bf16 pairs) between TMEM and registers
 __device__ __forceinline__ void tmem_ld16u(uint32_t taddr, uint32_t (&r)[16]) {
+  check_tmem(taddr, 16);
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -245,6 +290,7 @@ __device__ __forceinline__ void tmem_ld16u(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t (&r)[16]) {
+  check_tmem(taddr, 16);
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
       "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
@@ -281,6 +327,7 @@ __device__ __forceinline__ void arrive_remote(uint64_t* bar, uint32_t cta) {
 __device__ __forceinline__ void arrive_leader(uint64_t* bar) { arrive_remote(bar, 0); }
 // TMA 1-D bulk copy shared -> global, tracked by bulk groups
 __device__ __forceinline__ void bulk_copy_s2g(void* gdst, uint32_t src_smem, uint32_t bytes) {
+  check_smem(src_smem, bytes);
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(src_smem), "r"(bytes)
                : "memory");
 }
