@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_mlp_fp32(const MlpPara
     // ---- gather the tile's items and rows (x, aux) ----
     const int* items = prm.seg.items[seg] + segStart[seg];
     if (tid < per) {
-      int it = tid < nvalid ? items[first + tid] : -1;
+      int it = tid < nvalid ? item_at(prm.seg, seg, items, first + tid) : -1;
       sItem[tid] = it;
       float a = 0.0f;
       if (it >= 0) a = prm.aux_by_item[seg] ? prm.seg.aux[seg][it] : prm.seg.aux[seg][segStart[seg] + first + tid];

@@ -560,13 +560,13 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
     const int nv = min(pr, segCnt[sg] - fst);
     const int* its = prm.seg.items[sg] + segStart[sg];
     if (tid < pr && tid < nv) {
-      f.item = its[fst + tid];
+      f.item = item_at(prm.seg, sg, its, fst + tid);
       f.aux = prm.aux_by_item[sg] ? prm.seg.aux[sg][f.item] : prm.seg.aux[sg][segStart[sg] + fst + tid];
     }
     if (STAB && knd == kSegStencil) {   // row 8k + jr: x, h e_1..3 (P_d), 0 (Q_d, pad)
       const int k = tid >> 3, jr = tid & 7;
       if (k < nv && jr == 0) {
-        const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + k];
+        const float* src = prm.seg.src[sg] + 3 * (int64_t)item_at(prm.seg, sg, its, fst + k);
         f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
       } else if (k < nv && jr < 4) {
         if (jr == 1) f.x0 = prm.h; else if (jr == 2) f.x1 = prm.h; else f.x2 = prm.h;
@@ -574,7 +574,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
     } else if (knd == kSegStencil) {
       const int j = tid / kTPT, p = tid - j * kTPT;
       if (j < 7 && p < nv) {
-        const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + p];
+        const float* src = prm.seg.src[sg] + 3 * (int64_t)item_at(prm.seg, sg, its, fst + p);
         f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
         if (j > 0) {   // arms +x, -x, +y, -y, +z, -z (exact on the lattice)
           const float hs = (j & 1) ? prm.h : -prm.h;
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(TcLayout<W, NH, ACT, P, tc_stage_cols<W, STAB>
         }
       }
     } else if (tid < nv) {
-      const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + tid];
+      const float* src = prm.seg.src[sg] + 3 * (int64_t)item_at(prm.seg, sg, its, fst + tid);
       f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
     }
     return f;

@@ -358,13 +358,13 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
     const int nv = min(pr, segCnt[sg] - fst);
     const int* its = prm.seg.items[sg] + segStart[sg];
     if (th < pr && th < nv) {
-      f.item = its[fst + th];
+      f.item = item_at(prm.seg, sg, its, fst + th);
       f.aux = prm.aux_by_item[sg] ? prm.seg.aux[sg][f.item] : prm.seg.aux[sg][segStart[sg] + fst + th];
     }
     if (knd == kSegStencil) {
       const int j = th / kHP, p = th - j * kHP;
       if (j < 7 && p < nv) {
-        const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + p];
+        const float* src = prm.seg.src[sg] + 3 * (int64_t)item_at(prm.seg, sg, its, fst + p);
         f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
         if (j > 0) {   // arms +x, -x, +y, -y, +z, -z (exact on the lattice)
           const float hs = (j & 1) ? prm.h : -prm.h;
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(HLayout<W, NH>::THREADS, HLayout<W, NH>::MINB)
         }
       }
     } else if (th < nv) {
-      const float* src = prm.seg.src[sg] + 3 * (int64_t)its[fst + th];
+      const float* src = prm.seg.src[sg] + 3 * (int64_t)item_at(prm.seg, sg, its, fst + th);
       f.x0 = src[0]; f.x1 = src[1]; f.x2 = src[2];
     }
     return f;

@@ -542,6 +542,7 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
     pa.cnt_slot[k] = 12 + k;
     pa.seg.items[k] = w.xlist + (int64_t)k * 7 * w.xcap;
     pa.seg.src[k] = w.xrow_x;
+    pa.seg.src_n[k] = 7 * w.xcap;
     pa.seg.aux[k] = w.xrow_cot;
     pa.aux_by_item[k] = 1;
   }
@@ -563,6 +564,7 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
     pm.start_slot[s0] = kNumCls + kClsUnxMinus + side;
     pm.seg.items[s0] = w.list;
     pm.seg.src[s0] = pts_dev;
+    pm.seg.src_n[s0] = n;
     pm.seg.aux[s0] = w.list_aux;
     double bs = P.beta[side], d = side ? dpl : dm;
     pm.seg.chat[s0] = (float)((-bs / (hd * hd)) / d);
@@ -572,6 +574,7 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
     pm.cnt_slot[s0 + 1] = 12 + k;
     pm.seg.items[s0 + 1] = w.xlist + (int64_t)k * 7 * w.xcap;
     pm.seg.src[s0 + 1] = w.xrow_x;
+    pm.seg.src_n[s0 + 1] = 7 * w.xcap;
     pm.seg.aux[s0 + 1] = w.xrow_cot;
     pm.aux_by_item[s0 + 1] = 1;
     pm.seg.kind[s0 + 2] = kSegBRows;
@@ -580,6 +583,7 @@ int loss_grad_level(nbm_handle* h, const float* theta_dev, const float* pts_dev,
     pm.start_slot[s0 + 2] = kNumCls + kClsBndMinus + side;
     pm.seg.items[s0 + 2] = w.list;
     pm.seg.src[s0 + 2] = bpts_dev;
+    pm.seg.src_n[s0 + 2] = nb;
     pm.seg.aux[s0 + 2] = w.list_aux;
     pm.seg.a[s0 + 2] = (float)(2.0 * P.lambda_b / nbg);
   }
@@ -677,6 +681,7 @@ int nbm_eval(nbm_handle* h, const float* theta_dev, const float* pts_dev, int64_
     p.start_slot[k] = kNumCls + kClsBndMinus + k;
     p.seg.items[k] = w.list;
     p.seg.src[k] = pts_dev;
+    p.seg.src_n[k] = n;
     p.seg.aux[k] = w.list_aux;
   }
   p.u_out = u_dev;

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include "bounds.cuh"
+
 #include "../../include/nbm.h"
 
 namespace nbm {
@@ -66,11 +68,19 @@ struct SegTable {
   const int* count[kNumSeg];   // device pointer to the item count
   const int* items[kNumSeg];   // item list (indices into src)
   const float* src[kNumSeg];   // AoS [][3] coordinates the items index
+  int64_t src_n[kNumSeg];      // rows of src (bounds-checked builds: every item < src_n)
   const float* aux[kNumSeg];   // per-list-position scalar (rhs_hat / g / cotangent)
   float a[kNumSeg];            // boundary: 2 lambda_b / N_b,global
   float chat[kNumSeg];         // stencil: arm coefficient / diagonal (uncrossed row)
   float ccen[kNumSeg];         // stencil, stable form (G27): k / diagonal = 1 + 6 chat, in fp64
 };
+
+// item `pos` of a segment's list, range-checked in bounds-checked builds
+__device__ __forceinline__ int item_at(const SegTable& t, int sg, const int* its, int pos) {
+  const int it = its[pos];
+  NBM_CHECK(it >= 0 && it < t.src_n[sg]);
+  return it;
+}
 
 struct Workspace {
   int64_t cap;          // max points per call (interior and boundary each)

@@ -3,9 +3,8 @@
 // matrix descriptors.  Written for this library (no CUTLASS/CuTe dependency).
 #pragma once
 #include <stdint.h>
-#ifdef NBM_BOUNDS
-#include <cstdio>
-#endif
+
+#include "bounds.cuh"
 
 namespace nbm {
 namespace tc {
@@ -21,14 +20,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // lanes x 512 columns; kernels add their own global-range checks with NBM_CHECK.  A violation
 // prints its site and traps (the launch fails with cudaErrorLaunchFailure). ----
 #ifdef NBM_BOUNDS
-static __device__ __noinline__ void nbm_bounds_fail(const char* file, int line) {
-  printf("NBM_BOUNDS violation %s:%d block %d thread %d\n", file, line, (int)blockIdx.x, (int)threadIdx.x);
-  __trap();
-}
-#define NBM_CHECK(c)                                   \
-  do {                                                 \
-    if (!(c)) ::nbm::tc::nbm_bounds_fail(__FILE__, __LINE__); \
-  } while (0)
 __device__ __forceinline__ void check_smem(uint32_t addr, uint32_t bytes) {
   extern __shared__ __align__(16) uint8_t nbm_dyn_smem[];
   uint32_t sz;
@@ -40,9 +31,6 @@ __device__ __forceinline__ void check_tmem(uint32_t taddr, uint32_t cols) {
   NBM_CHECK((taddr >> 16) < 128u && (taddr & 0xFFFFu) + cols <= 512u);
 }
 #else
-#define NBM_CHECK(c) \
-  do {               \
-  } while (0)
 __device__ __forceinline__ void check_smem(uint32_t, uint32_t) {}
 __device__ __forceinline__ void check_tmem(uint32_t, uint32_t) {}
 #endif

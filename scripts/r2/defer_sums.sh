@@ -1,4 +1,5 @@
 # K3w: w_o / b_NH column sums deferred under the dH_NH GEMM (tooling): bench c4 x2 + W = 256 tests
+# (the change is not in the tree: measured slower and reverted)
 mkdir -p gpurun_out/r2
 for i in 1 2; do
 timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-secondary --steps 20 > gpurun_out/r2/ds_bench.log 2>&1
