@@ -4,7 +4,8 @@ side of the 32-sphere union the loss terms are (1/N) sum_outside (sin(x+y+z) h^2
 inside (f- = 0), and the mean of sin^2 over boundary points outside the union (P:40-41, S:256,
 S:267, G2, G12, G14); the only non-zero gradient entry is the outer network's output bias,
 -(2 / N_b) sum sin(x_b + y_b + z_b) (W_o = 0 blocks every other path; the uncrossed row sums
-c_0 + sum_j c_j vanish).  Each term is checked on its own (the interior term is ~1e-12).  Kernels: K3w
+c_0 + sum_j c_j vanish).  Each term is checked on its own (the interior term is ~1e-12), in the
+direct and the stable stencil form.  Kernels: K3w
 (config 4's 3-256^4-1 bf16), K3h / K3t (W = 128 / 64 bf16), K3f / K3fw (fp32).  Bars: loss 2e-5
 relative (fp32 sources), gradient 2e-5 of the output-bias entry."""
 import numpy as np
@@ -18,15 +19,25 @@ import _zero_theta
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("sizes,prec", [
-    ([3, 256, 256, 256, 256, 1], inputs.PREC_BF16),   # K3w (config 4)
-    ([3, 128, 128, 128, 128, 1], inputs.PREC_BF16),   # K3h
-    ([3, 64, 64, 64, 64, 1], inputs.PREC_BF16),       # K3t
-    ([3, 64, 64, 64, 1], inputs.PREC_FP32),           # K3f
-    ([3, 128, 128, 1], inputs.PREC_FP32),             # K3fw
+D, S = inputs.STENCIL_DIRECT, inputs.STENCIL_STABLE
+
+
+@pytest.mark.parametrize("sizes,prec,stencil", [
+    ([3, 256, 256, 256, 256, 1], inputs.PREC_BF16, D),   # K3w (config 4)
+    ([3, 128, 128, 128, 128, 1], inputs.PREC_BF16, D),   # K3h
+    ([3, 64, 64, 64, 64, 1], inputs.PREC_BF16, D),       # K3t
+    ([3, 64, 64, 64, 1], inputs.PREC_FP32, D),           # K3f
+    ([3, 128, 128, 1], inputs.PREC_FP32, D),             # K3fw
+    # the stable stencil form (G27): every propagated difference is 0 at theta = 0
+    ([3, 256, 256, 256, 256, 1], inputs.PREC_BF16, S),   # K3w<STAB>
+    ([3, 128, 128, 128, 128, 1], inputs.PREC_BF16, S),   # K3t<STAB> W = 128
+    ([3, 64, 64, 64, 64, 1], inputs.PREC_BF16, S),       # K3t<STAB> W = 64
+    ([3, 64, 64, 64, 1], inputs.PREC_FP32, S),           # K3f<STAB>
+    ([3, 128, 128, 1], inputs.PREC_FP32, S),             # K3fw<STAB>
 ])
-def test_config4_zero_theta_closed_form(sizes, prec):
+def test_config4_zero_theta_closed_form(sizes, prec, stencil):
     cfg, pts, b, h, r, rb, inside = _zero_theta.case_c4(sizes, prec)
+    cfg["stencil"] = stencil
     assert inside.sum() > 50 and (~inside).sum() > 1000 and len(b) > 400
     s = nbm.Solver(cfg, 0, max_points=len(pts))
     theta = torch.zeros(s.P, dtype=torch.float32, device="cuda")
